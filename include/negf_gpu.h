@@ -1,0 +1,161 @@
+/* negf_gpu.h -- C ABI of the B200 HSC selected-inversion path.
+ *
+ * Drop-in for the per-energy HSC solve of the reference C++ library
+ * (/root/reference/proj).  The reference has no C ABI and no plugin
+ * mechanism; each entry point below names the C++ interface it replaces:
+ *
+ *   negf_plan_create      build_tree            proj/src/run.cpp:123-133
+ *                         nested_dissection     proj/include/negf/partition.hpp:84-87
+ *                         (+ the structural half of group_by_partition
+ *                          block.hpp:61-63 and hsc_fold hsc.hpp:65-66)
+ *   negf_plan_tree        SeparatorTree accessors partition.hpp:19-68
+ *   negf_plan_ledger      FlopLedger of hsc_fold + hsc_gless dense.hpp:69-82
+ *   negf_gpu_create       (new) device arena + schedule upload, one per GPU
+ *   negf_gpu_solve_batch  solve_energy's HSC branch, batched over energies
+ *                         proj/src/run.cpp:141-192: assemble_system
+ *                         block.cpp:123-161 -> hsc_fold hsc.cpp:447-534 ->
+ *                         hsc_gless hsc.cpp:552-577 -> GreensDiagonal
+ *                         flattening block.cpp:163-205 -> the energy sum of
+ *                         electron_density observables.cpp:58-93
+ *   negf_gpu_density      electron_density's result (before the caller's
+ *                         geometric scaling, run.cpp:291-292)
+ *   negf_gpu_nccl_*       (new) the one cross-GPU exchange: allreduce of the
+ *                         energy-partial density over NCCL
+ *
+ * Conventions: complex values are interleaved (re, im) float64 -- the layout
+ * of std::complex<double>; all pointers are caller-owned host memory unless
+ * the name says _device; calls on one handle are not thread-safe (one host
+ * thread or one process per GPU, like the reference's per-thread energy
+ * solves).  Every call returns a NEGF_* status code and, when
+ * `st` is non-null, fills it.  Codes mirror proj/include/negf/errors.hpp.
+ */
+#ifndef NEGF_GPU_H
+#define NEGF_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  NEGF_OK = 0,
+  NEGF_SINGULAR_BLOCK = 1,       /* SingularBlock (errors.hpp:36-42)        */
+  NEGF_NON_SKEW_HERMITIAN = 2,   /* NonSkewHermitianInput (errors.hpp:61-65)*/
+  NEGF_CONTRACT_VIOLATION = 3,   /* ContractViolation (errors.hpp:27-31)    */
+  NEGF_CUDA_ERROR = 4,
+  NEGF_NCCL_ERROR = 5,
+  NEGF_OUT_OF_MEMORY = 6,
+  NEGF_CONFIG_ERROR = 7,         /* ConfigError (errors.hpp:21-25)          */
+  NEGF_PARTITION_VIOLATION = 8,  /* PartitionViolation (errors.hpp:44-53)   */
+  NEGF_RESIDUAL_TOO_LARGE = 9,   /* ResidualTooLarge (errors.hpp:67-71)     */
+  NEGF_INTERNAL = 10
+};
+
+typedef struct {
+  int code;
+  int energy_index; /* lowest failing energy index (run.cpp:258-262), or -1 */
+  int cluster;      /* cluster being eliminated (SingularBlock), or -1      */
+  int pivot;        /* pivot index within the block (SingularBlock), or -1  */
+  int dof;          /* offending dof (ResidualTooLarge), or -1              */
+  char msg[256];
+} negf_status;
+
+/* Problem description: the inputs of build_tree/solve_energy.
+ * A(E) = E*I - H - Sigma^r(E)   (assemble_system, block.cpp:123-161)
+ * Sigma^r(E) and Sigma^<(E) have fixed patterns; their values are supplied
+ * per energy in pattern order.  Contacts are dense sub-blocks of these
+ * patterns, the phonon self-energy their diagonal entries (device.cpp). */
+typedef struct {
+  int n_dofs;
+  int64_t h_nnz;
+  const int32_t* h_rows;
+  const int32_t* h_cols;
+  const double* h_vals;          /* complex, h_nnz                          */
+  int64_t sr_nnz;                /* Sigma^r pattern                         */
+  const int32_t* sr_rows;
+  const int32_t* sr_cols;
+  int64_t sl_nnz;                /* Sigma^< pattern (cluster-block-diagonal)*/
+  const int32_t* sl_rows;
+  const int32_t* sl_cols;
+  const double* coords;          /* 2*n_dofs (x, y) or NULL: BFS surrogate  */
+  int n_groups;                  /* atomic groups (dense contacts)          */
+  const int32_t* group_ptr;      /* n_groups+1                              */
+  const int32_t* group_dofs;
+  int max_leaf;
+  /* Optional explicit tree instead of nested dissection (fixture tests). */
+  int n_tree_clusters;           /* 0 = use nested dissection               */
+  const int32_t* tree_parent;    /* n_tree_clusters (-1 = root)             */
+  const int32_t* tree_ptr;       /* n_tree_clusters+1                       */
+  const int32_t* tree_dofs;
+} negf_problem;
+
+typedef struct negf_plan negf_plan;
+typedef struct negf_gpu negf_gpu;
+
+typedef struct {
+  int n_dofs, n_clusters, levels, root, max_block;
+  int64_t arena_bytes_per_energy;
+  int64_t ref_fold_mul, ref_fold_inv;    /* reference ledger, per energy */
+  int64_t ref_gless_mul, ref_gless_inv;
+  double exec_cmul;                      /* executed complex MACs / energy */
+  double exec_inv_cmul;
+  int n_ops, n_gemm_tasks, n_gemm_tiles, n_inv_tasks;
+} negf_plan_info;
+
+int negf_plan_create(const negf_problem* p, negf_plan** out, negf_status* st);
+int negf_plan_info_get(const negf_plan* p, negf_plan_info* info);
+/* Tree export: parent[nc], level[nc], dof_ptr[nc+1], dofs[n] (ascending per
+ * cluster), fold_order[nc-1].  Any pointer may be NULL. */
+int negf_plan_tree(const negf_plan* p, int32_t* parent, int32_t* level, int32_t* dof_ptr,
+                   int32_t* dofs, int32_t* fold_order);
+/* Fill sets S(i) (the Psi lists, nearest ancestor first): ptr[nc+1], ids. */
+int negf_plan_fill(const negf_plan* p, int32_t* ptr, int32_t* ids);
+void negf_plan_destroy(negf_plan* p);
+
+/* Device side: allocates the per-energy arenas for up to max_energy_batch
+ * energies (0 = as many as fit in 85% of free HBM) on `device`. */
+int negf_gpu_create(const negf_plan* plan, int device, int max_energy_batch, negf_gpu** out,
+                    negf_status* st);
+int negf_gpu_batch_capacity(const negf_gpu* g);
+
+/* Solves n_energies energy points (chunked internally by the batch
+ * capacity).  Host inputs:
+ *   energies[nE], weights[nE] (trapezoid weights, observables.cpp:14-32),
+ *   sigma_r[nE][sr_nnz], sigma_lesser[nE][sl_nnz] (complex),
+ *   first_energy_index: global index of energies[0] for error reports.
+ * Host outputs (nullable): gr_diag[nE][n], gless_diag[nE][n] (complex, per
+ * dof in global order).  The weighted Im G^< sum is accumulated on device
+ * into the handle's density (negf_gpu_density). */
+int negf_gpu_solve_batch(negf_gpu* g, int n_energies, const double* energies,
+                         const double* weights, const double* sigma_r,
+                         const double* sigma_lesser, int first_energy_index, double* gr_diag,
+                         double* gless_diag, negf_status* st);
+/* Same, with every input and output already resident in device memory
+ * (d_gr/d_gless nullable).  Runs on the handle's stream; no host sync unless
+ * `sync` is nonzero (errors are then reported by negf_gpu_check). */
+int negf_gpu_solve_batch_device(negf_gpu* g, int n_energies, const double* d_energies,
+                                const double* d_weights, const double* d_sigma_r,
+                                const double* d_sigma_lesser, int first_energy_index,
+                                double* d_gr, double* d_gless, int sync, negf_status* st);
+int negf_gpu_check(negf_gpu* g, negf_status* st);
+/* density_out[n] = (1/2pi) sum_k w_k Im G^<_jj(E_k) over all solved energies
+ * (observables.cpp:71-91).  reset != 0 zeroes the accumulator afterwards. */
+int negf_gpu_density(negf_gpu* g, double* density_out, int reset, negf_status* st);
+void* negf_gpu_stream(negf_gpu* g);       /* cudaStream_t of the handle */
+void* negf_gpu_density_device(negf_gpu* g); /* double[n] accumulator (unscaled) */
+/* Kernel launches issued by the last solve call (ours only). */
+int64_t negf_gpu_last_launches(const negf_gpu* g);
+void negf_gpu_destroy(negf_gpu* g);
+
+/* NCCL: one communicator per handle, bootstrapped by the caller (e.g. a
+ * torch.distributed broadcast of the 128-byte id). */
+int negf_nccl_unique_id(char id_out[128], negf_status* st);
+int negf_gpu_nccl_init(negf_gpu* g, const char id[128], int nranks, int rank, negf_status* st);
+/* In-place sum of the unscaled density accumulators across ranks. */
+int negf_gpu_allreduce_density(negf_gpu* g, negf_status* st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEGF_GPU_H */

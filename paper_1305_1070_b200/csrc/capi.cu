@@ -1,0 +1,537 @@
+// C ABI of the B200 HSC path (include/negf_gpu.h): host plan handles, device
+// handles, the per-batch schedule replay and the NCCL density exchange.
+#include "negf_gpu.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+#include "tree.hpp"
+
+using namespace negfb;
+
+struct negf_plan {
+  Plan plan;
+};
+
+namespace {
+
+// --- NCCL, resolved at run time so the process reuses whichever libnccl the
+// framework (torch) already loaded.
+typedef int (*nccl_get_id_t)(void*);
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_destroy_t)(void*);
+typedef const char* (*nccl_err_t)(int);
+struct NcclApi {
+  bool ok = false;
+  nccl_get_id_t get_id = nullptr;
+  void* init = nullptr;
+  nccl_allreduce_t allreduce = nullptr;
+  nccl_destroy_t destroy = nullptr;
+  nccl_err_t err = nullptr;
+};
+struct NcclId {
+  char internal[128];
+};
+typedef int (*nccl_init_by_value_t)(void**, int, NcclId, int);
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.get_id = reinterpret_cast<nccl_get_id_t>(dlsym(h, "ncclGetUniqueId"));
+  api.init = dlsym(h, "ncclCommInitRank");
+  api.allreduce = reinterpret_cast<nccl_allreduce_t>(dlsym(h, "ncclAllReduce"));
+  api.destroy = reinterpret_cast<nccl_destroy_t>(dlsym(h, "ncclCommDestroy"));
+  api.err = reinterpret_cast<nccl_err_t>(dlsym(h, "ncclGetErrorString"));
+  api.ok = api.get_id && api.init && api.allreduce && api.destroy;
+  return api;
+}
+
+int set_status(negf_status* st, int code, const std::string& msg, int energy = -1, int cluster = -1,
+               int pivot = -1, int dof = -1) {
+  if (st) {
+    st->code = code;
+    st->energy_index = energy;
+    st->cluster = cluster;
+    st->pivot = pivot;
+    st->dof = dof;
+    std::snprintf(st->msg, sizeof st->msg, "%s", msg.c_str());
+  }
+  return code;
+}
+
+int ok(negf_status* st) { return set_status(st, NEGF_OK, ""); }
+
+struct CudaFail {
+  int code;
+  std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    const int code = (e == cudaErrorMemoryAllocation) ? NEGF_OUT_OF_MEMORY : NEGF_CUDA_ERROR;
+    throw CudaFail{code, std::string(what) + ": " + cudaGetErrorString(e)};
+  }
+}
+
+template <class T>
+T* dev_upload(const std::vector<T>& v, std::vector<void*>& owned) {
+  if (v.empty()) return nullptr;
+  T* p = nullptr;
+  ck(cudaMalloc(&p, sizeof(T) * v.size()), "cudaMalloc");
+  owned.push_back(p);
+  ck(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "upload");
+  return p;
+}
+
+template <class T>
+T* dev_alloc(size_t count, std::vector<void*>& owned) {
+  if (count == 0) count = 1;
+  T* p = nullptr;
+  ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
+  owned.push_back(p);
+  return p;
+}
+
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+}  // namespace
+
+struct negf_gpu {
+  const Plan* plan = nullptr;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> owned;
+  int capacity = 1;
+  double2* arena = nullptr;
+  double2* d_template = nullptr;
+  int64_t* d_diag_pos = nullptr;
+  int64_t *d_sr_pos = nullptr, *d_sl_pos = nullptr, *d_gr_pos = nullptr, *d_gl_pos = nullptr;
+  int *d_sr_ptr = nullptr, *d_sr_src = nullptr, *d_sl_ptr = nullptr, *d_sl_src = nullptr;
+  int *d_sl_partner = nullptr, *d_sl_cidx = nullptr, *d_seeded = nullptr;
+  GemmTask* d_tasks = nullptr;
+  GemmTerm* d_terms = nullptr;
+  GemmTile* d_tiles = nullptr;
+  DiagTask* d_diag = nullptr;
+  GemmTerm* d_diag_terms = nullptr;
+  ScaleTask* d_scale = nullptr;
+  InvTask* d_inv = nullptr;
+  // per-batch staging
+  double *d_energies = nullptr, *d_weights = nullptr;
+  double2 *d_sigma_r = nullptr, *d_sigma_l = nullptr, *d_gr = nullptr, *d_gl = nullptr;
+  double* d_density = nullptr;
+  double* d_skew = nullptr;
+  DevStatus* d_status = nullptr;
+  void* comm = nullptr;
+  int64_t launches = 0;
+};
+
+namespace {
+
+void reset_status(negf_gpu* g) {
+  DevStatus h{~0ull, ~0ull, ~0ull};
+  ck(cudaMemcpyAsync(g->d_status, &h, sizeof h, cudaMemcpyHostToDevice, g->stream), "status reset");
+}
+
+// Replays the plan's schedule for one batch (all inputs on device).
+void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double* d_w,
+               const double2* d_sr, const double2* d_sl, double2* d_gr, double2* d_gl) {
+  const Plan& P = *g->plan;
+  BatchArgs b{g->arena, P.arena, nE, e_base};
+  cudaStream_t s = g->stream;
+  int64_t& L = g->launches;
+  launch_assemble(b, P, g->d_template, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr, g->d_sr_src,
+                  static_cast<int64_t>(P.desc.sr_rows.size()), d_sr, g->d_sl_pos, g->d_sl_ptr, g->d_sl_src,
+                  static_cast<int64_t>(P.desc.sl_rows.size()), d_sl, s, L);
+  launch_skew_check(b, d_sl, static_cast<int64_t>(P.desc.sl_rows.size()),
+                    static_cast<int>(P.sl_slot_pos.size()), g->d_sl_ptr, g->d_sl_src, g->d_sl_partner,
+                    g->d_sl_cidx, static_cast<int>(P.seeded_ids.size()), g->d_seeded, g->d_skew,
+                    g->d_status, s, L);
+  for (const Op& op : P.ops) {
+    switch (op.kind) {
+      case K_INVERSE:
+        launch_inverse(b, g->d_inv + op.begin, P.inv_tasks.data() + op.begin, op.count, g->d_status, s, L);
+        break;
+      case K_GEMM:
+        launch_gemm(b, g->d_tasks, g->d_terms, g->d_tiles, op.begin, op.count, s, L);
+        break;
+      case K_DIAG:
+        launch_diag(b, g->d_diag, g->d_diag_terms, op.begin, op.count, s, L);
+        break;
+      default:
+        launch_scale(b, g->d_scale, op.begin, op.count, s, L);
+        break;
+    }
+  }
+  launch_output(b, P.desc.n, g->d_gr_pos, g->d_gl_pos, d_w, d_gr, d_gl, g->d_density, g->d_status, s, L);
+  ck(cudaGetLastError(), "kernel launch");
+}
+
+// Reads the device status and maps it to the reference's precedence: the
+// lowest energy index wins; within one energy the fold's SingularBlock comes
+// before validate_sigma's NonSkewHermitianInput (hsc_fold runs first,
+// run.cpp:164-169); ResidualTooLarge is raised only when every energy solved
+// (electron_density runs after solve_all, run.cpp:285-291).
+int collect(negf_gpu* g, negf_status* st) {
+  DevStatus h;
+  ck(cudaMemcpyAsync(&h, g->d_status, sizeof h, cudaMemcpyDeviceToHost, g->stream), "status read");
+  ck(cudaStreamSynchronize(g->stream), "stream sync");
+  const unsigned long long none = ~0ull;
+  const long long es = h.singular_key == none ? -1 : static_cast<long long>(h.singular_key >> 40);
+  const long long en = h.nonskew_key == none ? -1 : static_cast<long long>(h.nonskew_key >> 32);
+  if (es >= 0 && (en < 0 || es <= en)) {
+    const int fold_pos = static_cast<int>((h.singular_key >> 20) & 0xFFFFF);
+    const int pivot = static_cast<int>(h.singular_key & 0xFFFFF);
+    const Tree& t = g->plan->tree;
+    const int cluster = fold_pos < static_cast<int>(t.fold_order().size()) ? t.fold_order()[fold_pos] : t.root();
+    return set_status(st, NEGF_SINGULAR_BLOCK,
+                      "energy point " + std::to_string(es) + ": inverse: singular pivot " +
+                          std::to_string(pivot) + " in " + std::to_string(t.cluster(cluster).size()) + "x" +
+                          std::to_string(t.cluster(cluster).size()) + " block of cluster " +
+                          std::to_string(cluster),
+                      static_cast<int>(es), cluster, pivot);
+  }
+  if (en >= 0) {
+    const int cluster = static_cast<int>(h.nonskew_key & 0xFFFFFFFFull);
+    return set_status(st, NEGF_NON_SKEW_HERMITIAN,
+                      "energy point " + std::to_string(en) + ": sigma_lesser block of cluster " +
+                          std::to_string(cluster) + " is not skew-Hermitian",
+                      static_cast<int>(en), cluster);
+  }
+  if (h.residual_key != none) {
+    const int e = static_cast<int>(h.residual_key >> 32);
+    const int d = static_cast<int>(h.residual_key & 0xFFFFFFFFull);
+    return set_status(st, NEGF_RESIDUAL_TOO_LARGE,
+                      "G^< diagonal entry has a real part beyond the skew-Hermitian tolerance at "
+                      "energy index " + std::to_string(e) + ", dof " + std::to_string(d),
+                      e, -1, -1, d);
+  }
+  return ok(st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int negf_plan_create(const negf_problem* p, negf_plan** out, negf_status* st) {
+  if (!p || !out) return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
+  try {
+    ProblemDesc d;
+    d.n = p->n_dofs;
+    d.h_rows.assign(p->h_rows, p->h_rows + p->h_nnz);
+    d.h_cols.assign(p->h_cols, p->h_cols + p->h_nnz);
+    d.h_vals.resize(static_cast<size_t>(p->h_nnz));
+    for (int64_t k = 0; k < p->h_nnz; ++k) d.h_vals[k] = cplx(p->h_vals[2 * k], p->h_vals[2 * k + 1]);
+    if (p->sr_nnz) {
+      d.sr_rows.assign(p->sr_rows, p->sr_rows + p->sr_nnz);
+      d.sr_cols.assign(p->sr_cols, p->sr_cols + p->sr_nnz);
+    }
+    if (p->sl_nnz) {
+      d.sl_rows.assign(p->sl_rows, p->sl_rows + p->sl_nnz);
+      d.sl_cols.assign(p->sl_cols, p->sl_cols + p->sl_nnz);
+    }
+    if (p->coords) {
+      d.coords.resize(static_cast<size_t>(p->n_dofs));
+      for (int i = 0; i < p->n_dofs; ++i) d.coords[i] = {p->coords[2 * i], p->coords[2 * i + 1]};
+    }
+    for (int gi = 0; gi < p->n_groups; ++gi)
+      d.atomic_groups.emplace_back(p->group_dofs + p->group_ptr[gi], p->group_dofs + p->group_ptr[gi + 1]);
+    d.max_leaf = p->max_leaf;
+    if (p->n_tree_clusters > 0) {
+      d.explicit_tree = true;
+      d.tree_parent.assign(p->tree_parent, p->tree_parent + p->n_tree_clusters);
+      for (int c = 0; c < p->n_tree_clusters; ++c)
+        d.tree_dofs.emplace_back(p->tree_dofs + p->tree_ptr[c], p->tree_dofs + p->tree_ptr[c + 1]);
+    }
+    auto* h = new negf_plan{build_plan(std::move(d))};
+    *out = h;
+    return ok(st);
+  } catch (const Failure& f) {
+    return set_status(st, f.code, f.what());
+  } catch (const std::exception& e) {
+    return set_status(st, NEGF_INTERNAL, e.what());
+  }
+}
+
+int negf_plan_info_get(const negf_plan* h, negf_plan_info* info) {
+  if (!h || !info) return NEGF_CONTRACT_VIOLATION;
+  const Plan& P = h->plan;
+  info->n_dofs = P.desc.n;
+  info->n_clusters = P.tree.num_clusters();
+  info->levels = P.tree.levels();
+  info->root = P.tree.root();
+  info->max_block = P.max_block;
+  info->arena_bytes_per_energy = P.arena * 16;
+  info->ref_fold_mul = P.ref_fold.multiply_ops;
+  info->ref_fold_inv = P.ref_fold.inverse_ops;
+  info->ref_gless_mul = P.ref_gless.multiply_ops;
+  info->ref_gless_inv = P.ref_gless.inverse_ops;
+  info->exec_cmul = P.exec_cmul;
+  info->exec_inv_cmul = P.exec_inv_cmul;
+  info->n_ops = static_cast<int>(P.ops.size());
+  info->n_gemm_tasks = static_cast<int>(P.gemm_tasks.size());
+  info->n_gemm_tiles = static_cast<int>(P.gemm_tiles.size());
+  info->n_inv_tasks = static_cast<int>(P.inv_tasks.size());
+  return NEGF_OK;
+}
+
+int negf_plan_tree(const negf_plan* h, int32_t* parent, int32_t* level, int32_t* dof_ptr, int32_t* dofs,
+                   int32_t* fold_order) {
+  if (!h) return NEGF_CONTRACT_VIOLATION;
+  const Tree& t = h->plan.tree;
+  int32_t off = 0;
+  for (int c = 0; c < t.num_clusters(); ++c) {
+    const Cluster& cl = t.cluster(c);
+    if (parent) parent[c] = cl.parent;
+    if (level) level[c] = cl.level;
+    if (dof_ptr) dof_ptr[c] = off;
+    if (dofs) std::copy(cl.dofs.begin(), cl.dofs.end(), dofs + off);
+    off += cl.size();
+  }
+  if (dof_ptr) dof_ptr[t.num_clusters()] = off;
+  if (fold_order) std::copy(t.fold_order().begin(), t.fold_order().end(), fold_order);
+  return NEGF_OK;
+}
+
+int negf_plan_fill(const negf_plan* h, int32_t* ptr, int32_t* ids) {
+  if (!h) return NEGF_CONTRACT_VIOLATION;
+  int32_t off = 0;
+  const auto& ci = h->plan.ci;
+  for (size_t c = 0; c < ci.size(); ++c) {
+    if (ptr) ptr[c] = off;
+    if (ids) std::copy(ci[c].S.begin(), ci[c].S.end(), ids + off);
+    off += static_cast<int32_t>(ci[c].S.size());
+  }
+  if (ptr) ptr[ci.size()] = off;
+  return NEGF_OK;
+}
+
+void negf_plan_destroy(negf_plan* p) { delete p; }
+
+int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_gpu** out,
+                    negf_status* st) {
+  if (!hp || !out) return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
+  auto g = std::make_unique<negf_gpu>();
+  try {
+    const Plan& P = hp->plan;
+    g->plan = &P;
+    g->device = device;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking), "stream");
+    auto& o = g->owned;
+    g->d_template = reinterpret_cast<double2*>(dev_upload(P.a_template, o));
+    g->d_diag_pos = dev_upload(P.diag_pos, o);
+    g->d_sr_pos = dev_upload(P.sr_slot_pos, o);
+    g->d_sr_ptr = dev_upload(P.sr_slot_ptr, o);
+    g->d_sr_src = dev_upload(P.sr_slot_src, o);
+    g->d_sl_pos = dev_upload(P.sl_slot_pos, o);
+    g->d_sl_ptr = dev_upload(P.sl_slot_ptr, o);
+    g->d_sl_src = dev_upload(P.sl_slot_src, o);
+    g->d_sl_partner = dev_upload(P.sl_partner, o);
+    g->d_sl_cidx = dev_upload(P.sl_cidx, o);
+    g->d_seeded = dev_upload(P.seeded_ids, o);
+    g->d_gr_pos = dev_upload(P.out_gr_pos, o);
+    g->d_gl_pos = dev_upload(P.out_gl_pos, o);
+    g->d_tasks = dev_upload(P.gemm_tasks, o);
+    g->d_terms = dev_upload(P.gemm_terms, o);
+    g->d_tiles = dev_upload(P.gemm_tiles, o);
+    g->d_diag = dev_upload(P.diag_tasks, o);
+    g->d_diag_terms = dev_upload(P.diag_terms, o);
+    g->d_scale = dev_upload(P.scale_tasks, o);
+    g->d_inv = dev_upload(P.inv_tasks, o);
+    const int n = P.desc.n;
+    const size_t sr = P.desc.sr_rows.size(), sl = P.desc.sl_rows.size();
+    const size_t per_energy = size_t(P.arena) * 16 + (sr + sl) * 16 + size_t(n) * 32 + 16 +
+                              P.seeded_ids.size() * 16;
+    size_t free_b = 0, total_b = 0;
+    ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    int cap = static_cast<int>(std::min<size_t>(size_t(0.85 * double(free_b)) / per_energy, 1 << 20));
+    if (max_energy_batch > 0) cap = std::min(cap, max_energy_batch);
+    if (cap < 1)
+      throw CudaFail{NEGF_OUT_OF_MEMORY, "one energy point needs " + std::to_string(per_energy) +
+                                             " bytes of device memory; " + std::to_string(free_b) + " free"};
+    g->capacity = cap;
+    g->arena = dev_alloc<double2>(size_t(P.arena) * cap, o);
+    g->d_energies = dev_alloc<double>(cap, o);
+    g->d_weights = dev_alloc<double>(cap, o);
+    g->d_sigma_r = dev_alloc<double2>(sr * cap, o);
+    g->d_sigma_l = dev_alloc<double2>(sl * cap, o);
+    g->d_gr = dev_alloc<double2>(size_t(n) * cap, o);
+    g->d_gl = dev_alloc<double2>(size_t(n) * cap, o);
+    g->d_density = dev_alloc<double>(n, o);
+    g->d_skew = dev_alloc<double>(2 * std::max<size_t>(1, P.seeded_ids.size()) * cap, o);
+    g->d_status = dev_alloc<DevStatus>(1, o);
+    ck(cudaMemsetAsync(g->d_density, 0, sizeof(double) * n, g->stream), "memset");
+    reset_status(g.get());
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    *out = g.release();
+    return ok(st);
+  } catch (const CudaFail& f) {
+    for (void* p : g->owned) cudaFree(p);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    return set_status(st, f.code, f.msg);
+  }
+}
+
+int negf_gpu_batch_capacity(const negf_gpu* g) { return g ? g->capacity : 0; }
+
+int negf_gpu_solve_batch(negf_gpu* g, int nE, const double* energies, const double* weights,
+                         const double* sigma_r, const double* sigma_lesser, int first, double* gr,
+                         double* gless, negf_status* st) {
+  if (!g || nE < 0 || (nE > 0 && (!energies || !weights)))
+    return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
+  try {
+    const Plan& P = *g->plan;
+    const size_t sr = P.desc.sr_rows.size(), sl = P.desc.sl_rows.size();
+    const int n = P.desc.n;
+    if ((sr && !sigma_r) || (sl && !sigma_lesser))
+      return set_status(st, NEGF_CONTRACT_VIOLATION, "self-energy values missing");
+    g->launches = 0;
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    reset_status(g);
+    for (int e0 = 0; e0 < nE; e0 += g->capacity) {
+      const int m = std::min(g->capacity, nE - e0);
+      cudaStream_t s = g->stream;
+      ck(cudaMemcpyAsync(g->d_energies, energies + e0, sizeof(double) * m, cudaMemcpyHostToDevice, s), "h2d");
+      ck(cudaMemcpyAsync(g->d_weights, weights + e0, sizeof(double) * m, cudaMemcpyHostToDevice, s), "h2d");
+      if (sr)
+        ck(cudaMemcpyAsync(g->d_sigma_r, sigma_r + 2 * sr * size_t(e0), 16 * sr * m, cudaMemcpyHostToDevice, s),
+           "h2d");
+      if (sl)
+        ck(cudaMemcpyAsync(g->d_sigma_l, sigma_lesser + 2 * sl * size_t(e0), 16 * sl * m,
+                           cudaMemcpyHostToDevice, s),
+           "h2d");
+      run_batch(g, m, first + e0, g->d_energies, g->d_weights, g->d_sigma_r, g->d_sigma_l,
+                gr ? g->d_gr : nullptr, gless ? g->d_gl : nullptr);
+      if (gr)
+        ck(cudaMemcpyAsync(gr + 2 * size_t(n) * e0, g->d_gr, 16 * size_t(n) * m, cudaMemcpyDeviceToHost, s),
+           "d2h");
+      if (gless)
+        ck(cudaMemcpyAsync(gless + 2 * size_t(n) * e0, g->d_gl, 16 * size_t(n) * m, cudaMemcpyDeviceToHost, s),
+           "d2h");
+      // Stop at the first batch holding a solver failure (its energies are the
+      // lowest failing ones); residual checks are deferred to the end.
+      DevStatus h;
+      ck(cudaMemcpyAsync(&h, g->d_status, sizeof h, cudaMemcpyDeviceToHost, s), "status");
+      ck(cudaStreamSynchronize(s), "sync");
+      if (h.singular_key != ~0ull || h.nonskew_key != ~0ull) break;
+    }
+    return collect(g, st);
+  } catch (const CudaFail& f) {
+    return set_status(st, f.code, f.msg);
+  }
+}
+
+int negf_gpu_solve_batch_device(negf_gpu* g, int nE, const double* d_E, const double* d_w,
+                                const double* d_sr, const double* d_sl, int first, double* d_gr,
+                                double* d_gless, int sync, negf_status* st) {
+  if (!g || nE < 0) return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
+  try {
+    const Plan& P = *g->plan;
+    const size_t sr = P.desc.sr_rows.size(), sl = P.desc.sl_rows.size();
+    const int n = P.desc.n;
+    g->launches = 0;
+    ck(cudaSetDevice(g->device), "cudaSetDevice");
+    reset_status(g);
+    for (int e0 = 0; e0 < nE; e0 += g->capacity) {
+      const int m = std::min(g->capacity, nE - e0);
+      run_batch(g, m, first + e0, d_E + e0, d_w + e0,
+                reinterpret_cast<const double2*>(d_sr) + sr * size_t(e0),
+                reinterpret_cast<const double2*>(d_sl) + sl * size_t(e0),
+                d_gr ? reinterpret_cast<double2*>(d_gr) + size_t(n) * e0 : nullptr,
+                d_gless ? reinterpret_cast<double2*>(d_gless) + size_t(n) * e0 : nullptr);
+    }
+    if (sync) return collect(g, st);
+    return ok(st);
+  } catch (const CudaFail& f) {
+    return set_status(st, f.code, f.msg);
+  }
+}
+
+int negf_gpu_check(negf_gpu* g, negf_status* st) {
+  if (!g) return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
+  try {
+    return collect(g, st);
+  } catch (const CudaFail& f) {
+    return set_status(st, f.code, f.msg);
+  }
+}
+
+int negf_gpu_density(negf_gpu* g, double* out, int reset, negf_status* st) {
+  if (!g || !out) return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
+  try {
+    const int n = g->plan->desc.n;
+    ck(cudaMemcpyAsync(out, g->d_density, sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    if (reset) ck(cudaMemsetAsync(g->d_density, 0, sizeof(double) * n, g->stream), "memset");
+    ck(cudaStreamSynchronize(g->stream), "sync");
+    for (int i = 0; i < n; ++i) out[i] /= kTwoPi;  // observables.cpp:91
+    return ok(st);
+  } catch (const CudaFail& f) {
+    return set_status(st, f.code, f.msg);
+  }
+}
+
+void* negf_gpu_stream(negf_gpu* g) { return g ? g->stream : nullptr; }
+void* negf_gpu_density_device(negf_gpu* g) { return g ? g->d_density : nullptr; }
+int64_t negf_gpu_last_launches(const negf_gpu* g) { return g ? g->launches : 0; }
+
+void negf_gpu_destroy(negf_gpu* g) {
+  if (!g) return;
+  cudaSetDevice(g->device);
+  if (g->comm && nccl().ok) nccl().destroy(g->comm);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  for (void* p : g->owned) cudaFree(p);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g;
+}
+
+int negf_nccl_unique_id(char id_out[128], negf_status* st) {
+  NcclApi& api = nccl();
+  if (!api.ok) return set_status(st, NEGF_NCCL_ERROR, "libnccl.so.2 could not be loaded");
+  NcclId id;
+  const int r = api.get_id(&id);
+  if (r != 0) return set_status(st, NEGF_NCCL_ERROR, api.err ? api.err(r) : "ncclGetUniqueId failed");
+  std::memcpy(id_out, id.internal, 128);
+  return ok(st);
+}
+
+int negf_gpu_nccl_init(negf_gpu* g, const char id[128], int nranks, int rank, negf_status* st) {
+  NcclApi& api = nccl();
+  if (!g) return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
+  if (!api.ok) return set_status(st, NEGF_NCCL_ERROR, "libnccl.so.2 could not be loaded");
+  cudaSetDevice(g->device);
+  NcclId nid;
+  std::memcpy(nid.internal, id, 128);
+  const int r = reinterpret_cast<nccl_init_by_value_t>(api.init)(&g->comm, nranks, nid, rank);
+  if (r != 0) return set_status(st, NEGF_NCCL_ERROR, api.err ? api.err(r) : "ncclCommInitRank failed");
+  return ok(st);
+}
+
+int negf_gpu_allreduce_density(negf_gpu* g, negf_status* st) {
+  NcclApi& api = nccl();
+  if (!g || !g->comm) return set_status(st, NEGF_CONTRACT_VIOLATION, "no NCCL communicator");
+  cudaSetDevice(g->device);
+  const int n = g->plan->desc.n;
+  // ncclFloat64 = 8, ncclSum = 0 (nccl.h)
+  const int r = api.allreduce(g->d_density, g->d_density, size_t(n), 8, 0, g->comm, g->stream);
+  if (r != 0) return set_status(st, NEGF_NCCL_ERROR, api.err ? api.err(r) : "ncclAllReduce failed");
+  if (cudaStreamSynchronize(g->stream) != cudaSuccess)
+    return set_status(st, NEGF_CUDA_ERROR, "sync after allreduce failed");
+  return ok(st);
+}
+
+}  // extern "C"

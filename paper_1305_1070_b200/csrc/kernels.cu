@@ -1,0 +1,636 @@
+// Device kernels of the B200 HSC path.  Complex FP64 throughout
+// (interleaved double2 in HBM, as std::complex<double> in the reference).
+//
+//   k_assemble_*   A(E) = E I - H - Sigma^r(E) into the per-energy block arena
+//                  (assemble_system + group_by_partition, block.cpp:49-82,
+//                  123-161): template copy + diagonal / pattern scatters.
+//   k_inverse_*    batched Gauss-Jordan explicit inverse with row partial
+//                  pivoting and the reference's singular-pivot rule
+//                  |u_kk| <= 1e-13 max|a| (dense.cpp:49-81).
+//   k_gemm         grouped multi-term complex GEMM on FP64 tensor cores
+//                  (mma.sync m8n8k4 f64 = SASS DMMA.8x8x4, the only FP64
+//                  tensor path on sm_100a): every Psi, Schur, G/N/P row and
+//                  diagonal-block update of hsc.cpp is one task of it.
+//   k_diag         diagonal-only dot products for never-referenced clusters.
+//   k_scale        diagonal Sigma^< seeds N = diag(s) conj(G) (hsc.cpp:122-125).
+//   k_output       per-dof diag G^r / G^<, Re-residual guard and the weighted
+//                  energy sum of electron_density (observables.cpp:71-91).
+#include "kernels.hpp"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace negfb {
+
+namespace {
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double cabs2(double2 a) { return hypot(a.x, a.y); }
+__device__ __forceinline__ double2 cinv(double2 a) {
+  // 1/a with scaling against overflow (Smith's algorithm).
+  if (fabs(a.x) >= fabs(a.y)) {
+    const double r = a.y / a.x, d = a.x + a.y * r;
+    return make_double2(1.0 / d, -r / d);
+  }
+  const double r = a.x / a.y, d = a.x * r + a.y;
+  return make_double2(r / d, -1.0 / d);
+}
+
+// ---------------------------------------------------------------------------
+// Assembly
+// ---------------------------------------------------------------------------
+__global__ void k_copy_template(double2* arena, int64_t stride, const double2* __restrict__ tmpl,
+                                int64_t len, int64_t z_begin, int64_t z_end) {
+  double2* a = arena + blockIdx.y * stride;
+  const int64_t step = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += step) a[i] = tmpl[i];
+  for (int64_t i = z_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < z_end; i += step)
+    a[i] = make_double2(0.0, 0.0);
+}
+
+// E on the diagonal and the Sigma^< slots (which live outside the A region).
+__global__ void k_scatter(double2* arena, int64_t stride, int n, const int64_t* __restrict__ diag_pos,
+                          const double* __restrict__ energies, const int64_t* __restrict__ sl_pos, const int* __restrict__ sl_ptr,
+                          const int* __restrict__ sl_src, int sl_slots, int64_t sl_nnz,
+                          const double2* __restrict__ sigma_l) {
+  const int e = blockIdx.y;
+  double2* a = arena + e * stride;
+  const double E = energies[e];
+  const int64_t step = int64_t(gridDim.x) * blockDim.x;
+  const int64_t t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t i = t0; i < n; i += step) a[diag_pos[i]].x += E;
+  const double2* sl = sigma_l + e * sl_nnz;
+  for (int64_t s = t0; s < sl_slots; s += step) {
+    double2 v = make_double2(0.0, 0.0);
+    for (int q = sl_ptr[s]; q < sl_ptr[s + 1]; ++q) v = cadd(v, sl[sl_src[q]]);
+    a[sl_pos[s]] = v;
+  }
+}
+
+// Sigma^r slots: ordered after k_scatter (a diagonal slot hits an entry that
+// k_scatter has just shifted by E).
+__global__ void k_scatter_sigma_r(double2* arena, int64_t stride, const int64_t* __restrict__ sr_pos,
+                                  const int* __restrict__ sr_ptr, const int* __restrict__ sr_src,
+                                  int sr_slots, int64_t sr_nnz, const double2* __restrict__ sigma_r) {
+  const int e = blockIdx.y;
+  double2* a = arena + e * stride;
+  const double2* sr = sigma_r + e * sr_nnz;
+  const int64_t step = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t s = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < sr_slots; s += step) {
+    double2 v = make_double2(0.0, 0.0);
+    for (int q = sr_ptr[s]; q < sr_ptr[s + 1]; ++q) v = cadd(v, sr[sr_src[q]]);
+    const int64_t p = sr_pos[s];
+    a[p] = csub(a[p], v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batched explicit inverse (Gauss-Jordan, row partial pivoting, in place)
+// ---------------------------------------------------------------------------
+__device__ void report_singular(DevStatus* st, int e_global, int fold_pos, int pivot) {
+  const unsigned long long key = (static_cast<unsigned long long>(e_global) << 40) |
+                                 (static_cast<unsigned long long>(fold_pos) << 20) |
+                                 static_cast<unsigned long long>(pivot);
+  atomicMin(&st->singular_key, key);
+}
+
+// Block-wide reduction helpers (blockDim.x multiple of 32, <= 1024).
+__device__ double block_max(double v, double* red) {
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (l < (blockDim.x >> 5)) ? red[l] : 0.0;
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// Matrix view: element (r, c) at base[r * ld + c]; base in smem or global.
+template <bool kShared>
+__device__ void gauss_jordan(double2* a, int m, int* perm, double2* colk, double* red, int* flag,
+                             DevStatus* st, int e_global, int fold_pos) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double mx = 0.0;
+  for (int i = tid; i < m * m; i += nt) mx = fmax(mx, cabs2(a[i]));
+  const double thresh = 1e-13 * block_max(mx, red);
+  for (int k = 0; k < m; ++k) {
+    // Pivot: largest |a_rk| over r >= k, lowest row on ties (warp 0).
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int r = k + tid; r < m; r += 32) {
+        const double v = cabs2(a[r * m + k]);
+        if (v > best) {
+          best = v;
+          bi = r;
+        }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (tid == 0) {
+        perm[k] = bi;
+        // Same pivot magnitudes as LU with partial pivoting (the rows below
+        // k hold the Schur complement); NaN never trips the test, as in
+        // the reference's `mag <= threshold`.
+        if (best <= thresh) {
+          *flag = 1;
+          report_singular(st, e_global, fold_pos, k);
+        }
+      }
+    }
+    __syncthreads();
+    if (*flag) return;
+    const int p = perm[k];
+    if (p != k)
+      for (int c = tid; c < m; c += nt) {
+        const double2 t = a[k * m + c];
+        a[k * m + c] = a[p * m + c];
+        a[p * m + c] = t;
+      }
+    __syncthreads();
+    for (int r = tid; r < m; r += nt) colk[r] = a[r * m + k];
+    __syncthreads();
+    const double2 ip = cinv(colk[k]);
+    for (int c = tid; c < m; c += nt) a[k * m + c] = (c == k) ? ip : cmul(a[k * m + c], ip);
+    __syncthreads();
+    for (int i = tid; i < m * m; i += nt) {
+      const int r = i / m, c = i - r * m;
+      if (r == k) continue;
+      const double2 f = colk[r];
+      if (c == k) a[i] = make_double2(-(f.x * ip.x - f.y * ip.y), -(f.x * ip.y + f.y * ip.x));
+      else a[i] = csub(a[i], cmul(f, a[k * m + c]));
+    }
+    __syncthreads();
+  }
+  // Undo the row interchanges as column interchanges, last first.
+  for (int k = m - 1; k >= 0; --k) {
+    const int p = perm[k];
+    if (p != k)
+      for (int r = tid; r < m; r += nt) {
+        const double2 t = a[r * m + k];
+        a[r * m + k] = a[r * m + p];
+        a[r * m + p] = t;
+      }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(512) k_inverse_smem(double2* arena, int64_t stride,
+                                                      const InvTask* __restrict__ tasks, int e_base,
+                                                      DevStatus* st) {
+  extern __shared__ double2 sm[];
+  const InvTask tk = tasks[blockIdx.x];
+  const int m = tk.m;
+  double2* g = arena + blockIdx.y * stride + tk.off;
+  double* red = reinterpret_cast<double*>(sm);
+  double2* colk = sm + 16;
+  double2* a = colk + m;
+  int* perm = reinterpret_cast<int*>(a + m * m);
+  int* flag = perm + m;
+  if (threadIdx.x == 0) *flag = 0;
+  for (int i = threadIdx.x; i < m * m; i += blockDim.x) a[i] = g[i];
+  __syncthreads();
+  gauss_jordan<true>(a, m, perm, colk, red, flag, st, e_base + blockIdx.y, tk.fold_pos);
+  __syncthreads();
+  for (int i = threadIdx.x; i < m * m; i += blockDim.x) g[i] = a[i];
+}
+
+__global__ void __launch_bounds__(1024) k_inverse_global(double2* arena, int64_t stride,
+                                                         const InvTask* __restrict__ tasks,
+                                                         int e_base, DevStatus* st) {
+  extern __shared__ double2 sm[];
+  const InvTask tk = tasks[blockIdx.x];
+  const int m = tk.m;
+  double2* a = arena + blockIdx.y * stride + tk.off;
+  double* red = reinterpret_cast<double*>(sm);
+  double2* colk = sm + 16;
+  int* perm = reinterpret_cast<int*>(colk + m);
+  int* flag = perm + m;
+  if (threadIdx.x == 0) *flag = 0;
+  __syncthreads();
+  gauss_jordan<false>(a, m, perm, colk, red, flag, st, e_base + blockIdx.y, tk.fold_pos);
+}
+
+// ---------------------------------------------------------------------------
+// Grouped multi-term complex GEMM on DMMA (mma.sync.m8n8k4.f64)
+// ---------------------------------------------------------------------------
+constexpr int TM = kTileM, TN = kTileN, KC = 16;
+constexpr int LD_RK = KC + 4;   // (row, k) layouts: stride = 4 mod 8 (conflict-free frags)
+constexpr int LD_KR = TM + 2;   // (k, row) layouts: stride = 2 mod 8
+constexpr int OPND = (TM * LD_RK > KC * LD_KR) ? TM * LD_RK : KC * LD_KR;  // complex / operand / stage
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct ChunkCursor {
+  int term, k0;
+};
+
+__device__ __forceinline__ void load_chunk(double2* As, double2* Bs, const double2* base,
+                                           const GemmTerm& tm, int k0, int m, int n, int m0, int n0) {
+  const int tid = threadIdx.x;
+  const int k = tm.k;
+  // A: TM x KC elements
+  if (tm.a_op == OP_N) {
+#pragma unroll
+    for (int i = 0; i < (TM * KC) / 128; ++i) {
+      const int idx = tid + i * 128, r = idx / KC, kk = idx % KC;
+      const bool v = (m0 + r < m) && (k0 + kk < k);
+      const double2* src = v ? base + tm.a_off + int64_t(m0 + r) * tm.lda + (k0 + kk) : base;
+      cp_async16(As + r * LD_RK + kk, src, v);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < (TM * KC) / 128; ++i) {
+      const int idx = tid + i * 128, kk = idx / TM, r = idx % TM;
+      const bool v = (m0 + r < m) && (k0 + kk < k);
+      const double2* src = v ? base + tm.a_off + int64_t(k0 + kk) * tm.lda + (m0 + r) : base;
+      cp_async16(As + kk * LD_KR + r, src, v);
+    }
+  }
+  // B: KC x TN elements
+  if (tm.b_op == OP_N || tm.b_op == OP_C) {
+#pragma unroll
+    for (int i = 0; i < (TN * KC) / 128; ++i) {
+      const int idx = tid + i * 128, kk = idx / TN, c = idx % TN;
+      const bool v = (n0 + c < n) && (k0 + kk < k);
+      const double2* src = v ? base + tm.b_off + int64_t(k0 + kk) * tm.ldb + (n0 + c) : base;
+      cp_async16(Bs + kk * LD_KR + c, src, v);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < (TN * KC) / 128; ++i) {
+      const int idx = tid + i * 128, c = idx / KC, kk = idx % KC;
+      const bool v = (n0 + c < n) && (k0 + kk < k);
+      const double2* src = v ? base + tm.b_off + int64_t(n0 + c) * tm.ldb + (k0 + kk) : base;
+      cp_async16(Bs + c * LD_RK + kk, src, v);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride,
+                                              const GemmTask* __restrict__ tasks,
+                                              const GemmTerm* __restrict__ terms,
+                                              const GemmTile* __restrict__ tiles, int tile_begin) {
+  __shared__ __align__(16) double2 smA[2][OPND];
+  __shared__ __align__(16) double2 smB[2][OPND];
+  const GemmTile tl = tiles[tile_begin + blockIdx.x];
+  const GemmTask tk = tasks[tl.task];
+  double2* base = arena + blockIdx.y * stride;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
+
+  double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) cr[i][j][q] = ci[i][j][q] = 0.0;
+
+  // Flattened (term, k-chunk) sequence, double-buffered with cp.async.
+  const int tend = tk.term_begin + tk.term_count;
+  ChunkCursor cur{tk.term_begin, 0};
+  while (cur.term < tend && terms[cur.term].k <= 0) ++cur.term;
+  int stage = 0;
+  GemmTerm tm_load;
+  if (cur.term < tend) {
+    tm_load = terms[cur.term];
+    load_chunk(smA[0], smB[0], base, tm_load, 0, tk.m, tk.n, tl.m0, tl.n0);
+  }
+  cp_async_commit();
+  while (cur.term < tend) {
+    const GemmTerm tm = terms[cur.term];
+    const int k0 = cur.k0;
+    // Advance the cursor and prefetch the next chunk into the other stage.
+    ChunkCursor nxt = cur;
+    nxt.k0 += KC;
+    if (nxt.k0 >= tm.k) {
+      nxt.k0 = 0;
+      ++nxt.term;
+      while (nxt.term < tend && terms[nxt.term].k <= 0) ++nxt.term;
+    }
+    if (nxt.term < tend) {
+      const GemmTerm tn = terms[nxt.term];
+      load_chunk(smA[stage ^ 1], smB[stage ^ 1], base, tn, nxt.k0, tk.m, tk.n, tl.m0, tl.n0);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+
+    const double2* As = smA[stage];
+    const double2* Bs = smB[stage];
+    const double sg = static_cast<double>(tm.sign);
+    const bool conjb = (tm.b_op == OP_C || tm.b_op == OP_H);
+    const bool a_rk = (tm.a_op == OP_N);
+    const bool b_kr = (tm.b_op == OP_N || tm.b_op == OP_C);
+    const int ksteps = min(KC, tm.k - k0);
+#pragma unroll
+    for (int s = 0; s < KC / 4; ++s) {
+      if (4 * s >= ksteps) break;
+      const int kk = 4 * s + t;
+      double2 a[2], b[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = wm + 8 * i + g;
+        a[i] = a_rk ? As[r * LD_RK + kk] : As[kk * LD_KR + r];
+        a[i].x *= sg;
+        a[i].y *= sg;
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int c = wn + 8 * j + g;
+        b[j] = b_kr ? Bs[kk * LD_KR + c] : Bs[c * LD_RK + kk];
+        if (conjb) b[j].y = -b[j].y;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double nai = -a[i].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+          dmma(cr[i][j][0], cr[i][j][1], nai, b[j].y);
+          dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+          dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+        }
+      }
+    }
+    __syncthreads();
+    stage ^= 1;
+    cur = nxt;
+  }
+  cp_async_wait<0>();
+
+  // Epilogue: lane owns C[r][c], C[r][c+1] of each 8x8 subtile.
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = tl.m0 + wm + 8 * i + g;
+    if (r >= tk.m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = tl.n0 + wn + 8 * j + 2 * t + q;
+        if (c >= tk.n) continue;
+        double2 v = make_double2(cr[i][j][q], ci[i][j][q]);
+        double2* dst = base + tk.c_off + int64_t(r) * tk.ldc + c;
+        if (tk.mode == MODE_ADD) v = cadd(*dst, v);
+        else if (tk.mode == MODE_INIT) v = cadd(base[tk.init_off + int64_t(r) * tk.ld_init + c], v);
+        *dst = v;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Diagonal-only products, diagonal seeds, outputs
+// ---------------------------------------------------------------------------
+__global__ void k_diag(double2* arena, int64_t stride, const DiagTask* __restrict__ tasks,
+                       const GemmTerm* __restrict__ terms, int begin) {
+  const DiagTask tk = tasks[begin + blockIdx.x];
+  double2* base = arena + blockIdx.y * stride;
+  for (int a = threadIdx.x; a < tk.m; a += blockDim.x) {
+    double2 acc = tk.has_init ? base[tk.init_off + int64_t(a) * tk.init_stride] : make_double2(0.0, 0.0);
+    for (int q = tk.term_begin; q < tk.term_begin + tk.term_count; ++q) {
+      const GemmTerm tm = terms[q];
+      double2 s = make_double2(0.0, 0.0);
+      for (int b = 0; b < tm.k; ++b) {
+        const double2 av = tm.a_op == OP_N ? base[tm.a_off + int64_t(a) * tm.lda + b]
+                                           : base[tm.a_off + int64_t(b) * tm.lda + a];
+        double2 bv;
+        if (tm.b_op == OP_N || tm.b_op == OP_C) bv = base[tm.b_off + int64_t(b) * tm.ldb + a];
+        else bv = base[tm.b_off + int64_t(a) * tm.ldb + b];
+        if (tm.b_op == OP_C || tm.b_op == OP_H) bv.y = -bv.y;
+        s = cadd(s, cmul(av, bv));
+      }
+      if (tm.sign < 0) acc = csub(acc, s);
+      else acc = cadd(acc, s);
+    }
+    base[tk.out_off + a] = acc;
+  }
+}
+
+__global__ void k_scale(double2* arena, int64_t stride, const ScaleTask* __restrict__ tasks, int begin) {
+  const ScaleTask tk = tasks[begin + blockIdx.x];
+  double2* base = arena + blockIdx.y * stride;
+  const int total = tk.m * tk.n;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int a = i / tk.n, b = i - a * tk.n;
+    double2 src = base[tk.src_off + int64_t(a) * tk.ld_src + b];
+    src.y = -src.y;
+    base[tk.dst_off + int64_t(a) * tk.ld_dst + b] = cmul(base[tk.sig_off + a], src);
+  }
+}
+
+__global__ void k_output(const double2* __restrict__ arena, int64_t stride, int nE, int e_base, int n,
+                         const int64_t* __restrict__ gr_pos, const int64_t* __restrict__ gl_pos,
+                         const double* __restrict__ weights, double2* gr, double2* gl, double* density,
+                         DevStatus* st) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const int64_t pr = gr_pos[d], pl = gl_pos[d];
+  double acc = density[d];
+  for (int e = 0; e < nE; ++e) {
+    const double2* a = arena + int64_t(e) * stride;
+    if (gr) gr[int64_t(e) * n + d] = a[pr];
+    const double2 v = pl >= 0 ? a[pl] : make_double2(0.0, 0.0);
+    if (gl) gl[int64_t(e) * n + d] = v;
+    const double mag = hypot(v.x, v.y);
+    if (fabs(v.x) > 1e-8 * mag)
+      atomicMin(&st->residual_key, (static_cast<unsigned long long>(e_base + e) << 32) |
+                                       static_cast<unsigned long long>(d));
+    acc += weights[e] * v.y;
+  }
+  density[d] = acc;
+}
+
+// Sigma^< skewness per cluster block (validate_sigma, hsc.cpp:108-112 with
+// skew_hermitian_defect, dense.cpp:221-230): accumulate ||S + S^H||_F^2 and
+// ||S||_F^2 per (energy, seeded cluster) from the slots.
+__device__ __forceinline__ double2 slot_value(const double2* sl, const int* ptr, const int* src, int s) {
+  double2 v = make_double2(0.0, 0.0);
+  for (int q = ptr[s]; q < ptr[s + 1]; ++q) v = cadd(v, sl[src[q]]);
+  return v;
+}
+
+__global__ void k_skew_accum(const double2* __restrict__ sigma_l, int64_t sl_nnz, int slots,
+                             const int* __restrict__ ptr, const int* __restrict__ src,
+                             const int* __restrict__ partner, const int* __restrict__ cidx, int nsc,
+                             double* acc) {
+  const int e = blockIdx.y;
+  const double2* sl = sigma_l + e * sl_nnz;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
+    const double2 v = slot_value(sl, ptr, src, s);
+    double num;
+    const int p = partner[s];
+    if (p >= 0) {
+      const double2 w = slot_value(sl, ptr, src, p);
+      const double re = v.x + w.x, im = v.y - w.y;
+      num = re * re + im * im;
+    } else {
+      num = 2.0 * (v.x * v.x + v.y * v.y);
+    }
+    double* a = acc + (int64_t(e) * nsc + cidx[s]) * 2;
+    atomicAdd(a, num);
+    atomicAdd(a + 1, v.x * v.x + v.y * v.y);
+  }
+}
+
+__global__ void k_skew_flag(const double* __restrict__ acc, int nsc, const int* __restrict__ ids,
+                            int nE, int e_base, DevStatus* st) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nsc * nE) return;
+  const int e = i / nsc, c = i - e * nsc;
+  const double num = sqrt(acc[2 * i]), den = sqrt(acc[2 * i + 1]);
+  const double defect = den == 0.0 ? num : num / den;
+  if (defect > 1e-10)
+    atomicMin(&st->nonskew_key, (static_cast<unsigned long long>(e_base + e) << 32) |
+                                    static_cast<unsigned long long>(ids[c]));
+}
+
+int grid_for(int64_t work, int threads, int cap) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return static_cast<int>(b);
+}
+
+}  // namespace
+
+void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_template,
+                     const int64_t* d_diag_pos, const double* d_energies, const int64_t* d_sr_pos,
+                     const int* d_sr_ptr, const int* d_sr_src, int64_t sr_nnz,
+                     const double2* d_sigma_r, const int64_t* d_sl_pos, const int* d_sl_ptr,
+                     const int* d_sl_src, int64_t sl_nnz, const double2* d_sigma_l, cudaStream_t s,
+                     int64_t& launches) {
+  const int64_t len = std::max<int64_t>(p.a_region, p.z_end - p.z_begin);
+  dim3 g1(grid_for(len, 256, 2048), b.nE);
+  k_copy_template<<<g1, 256, 0, s>>>(b.arena, b.stride, d_template, p.a_region, p.z_begin, p.z_end);
+  const int sr_slots = static_cast<int>(p.sr_slot_pos.size());
+  const int sl_slots = static_cast<int>(p.sl_slot_pos.size());
+  dim3 g2(grid_for(std::max<int64_t>(p.desc.n, sl_slots), 256, 1024), b.nE);
+  k_scatter<<<g2, 256, 0, s>>>(b.arena, b.stride, p.desc.n, d_diag_pos, d_energies, d_sl_pos, d_sl_ptr,
+                               d_sl_src, sl_slots, sl_nnz, d_sigma_l);
+  launches += 2;
+  if (sr_slots > 0) {
+    dim3 g3(grid_for(sr_slots, 256, 1024), b.nE);
+    k_scatter_sigma_r<<<g3, 256, 0, s>>>(b.arena, b.stride, d_sr_pos, d_sr_ptr, d_sr_src, sr_slots,
+                                         sr_nnz, d_sigma_r);
+    ++launches;
+  }
+}
+
+void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
+                    DevStatus* st, cudaStream_t s, int64_t& launches) {
+  // Split the level's tasks into the shared-memory and global-memory variants
+  // (tasks are pre-sorted so each variant is a contiguous range).
+  int i = 0;
+  while (i < count) {
+    const bool small = h_tasks[i].m <= kSmemInvMax;
+    int j = i;
+    int mmax = 0;
+    while (j < count && (h_tasks[j].m <= kSmemInvMax) == small) {
+      mmax = std::max(mmax, h_tasks[j].m);
+      ++j;
+    }
+    dim3 grid(j - i, b.nE);
+    if (small) {
+      const size_t smem = 256 + size_t(mmax) * mmax * 16 + size_t(mmax) * 16 + size_t(mmax) * 4 + 16;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_inverse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+      }
+      const int threads = mmax <= 32 ? 128 : (mmax <= 64 ? 256 : 512);
+      k_inverse_smem<<<grid, threads, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+    } else {
+      const size_t smem = 256 + size_t(mmax) * 16 + size_t(mmax) * 4 + 16;
+      k_inverse_global<<<grid, 1024, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+    }
+    ++launches;
+    i = j;
+  }
+}
+
+void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
+                 const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s,
+                 int64_t& launches) {
+  if (tile_count <= 0) return;
+  dim3 grid(tile_count, b.nE);
+  k_gemm<<<grid, 128, 0, s>>>(b.arena, b.stride, d_tasks, d_terms, d_tiles, tile_begin);
+  ++launches;
+}
+
+void launch_diag(const BatchArgs& b, const DiagTask* d_tasks, const GemmTerm* d_terms, int begin,
+                 int count, cudaStream_t s, int64_t& launches) {
+  if (count <= 0) return;
+  dim3 grid(count, b.nE);
+  k_diag<<<grid, 64, 0, s>>>(b.arena, b.stride, d_tasks, d_terms, begin);
+  ++launches;
+}
+
+void launch_scale(const BatchArgs& b, const ScaleTask* d_tasks, int begin, int count, cudaStream_t s,
+                  int64_t& launches) {
+  if (count <= 0) return;
+  dim3 grid(count, b.nE);
+  k_scale<<<grid, 256, 0, s>>>(b.arena, b.stride, d_tasks, begin);
+  ++launches;
+}
+
+void launch_skew_check(const BatchArgs& b, const double2* d_sigma_l, int64_t sl_nnz, int sl_slots,
+                       const int* d_sl_ptr, const int* d_sl_src, const int* d_sl_partner,
+                       const int* d_sl_cidx, int n_seeded, const int* d_seeded_ids, double* d_acc,
+                       DevStatus* st, cudaStream_t s, int64_t& launches) {
+  if (sl_slots <= 0 || n_seeded <= 0) return;
+  cudaMemsetAsync(d_acc, 0, sizeof(double) * 2 * size_t(n_seeded) * b.nE, s);
+  dim3 g(grid_for(sl_slots, 256, 1024), b.nE);
+  k_skew_accum<<<g, 256, 0, s>>>(d_sigma_l, sl_nnz, sl_slots, d_sl_ptr, d_sl_src, d_sl_partner, d_sl_cidx,
+                                 n_seeded, d_acc);
+  const int tot = n_seeded * b.nE;
+  k_skew_flag<<<(tot + 255) / 256, 256, 0, s>>>(d_acc, n_seeded, d_seeded_ids, b.nE, b.e_base, st);
+  launches += 2;
+}
+
+void launch_output(const BatchArgs& b, int n, const int64_t* d_gr_pos, const int64_t* d_gl_pos,
+                   const double* d_weights, double2* d_gr, double2* d_gl, double* d_density,
+                   DevStatus* st, cudaStream_t s, int64_t& launches) {
+  k_output<<<(n + 255) / 256, 256, 0, s>>>(b.arena, b.stride, b.nE, b.e_base, n, d_gr_pos, d_gl_pos,
+                                           d_weights, d_gr, d_gl, d_density, st);
+  ++launches;
+}
+
+}  // namespace negfb

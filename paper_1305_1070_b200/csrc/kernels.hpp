@@ -1,0 +1,48 @@
+// Device kernels of the B200 HSC path (sm_100a, complex FP64).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "plan.hpp"
+
+namespace negfb {
+
+// Device-side error record (lowest key wins, like run.cpp:258-262).
+struct DevStatus {
+  unsigned long long singular_key;   // energy<<40 | fold_pos<<20 | pivot
+  unsigned long long residual_key;   // energy<<32 | dof
+  unsigned long long nonskew_key;    // energy<<32 | cluster
+};
+
+struct BatchArgs {
+  double2* arena;
+  int64_t stride;     // complex elements per energy arena
+  int nE;
+  int e_base;         // global index of energy 0 of this batch
+};
+
+void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_template,
+                     const int64_t* d_diag_pos, const double* d_energies,
+                     const int64_t* d_sr_pos, const int* d_sr_ptr, const int* d_sr_src,
+                     int64_t sr_nnz, const double2* d_sigma_r, const int64_t* d_sl_pos,
+                     const int* d_sl_ptr, const int* d_sl_src, int64_t sl_nnz,
+                     const double2* d_sigma_l, cudaStream_t s, int64_t& launches);
+void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
+                    DevStatus* st, cudaStream_t s, int64_t& launches);
+void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
+                 const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s,
+                 int64_t& launches);
+void launch_diag(const BatchArgs& b, const DiagTask* d_tasks, const GemmTerm* d_terms, int begin,
+                 int count, cudaStream_t s, int64_t& launches);
+void launch_scale(const BatchArgs& b, const ScaleTask* d_tasks, int begin, int count,
+                  cudaStream_t s, int64_t& launches);
+void launch_skew_check(const BatchArgs& b, const double2* d_sigma_l, int64_t sl_nnz, int sl_slots,
+                       const int* d_sl_ptr, const int* d_sl_src, const int* d_sl_partner,
+                       const int* d_sl_cidx, int n_seeded, const int* d_seeded_ids, double* d_acc,
+                       DevStatus* st, cudaStream_t s, int64_t& launches);
+void launch_output(const BatchArgs& b, int n, const int64_t* d_gr_pos, const int64_t* d_gl_pos,
+                   const double* d_weights, double2* d_gr, double2* d_gl, double* d_density,
+                   DevStatus* st, cudaStream_t s, int64_t& launches);
+
+}  // namespace negfb

@@ -1,0 +1,705 @@
+// Host plan construction (see plan.hpp).  Reference anchors per step are
+// given inline; all of this runs once per device, never per energy.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <map>
+#include <numeric>
+#include <set>
+#include <unordered_map>
+
+namespace negfb {
+
+namespace {
+
+int64_t align8(int64_t x) { return (x + 7) & ~int64_t(7); }
+
+int find_pos(const std::vector<int>& v, int x) {
+  for (std::size_t i = 0; i < v.size(); ++i)
+    if (v[i] == x) return static_cast<int>(i);
+  return -1;
+}
+
+// Keeps `list` in ancestor order (nearest first) while inserting j.
+void insert_anc_order(std::vector<int>& list, const Tree& t, int j) {
+  if (find_pos(list, j) >= 0) return;
+  const int lj = t.cluster(j).level;
+  auto it = list.begin();
+  while (it != list.end() && t.cluster(*it).level < lj) ++it;
+  list.insert(it, j);
+}
+
+struct Builder {
+  Plan& P;
+  const Tree& t;
+  explicit Builder(Plan& p) : P(p), t(p.tree) {}
+
+  int msz(int c) const { return t.cluster(c).size(); }
+  int lev(int c) const { return t.cluster(c).level; }
+  ClusterInfo& I(int c) { return P.ci[static_cast<std::size_t>(c)]; }
+
+  int64_t col_of(const std::vector<int>& cols, const std::vector<int64_t>& offs, int j) const {
+    const int p = find_pos(cols, j);
+    if (p < 0) fail(kInternal, "plan: missing column block");
+    return offs[static_cast<std::size_t>(p)];
+  }
+
+  int add_term(std::vector<GemmTerm>& terms, int k, int a_op, int64_t a_off, int lda, int b_op,
+               int64_t b_off, int ldb, int sign) {
+    GemmTerm g;
+    g.k = k;
+    g.a_op = a_op;
+    g.b_op = b_op;
+    g.sign = sign;
+    g.lda = lda;
+    g.ldb = ldb;
+    g.a_off = a_off;
+    g.b_off = b_off;
+    terms.push_back(g);
+    return static_cast<int>(terms.size()) - 1;
+  }
+
+  // Open/close helpers for ops.
+  Op cur{};
+  void open(int kind, int phase, int level) {
+    cur = Op{};
+    cur.kind = kind;
+    cur.phase = phase;
+    cur.level = level;
+    switch (kind) {
+      case K_INVERSE: cur.begin = static_cast<int>(P.inv_tasks.size()); break;
+      case K_GEMM:
+        cur.begin = static_cast<int>(P.gemm_tiles.size());
+        cur.task_begin = static_cast<int>(P.gemm_tasks.size());
+        break;
+      case K_DIAG: cur.begin = static_cast<int>(P.diag_tasks.size()); break;
+      default: cur.begin = static_cast<int>(P.scale_tasks.size()); break;
+    }
+  }
+  void close() {
+    switch (cur.kind) {
+      case K_INVERSE: cur.count = static_cast<int>(P.inv_tasks.size()) - cur.begin; break;
+      case K_GEMM:
+        cur.count = static_cast<int>(P.gemm_tiles.size()) - cur.begin;
+        cur.task_count = static_cast<int>(P.gemm_tasks.size()) - cur.task_begin;
+        break;
+      case K_DIAG: cur.count = static_cast<int>(P.diag_tasks.size()) - cur.begin; break;
+      default: cur.count = static_cast<int>(P.scale_tasks.size()) - cur.begin; break;
+    }
+    if (cur.count > 0) {
+      P.ops.push_back(cur);
+      P.exec_cmul += cur.cmul;
+    }
+  }
+
+  void gemm_task(int m, int n, int64_t c_off, int ldc, int mode, int64_t init_off, int ld_init,
+                 int term_begin) {
+    if (m <= 0 || n <= 0) {
+      P.gemm_terms.resize(static_cast<std::size_t>(term_begin));
+      return;
+    }
+    GemmTask tk;
+    tk.m = m;
+    tk.n = n;
+    tk.ldc = ldc;
+    tk.mode = mode;
+    tk.c_off = c_off;
+    tk.init_off = init_off;
+    tk.ld_init = ld_init;
+    tk.term_begin = term_begin;
+    tk.term_count = static_cast<int>(P.gemm_terms.size()) - term_begin;
+    const int id = static_cast<int>(P.gemm_tasks.size());
+    P.gemm_tasks.push_back(tk);
+    for (int t2 = tk.term_begin; t2 < tk.term_begin + tk.term_count; ++t2)
+      cur.cmul += static_cast<double>(m) * n * P.gemm_terms[t2].k;
+    for (int m0 = 0; m0 < m; m0 += kTileM)
+      for (int n0 = 0; n0 < n; n0 += kTileN) P.gemm_tiles.push_back(GemmTile{id, m0, n0, 0});
+  }
+};
+
+}  // namespace
+
+Plan build_plan(ProblemDesc desc) {
+  Plan P;
+  P.desc = std::move(desc);
+  const ProblemDesc& d = P.desc;
+  const int n = d.n;
+  if (n <= 0) fail(kContractViolation, "problem: no dofs");
+  if (d.h_rows.size() != d.h_cols.size() || d.h_rows.size() != d.h_vals.size())
+    fail(kContractViolation, "problem: H arrays disagree in length");
+  if (d.sr_rows.size() != d.sr_cols.size() || d.sl_rows.size() != d.sl_cols.size())
+    fail(kContractViolation, "problem: self-energy pattern arrays disagree in length");
+  auto check_idx = [&](const std::vector<int>& v, const char* what) {
+    for (int x : v)
+      if (x < 0 || x >= n) fail(kContractViolation, std::string("problem: ") + what + " index out of range");
+  };
+  check_idx(d.h_rows, "H");
+  check_idx(d.h_cols, "H");
+  check_idx(d.sr_rows, "sigma_r");
+  check_idx(d.sr_cols, "sigma_r");
+  check_idx(d.sl_rows, "sigma_lesser");
+  check_idx(d.sl_cols, "sigma_lesser");
+
+  // ---- tree (run.cpp:123-133: graph of A's pattern, atomic contact groups)
+  std::vector<std::pair<int, int>> pat;
+  pat.reserve(d.h_rows.size() + d.sr_rows.size());
+  for (std::size_t k = 0; k < d.h_rows.size(); ++k) pat.push_back({d.h_rows[k], d.h_cols[k]});
+  for (std::size_t k = 0; k < d.sr_rows.size(); ++k) pat.push_back({d.sr_rows[k], d.sr_cols[k]});
+  P.graph = graph_of_pattern(n, pat);
+  if (d.explicit_tree) {
+    if (d.tree_parent.size() != d.tree_dofs.size())
+      fail(kContractViolation, "problem: explicit tree arrays disagree");
+    std::vector<Cluster> cs(d.tree_parent.size());
+    for (std::size_t i = 0; i < cs.size(); ++i) {
+      cs[i].parent = d.tree_parent[i];
+      cs[i].dofs = d.tree_dofs[i];
+    }
+    P.tree = Tree::build(std::move(cs), n);
+  } else {
+    P.tree = nested_dissection(P.graph, d.atomic_groups, d.max_leaf, d.coords);
+  }
+  const Tree& t = P.tree;
+  const int nc = t.num_clusters();
+  P.ci.assign(static_cast<std::size_t>(nc), ClusterInfo{});
+  Builder B(P);
+  for (int c = 0; c < nc; ++c) {
+    B.I(c).m = t.cluster(c).size();
+    P.max_block = std::max(P.max_block, B.I(c).m);
+  }
+
+  // ---- partition rule (block.cpp:55-72): every A entry joins related clusters
+  {
+    int bad = 0;
+    for (const auto& e : pat) {
+      const int ci = t.dof_cluster(e.first), cj = t.dof_cluster(e.second);
+      if (ci == cj || t.is_ancestor(cj, ci) || t.is_ancestor(ci, cj)) continue;
+      if (e.first < e.second) ++bad;
+    }
+    if (bad) fail(kPartitionViolation, std::to_string(bad) +
+                                           " matrix entr(ies) join clusters that are not ancestor-related");
+  }
+  // Sigma^< must be cluster-block-diagonal (hsc.cpp:104-107).
+  for (std::size_t k = 0; k < d.sl_rows.size(); ++k)
+    if (t.dof_cluster(d.sl_rows[k]) != t.dof_cluster(d.sl_cols[k]))
+      fail(kContractViolation, "sigma_lesser must be block diagonal on the cluster partition");
+
+  // ---- symbolic fold (hsc.cpp:482-511): S0 from the (descendant, ancestor)
+  // orientation of A's pattern, then fill of every ancestor pair.
+  std::vector<std::set<int>> S0(static_cast<std::size_t>(nc));
+  for (const auto& e : pat) {
+    const int ci = t.dof_cluster(e.first), cj = t.dof_cluster(e.second);
+    if (ci != cj && t.is_ancestor(cj, ci)) S0[ci].insert(cj);
+  }
+  for (int c = 0; c < nc; ++c)
+    for (int j : t.cluster(c).anc)
+      if (S0[c].count(j)) B.I(c).S.push_back(j);
+  for (int i : t.fold_order()) {
+    const std::vector<int> js = B.I(i).S;  // complete: all descendants folded
+    for (std::size_t p = 0; p < js.size(); ++p)
+      for (std::size_t q = p + 1; q < js.size(); ++q) insert_anc_order(B.I(js[p]).S, t, js[q]);
+  }
+  for (int c = 0; c < nc; ++c) {
+    ClusterInfo& ci = B.I(c);
+    int64_t off = 0;
+    for (int j : ci.S) {
+      ci.s_col.push_back(off);
+      off += B.msz(j);
+      B.I(j).referenced = true;
+    }
+    ci.K = static_cast<int>(off);
+  }
+
+  // ---- Sigma^< structure (hsc.cpp:89-125): seeded clusters, dense or diagonal
+  for (std::size_t k = 0; k < d.sl_rows.size(); ++k) {
+    const int c = t.dof_cluster(d.sl_rows[k]);
+    B.I(c).seeded = true;
+    if (d.sl_rows[k] != d.sl_cols[k]) B.I(c).seed_dense = true;
+    P.any_seed = true;
+  }
+
+  // ---- needed-block closure for the top-down sweeps
+  const int root = t.root();
+  {
+    std::vector<std::set<int>> needG(static_cast<std::size_t>(nc)), needP(static_cast<std::size_t>(nc));
+    for (int c = 0; c < nc; ++c) {
+      if (c == root) continue;
+      for (int j : B.I(c).S) {
+        needG[c].insert(j);
+        needP[c].insert(j);
+      }
+      if (B.I(c).seeded)
+        for (int j : t.cluster(c).anc) needG[c].insert(j);
+    }
+    auto propagate = [&](std::vector<std::set<int>>& need, int y) {
+      for (int j : need[y])
+        for (int k : B.I(y).S) {
+          if (k == j) continue;
+          if (B.lev(k) < B.lev(j)) need[k].insert(j);
+          else need[j].insert(k);
+        }
+    };
+    for (int y : t.fold_order()) {
+      propagate(needG, y);
+      propagate(needP, y);
+    }
+    for (int c = 0; c < nc; ++c) {
+      ClusterInfo& ci = B.I(c);
+      for (int j : t.cluster(c).anc) {
+        if (needG[c].count(j)) ci.gcols.push_back(j);
+        if (needP[c].count(j)) ci.pcols.push_back(j);
+      }
+      ci.full_g = ci.referenced || ci.seeded || c == root;
+      ci.full_p = ci.referenced || c == root;
+    }
+  }
+  // ---- N structure (hsc.cpp:229-266)
+  {
+    std::vector<std::vector<int>> ncols(static_cast<std::size_t>(nc));
+    for (int c = 0; c < nc; ++c)
+      if (B.I(c).seeded) {
+        ncols[c] = t.cluster(c).anc;
+        B.I(c).has_nd = true;
+      }
+    for (int i : t.fold_order()) {
+      if (ncols[i].empty()) continue;
+      for (int j : B.I(i).S)
+        for (int k : ncols[i]) {
+          if (B.lev(k) < B.lev(j)) continue;
+          if (k == j) B.I(j).has_nd = true;
+          else insert_anc_order(ncols[j], t, k);
+        }
+    }
+    for (int c = 0; c < nc; ++c) B.I(c).ncols = ncols[c];
+  }
+  for (int c = 0; c < nc; ++c) {
+    ClusterInfo& ci = B.I(c);
+    auto offs = [&](const std::vector<int>& cols, std::vector<int64_t>& o, int& w) {
+      int64_t acc = 0;
+      for (int j : cols) {
+        o.push_back(acc);
+        acc += B.msz(j);
+      }
+      w = static_cast<int>(acc);
+    };
+    offs(ci.gcols, ci.gcol_off, ci.WG);
+    offs(ci.ncols, ci.ncol_off, ci.WN);
+    offs(ci.pcols, ci.pcol_off, ci.WP);
+  }
+
+  // ---- arena layout (complex elements per energy)
+  int64_t cur = 0;
+  auto take = [&](int64_t cnt) {
+    const int64_t o = cur;
+    cur = align8(cur + cnt);
+    return o;
+  };
+  for (int c = 0; c < nc; ++c) B.I(c).off_d = take(int64_t(B.msz(c)) * B.msz(c));
+  for (int c = 0; c < nc; ++c)
+    if (B.I(c).K) B.I(c).off_arow = take(int64_t(B.msz(c)) * B.I(c).K);
+  P.a_region = cur;
+  P.z_begin = cur;
+  for (int c = 0; c < nc; ++c) {
+    ClusterInfo& ci = B.I(c);
+    if (!ci.seeded) continue;
+    ci.off_sig = take(ci.seed_dense ? int64_t(ci.m) * ci.m : int64_t(ci.m));
+  }
+  for (int c = 0; c < nc; ++c) {
+    ClusterInfo& ci = B.I(c);
+    if (ci.has_nd) ci.off_nd = take(int64_t(ci.m) * ci.m);
+    if (ci.WN) ci.off_nrow = take(int64_t(ci.m) * ci.WN);
+  }
+  if (P.any_seed) B.I(root).off_pd = take(int64_t(B.msz(root)) * B.msz(root));
+  P.z_end = cur;
+  for (int c = 0; c < nc; ++c) {
+    ClusterInfo& ci = B.I(c);
+    if (ci.K) ci.off_psi = take(int64_t(ci.m) * ci.K);
+    if (c == root) ci.off_gd = ci.off_d;  // G_rr = (A_rr folded)^-1 (hsc.cpp:148-150)
+    else ci.off_gd = take(ci.full_g ? int64_t(ci.m) * ci.m : int64_t(ci.m));
+    if (ci.WG) ci.off_grow = take(int64_t(ci.m) * ci.WG);
+    if (P.any_seed && c != root) ci.off_pd = take(ci.full_p ? int64_t(ci.m) * ci.m : int64_t(ci.m));
+    if (P.any_seed && ci.WP) ci.off_prow = take(int64_t(ci.m) * ci.WP);
+  }
+  P.arena = std::max<int64_t>(cur, 8);
+
+  // ---- template of the A region: -H scattered into the descendant-row
+  // orientation (the only one the lean fold reads, hsc.cpp:483-490).
+  P.a_template.assign(static_cast<std::size_t>(P.a_region), cplx(0.0, 0.0));
+  auto a_pos = [&](int r, int c) -> int64_t {
+    const int ci = t.dof_cluster(r), cj = t.dof_cluster(c);
+    const int lr = t.local_index(r), lc = t.local_index(c);
+    const ClusterInfo& I = P.ci[ci];
+    if (ci == cj) return I.off_d + int64_t(lr) * I.m + lc;
+    const int p = find_pos(I.S, cj);
+    if (p < 0) return -1;  // ancestor-row orientation: never read
+    return I.off_arow + int64_t(lr) * I.K + I.s_col[p] + lc;
+  };
+  for (std::size_t k = 0; k < d.h_rows.size(); ++k) {
+    const int64_t pos = a_pos(d.h_rows[k], d.h_cols[k]);
+    if (pos >= 0) P.a_template[static_cast<std::size_t>(pos)] -= d.h_vals[k];
+  }
+  P.diag_pos.resize(static_cast<std::size_t>(n));
+  for (int dof = 0; dof < n; ++dof) {
+    const ClusterInfo& I = P.ci[t.dof_cluster(dof)];
+    P.diag_pos[dof] = I.off_d + int64_t(t.local_index(dof)) * (I.m + 1);
+  }
+  // Sigma^r slots (duplicates summed, coo_normalize semantics).
+  {
+    std::map<int64_t, std::vector<int>> by_pos;
+    for (std::size_t k = 0; k < d.sr_rows.size(); ++k) {
+      const int64_t pos = a_pos(d.sr_rows[k], d.sr_cols[k]);
+      if (pos >= 0) by_pos[pos].push_back(static_cast<int>(k));
+    }
+    P.sr_slot_ptr.push_back(0);
+    for (const auto& kv : by_pos) {
+      P.sr_slot_pos.push_back(kv.first);
+      for (int s : kv.second) P.sr_slot_src.push_back(s);
+      P.sr_slot_ptr.push_back(static_cast<int>(P.sr_slot_src.size()));
+    }
+  }
+  // Sigma^< slots: one per distinct (r, c); partner = slot of (c, r).
+  {
+    std::map<std::pair<int, int>, std::vector<int>> by_rc;
+    for (std::size_t k = 0; k < d.sl_rows.size(); ++k)
+      by_rc[{d.sl_rows[k], d.sl_cols[k]}].push_back(static_cast<int>(k));
+    std::map<std::pair<int, int>, int> slot_of;
+    P.sl_slot_ptr.push_back(0);
+    for (const auto& kv : by_rc) {
+      const int r = kv.first.first, c = kv.first.second;
+      const ClusterInfo& I = P.ci[t.dof_cluster(r)];
+      const int lr = t.local_index(r), lc = t.local_index(c);
+      slot_of[kv.first] = static_cast<int>(P.sl_slot_pos.size());
+      P.sl_slot_pos.push_back(I.seed_dense ? I.off_sig + int64_t(lr) * I.m + lc : I.off_sig + lr);
+      P.sl_cluster.push_back(t.dof_cluster(r));
+      for (int s : kv.second) P.sl_slot_src.push_back(s);
+      P.sl_slot_ptr.push_back(static_cast<int>(P.sl_slot_src.size()));
+    }
+    for (const auto& kv : by_rc) {
+      auto it = slot_of.find({kv.first.second, kv.first.first});
+      P.sl_partner.push_back(it == slot_of.end() ? -1 : it->second);
+    }
+    std::vector<int> cidx(static_cast<std::size_t>(nc), -1);
+    for (int c = 0; c < nc; ++c)
+      if (B.I(c).seeded) {
+        cidx[c] = static_cast<int>(P.seeded_ids.size());
+        P.seeded_ids.push_back(c);
+      }
+    for (int c : P.sl_cluster) P.sl_cidx.push_back(cidx[c]);
+  }
+  P.out_gr_pos.resize(static_cast<std::size_t>(n));
+  P.out_gl_pos.resize(static_cast<std::size_t>(n));
+  for (int dof = 0; dof < n; ++dof) {
+    const int c = t.dof_cluster(dof);
+    const ClusterInfo& I = P.ci[c];
+    const int l = t.local_index(dof);
+    P.out_gr_pos[dof] = I.off_gd + (I.full_g ? int64_t(l) * (I.m + 1) : l);
+    P.out_gl_pos[dof] = P.any_seed ? I.off_pd + (I.full_p ? int64_t(l) * (I.m + 1) : l) : -1;
+  }
+
+  // ---- schedule
+  std::vector<std::vector<int>> by_level(static_cast<std::size_t>(t.levels()) + 1);
+  for (int c : t.fold_order()) by_level[B.lev(c)].push_back(c);
+  std::vector<int> fold_pos(static_cast<std::size_t>(nc), nc - 1);
+  for (std::size_t k = 0; k < t.fold_order().size(); ++k) fold_pos[t.fold_order()[k]] = static_cast<int>(k);
+  auto& T = P.gemm_terms;
+
+  // Fold (hsc.cpp:473-526), level by level.
+  for (int l = 1; l <= t.levels() - 1; ++l) {
+    const auto& xs = by_level[l];
+    B.open(K_INVERSE, 0, l);
+    for (int pass = 0; pass < 2; ++pass)  // shared-memory-sized blocks first
+      for (int x : xs)
+        if (B.msz(x) > 0 && (B.msz(x) <= kSmemInvMax) == (pass == 0)) {
+          P.inv_tasks.push_back(InvTask{B.msz(x), x, fold_pos[x], 0, B.I(x).off_d});
+          B.cur.cmul += double(B.msz(x)) * B.msz(x) * B.msz(x);
+        }
+    B.close();
+    B.open(K_GEMM, 0, l);  // Psi_x = -inv_x A_{x,S(x)}
+    for (int x : xs) {
+      const ClusterInfo& I = B.I(x);
+      if (!I.K) continue;
+      const int tb = static_cast<int>(T.size());
+      B.add_term(T, I.m, OP_N, I.off_d, I.m, OP_N, I.off_arow, I.K, -1);
+      B.gemm_task(I.m, I.K, I.off_psi, I.K, MODE_SET, 0, 0, tb);
+    }
+    B.close();
+    // Schur: A_{jp,jq} += Psi_{x,jp}^T A_{x,jq}, p <= q; one task per target,
+    // contributions in ascending x (fold order within the level).
+    std::map<std::pair<int, int>, std::vector<std::array<int, 3>>> targets;
+    for (int x : xs) {
+      const auto& js = B.I(x).S;
+      for (std::size_t p = 0; p < js.size(); ++p)
+        for (std::size_t q = p; q < js.size(); ++q)
+          targets[{js[p], js[q]}].push_back({x, static_cast<int>(p), static_cast<int>(q)});
+    }
+    B.open(K_GEMM, 0, l);
+    for (const auto& kv : targets) {
+      const int jp = kv.first.first, jq = kv.first.second;
+      const ClusterInfo& J = B.I(jp);
+      const int tb = static_cast<int>(T.size());
+      for (const auto& c3 : kv.second) {
+        const ClusterInfo& X = B.I(c3[0]);
+        B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N, X.off_arow + X.s_col[c3[2]],
+                   X.K, +1);
+      }
+      if (jp == jq) B.gemm_task(J.m, J.m, J.off_d, J.m, MODE_ADD, 0, 0, tb);
+      else {
+        const int p = find_pos(J.S, jq);
+        if (p < 0) fail(kInternal, "plan: fill block missing from S");
+        B.gemm_task(J.m, B.msz(jq), J.off_arow + J.s_col[p], J.K, MODE_ADD, 0, 0, tb);
+      }
+    }
+    B.close();
+  }
+  B.open(K_INVERSE, 0, t.levels());
+  if (B.msz(root) > 0) {
+    P.inv_tasks.push_back(InvTask{B.msz(root), root, nc - 1, 0, B.I(root).off_d});
+    B.cur.cmul += double(B.msz(root)) * B.msz(root) * B.msz(root);
+  }
+  B.close();
+  P.exec_inv_cmul = 0;
+  for (const auto& iv : P.inv_tasks) P.exec_inv_cmul += double(iv.m) * iv.m * iv.m;
+
+  // G^r extraction top-down (hsc.cpp:171-227).
+  for (int l = t.levels() - 1; l >= 1; --l) {
+    const auto& xs = by_level[l];
+    B.open(K_GEMM, 1, l);
+    for (int x : xs) {
+      const ClusterInfo& X = B.I(x);
+      for (std::size_t jj = 0; jj < X.gcols.size(); ++jj) {
+        const int j = X.gcols[jj];
+        const int tb = static_cast<int>(T.size());
+        for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
+          const int k = X.S[kk];
+          const int64_t a = X.off_psi + X.s_col[kk];
+          if (k == j) B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N, B.I(j).off_gd, B.msz(j), +1);
+          else if (B.lev(k) < B.lev(j))
+            B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N,
+                       B.I(k).off_grow + B.col_of(B.I(k).gcols, B.I(k).gcol_off, j), B.I(k).WG, +1);
+          else
+            B.add_term(T, B.msz(k), OP_N, a, X.K, OP_T,
+                       B.I(j).off_grow + B.col_of(B.I(j).gcols, B.I(j).gcol_off, k), B.I(j).WG, +1);
+        }
+        B.gemm_task(X.m, B.msz(j), X.off_grow + X.gcol_off[jj], X.WG, MODE_SET, 0, 0, tb);
+      }
+    }
+    B.close();
+    B.open(K_GEMM, 1, l);  // full diagonal blocks
+    for (int x : xs) {
+      const ClusterInfo& X = B.I(x);
+      if (!X.full_g) continue;
+      const int tb = static_cast<int>(T.size());
+      for (std::size_t kk = 0; kk < X.S.size(); ++kk)
+        B.add_term(T, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_T,
+                   X.off_grow + B.col_of(X.gcols, X.gcol_off, X.S[kk]), X.WG, +1);
+      B.gemm_task(X.m, X.m, X.off_gd, X.m, MODE_INIT, X.off_d, X.m, tb);
+    }
+    B.close();
+    B.open(K_DIAG, 1, l);  // diagonal entries only (never-referenced, unseeded)
+    for (int x : xs) {
+      const ClusterInfo& X = B.I(x);
+      if (X.full_g || X.m == 0) continue;
+      DiagTask dt{};
+      dt.m = X.m;
+      dt.init_stride = X.m + 1;
+      dt.has_init = 1;
+      dt.out_off = X.off_gd;
+      dt.init_off = X.off_d;
+      dt.term_begin = static_cast<int>(P.diag_terms.size());
+      for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
+        B.add_term(P.diag_terms, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_T,
+                   X.off_grow + B.col_of(X.gcols, X.gcol_off, X.S[kk]), X.WG, +1);
+        B.cur.cmul += double(X.m) * B.msz(X.S[kk]);
+      }
+      dt.term_count = static_cast<int>(P.diag_terms.size()) - dt.term_begin;
+      P.diag_tasks.push_back(dt);
+    }
+    B.close();
+  }
+
+  if (P.any_seed) {
+    // Seeds N = Sigma^<_x conj(G_x.) (hsc.cpp:229-237), all clusters at once.
+    B.open(K_GEMM, 2, 0);
+    for (int x = 0; x < nc; ++x) {
+      const ClusterInfo& X = B.I(x);
+      if (!X.seeded || !X.seed_dense || X.m == 0) continue;
+      int tb = static_cast<int>(T.size());
+      B.add_term(T, X.m, OP_N, X.off_sig, X.m, OP_C, X.off_gd, X.m, +1);
+      B.gemm_task(X.m, X.m, X.off_nd, X.m, MODE_SET, 0, 0, tb);
+      if (X.WN) {
+        tb = static_cast<int>(T.size());
+        B.add_term(T, X.m, OP_N, X.off_sig, X.m, OP_C, X.off_grow, X.WG, +1);
+        B.gemm_task(X.m, X.WN, X.off_nrow, X.WN, MODE_SET, 0, 0, tb);
+      }
+    }
+    B.close();
+    B.open(K_SCALE, 2, 0);
+    for (int x = 0; x < nc; ++x) {
+      const ClusterInfo& X = B.I(x);
+      if (!X.seeded || X.seed_dense || X.m == 0) continue;
+      P.scale_tasks.push_back(ScaleTask{X.m, X.m, X.m, X.m, X.off_gd, X.off_nd, X.off_sig});
+      B.cur.cmul += double(X.m) * X.m;
+      if (X.WN) {
+        P.scale_tasks.push_back(ScaleTask{X.m, X.WN, X.WG, X.WN, X.off_grow, X.off_nrow, X.off_sig});
+        B.cur.cmul += double(X.m) * X.WN;
+      }
+    }
+    B.close();
+    // N fold bottom-up (hsc.cpp:246-266).
+    for (int l = 1; l <= t.levels() - 1; ++l) {
+      std::map<std::pair<int, int>, std::vector<std::array<int, 3>>> targets;
+      for (int x : by_level[l]) {
+        const ClusterInfo& X = B.I(x);
+        if (X.ncols.empty()) continue;
+        for (std::size_t jj = 0; jj < X.S.size(); ++jj)
+          for (std::size_t kk = 0; kk < X.ncols.size(); ++kk) {
+            const int j = X.S[jj], k = X.ncols[kk];
+            if (B.lev(k) < B.lev(j)) continue;
+            targets[{j, k}].push_back({x, static_cast<int>(jj), static_cast<int>(kk)});
+          }
+      }
+      B.open(K_GEMM, 3, l);
+      for (const auto& kv : targets) {
+        const int j = kv.first.first, k = kv.first.second;
+        const ClusterInfo& J = B.I(j);
+        const int tb = static_cast<int>(T.size());
+        for (const auto& c3 : kv.second) {
+          const ClusterInfo& X = B.I(c3[0]);
+          B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N,
+                     X.off_nrow + X.ncol_off[c3[2]], X.WN, +1);
+        }
+        if (k == j) B.gemm_task(J.m, J.m, J.off_nd, J.m, MODE_ADD, 0, 0, tb);
+        else B.gemm_task(J.m, B.msz(k), J.off_nrow + B.col_of(J.ncols, J.ncol_off, k), J.WN, MODE_ADD, 0, 0, tb);
+      }
+      B.close();
+    }
+    // P = G^< extraction top-down (hsc.cpp:190-208, 275-319).
+    B.open(K_GEMM, 4, t.levels());
+    {
+      const ClusterInfo& R = B.I(root);
+      if (R.has_nd && R.m > 0) {
+        const int tb = static_cast<int>(T.size());
+        B.add_term(T, R.m, OP_N, R.off_d, R.m, OP_N, R.off_nd, R.m, +1);
+        B.gemm_task(R.m, R.m, R.off_pd, R.m, MODE_SET, 0, 0, tb);
+      }
+    }
+    B.close();
+    for (int l = t.levels() - 1; l >= 1; --l) {
+      const auto& xs = by_level[l];
+      B.open(K_GEMM, 4, l);
+      for (int x : xs) {
+        const ClusterInfo& X = B.I(x);
+        for (std::size_t jj = 0; jj < X.pcols.size(); ++jj) {
+          const int j = X.pcols[jj];
+          const int tb = static_cast<int>(T.size());
+          const int np = find_pos(X.ncols, j);
+          if (np >= 0) B.add_term(T, X.m, OP_N, X.off_d, X.m, OP_N, X.off_nrow + X.ncol_off[np], X.WN, +1);
+          for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
+            const int k = X.S[kk];
+            const int64_t a = X.off_psi + X.s_col[kk];
+            if (k == j) B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N, B.I(j).off_pd, B.msz(j), +1);
+            else if (B.lev(k) < B.lev(j))
+              B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N,
+                         B.I(k).off_prow + B.col_of(B.I(k).pcols, B.I(k).pcol_off, j), B.I(k).WP, +1);
+            else
+              B.add_term(T, B.msz(k), OP_N, a, X.K, OP_H,
+                         B.I(j).off_prow + B.col_of(B.I(j).pcols, B.I(j).pcol_off, k), B.I(j).WP, -1);
+          }
+          B.gemm_task(X.m, B.msz(j), X.off_prow + X.pcol_off[jj], X.WP, MODE_SET, 0, 0, tb);
+        }
+      }
+      B.close();
+      B.open(K_GEMM, 4, l);
+      for (int x : xs) {
+        const ClusterInfo& X = B.I(x);
+        if (!X.full_p) continue;
+        const int tb = static_cast<int>(T.size());
+        if (X.has_nd) B.add_term(T, X.m, OP_N, X.off_d, X.m, OP_N, X.off_nd, X.m, +1);
+        for (std::size_t kk = 0; kk < X.S.size(); ++kk)
+          B.add_term(T, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_H,
+                     X.off_prow + B.col_of(X.pcols, X.pcol_off, X.S[kk]), X.WP, -1);
+        B.gemm_task(X.m, X.m, X.off_pd, X.m, MODE_SET, 0, 0, tb);
+      }
+      B.close();
+      B.open(K_DIAG, 4, l);
+      for (int x : xs) {
+        const ClusterInfo& X = B.I(x);
+        if (X.full_p || X.m == 0) continue;
+        DiagTask dt{};
+        dt.m = X.m;
+        dt.init_stride = 0;
+        dt.has_init = 0;
+        dt.out_off = X.off_pd;
+        dt.term_begin = static_cast<int>(P.diag_terms.size());
+        if (X.has_nd) {
+          B.add_term(P.diag_terms, X.m, OP_N, X.off_d, X.m, OP_N, X.off_nd, X.m, +1);
+          B.cur.cmul += double(X.m) * X.m;
+        }
+        for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
+          B.add_term(P.diag_terms, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_H,
+                     X.off_prow + B.col_of(X.pcols, X.pcol_off, X.S[kk]), X.WP, -1);
+          B.cur.cmul += double(X.m) * B.msz(X.S[kk]);
+        }
+        dt.term_count = static_cast<int>(P.diag_terms.size()) - dt.term_begin;
+        P.diag_tasks.push_back(dt);
+      }
+      B.close();
+    }
+  }
+
+  // ---- reference ledger (lean mode, dense.hpp charges)
+  {
+    Ledger& f = P.ref_fold;
+    for (int i : t.fold_order()) {
+      const int64_t m = B.msz(i);
+      f.inverse_ops += m * m * m;
+      const auto& js = B.I(i).S;
+      for (int j : js) f.multiply_ops += m * m * B.msz(j);
+      for (std::size_t p = 0; p < js.size(); ++p)
+        for (std::size_t q = p; q < js.size(); ++q) f.multiply_ops += int64_t(B.msz(js[p])) * m * B.msz(js[q]);
+    }
+    f.inverse_ops += int64_t(B.msz(root)) * B.msz(root) * B.msz(root);
+    Ledger& g = P.ref_gless;
+    int64_t sum_anc_cache = 0;
+    (void)sum_anc_cache;
+    for (int x = 0; x < nc; ++x) {
+      const int64_t m = B.msz(x);
+      int64_t wanc = 0;
+      for (int j : t.cluster(x).anc) wanc += B.msz(j);
+      if (x != root) {
+        for (int k : B.I(x).S) {
+          g.multiply_ops += m * B.msz(k) * wanc;  // rows
+          g.multiply_ops += m * B.msz(k) * m;     // diagonal
+        }
+      }
+      if (B.I(x).seeded) {
+        if (B.I(x).seed_dense) g.multiply_ops += m * m * m + m * m * wanc;
+        else g.multiply_ops += m * m + m * wanc;
+      }
+    }
+    if (P.any_seed) {
+      for (int i : t.fold_order()) {
+        const auto& ncl = B.I(i).ncols;
+        for (int j : B.I(i).S)
+          for (int k : ncl)
+            if (B.lev(k) >= B.lev(j)) g.multiply_ops += int64_t(B.msz(j)) * B.msz(i) * B.msz(k);
+      }
+      for (int x = 0; x < nc; ++x) {
+        const int64_t m = B.msz(x);
+        const ClusterInfo& X = B.I(x);
+        if (x == root) {
+          if (X.has_nd) g.multiply_ops += m * m * m;
+          continue;
+        }
+        for (int j : t.cluster(x).anc) {
+          if (find_pos(X.ncols, j) >= 0) g.multiply_ops += m * m * B.msz(j);
+          for (int k : X.S) g.multiply_ops += m * B.msz(k) * B.msz(j);
+        }
+        if (X.has_nd) g.multiply_ops += m * m * m;
+        for (int k : X.S) g.multiply_ops += m * B.msz(k) * m;
+      }
+    }
+  }
+  return P;
+}
+
+}  // namespace negfb

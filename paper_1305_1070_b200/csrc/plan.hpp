@@ -1,0 +1,186 @@
+// Host plan: everything about one device that does not depend on the energy.
+//
+// Built once (reference analogue: build_tree + the structural half of
+// group_by_partition / hsc_fold / LeanSolver, proj/src/run.cpp:123-133,
+// block.cpp:49-82, hsc.cpp:131-327,447-534) and replayed for every energy
+// batch:
+//   * the separator tree (tree.hpp, bit-exact with the reference),
+//   * the symbolic fold: fill sets S(i) (hsc.cpp:482-511),
+//   * the needed-block closure for the top-down sweeps (SURVEY App. A.4,
+//     generalised to the exact transitive rule),
+//   * the per-energy HBM arena layout of every block,
+//   * the level-synchronous task lists (inverse / grouped GEMM / diagonal
+//     dot / seed scaling) in a deterministic order,
+//   * the reference's operation ledger (dense.hpp:69-82 rules) and the
+//     executed (needed-only) ledger that is the roofline numerator.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "tree.hpp"
+
+namespace negfb {
+
+struct ProblemDesc {
+  int n = 0;
+  // Energy-independent Hamiltonian, COO (duplicates summed).
+  std::vector<int> h_rows, h_cols;
+  std::vector<cplx> h_vals;
+  // Energy-dependent retarded self-energy pattern (values per energy):
+  // A(E) = E I - H - Sigma^r(E)  (block.cpp:123-161).
+  std::vector<int> sr_rows, sr_cols;
+  // Lesser self-energy pattern; must be cluster-block-diagonal.
+  std::vector<int> sl_rows, sl_cols;
+  // Partition inputs (run.cpp:113-133) ...
+  std::vector<std::array<double, 2>> coords;
+  std::vector<std::vector<int>> atomic_groups;
+  int max_leaf = 64;
+  // ... or an explicit tree (parent per cluster + dof lists).
+  bool explicit_tree = false;
+  std::vector<int> tree_parent;
+  std::vector<std::vector<int>> tree_dofs;
+};
+
+// Operand transforms.
+enum : int { OP_N = 0, OP_T = 1, OP_C = 2, OP_H = 3 };
+// Epilogue modes.
+enum : int { MODE_SET = 0, MODE_ADD = 1, MODE_INIT = 2 };
+
+// One output block C (m x n) = [Init +] sum_t sign_t op(A_t) op(B_t).
+// Offsets are complex-element offsets inside one energy's arena.
+struct GemmTask {
+  int m, n;
+  int ldc;
+  int mode;
+  int64_t c_off;
+  int64_t init_off;
+  int ld_init;
+  int term_begin, term_count;
+};
+
+struct GemmTerm {
+  int k;
+  int a_op;        // OP_N: A stored m x k; OP_T: stored k x m
+  int b_op;        // OP_N/OP_C: stored k x n; OP_T/OP_H: stored n x k
+  int sign;        // +1 / -1
+  int lda, ldb;
+  int64_t a_off, b_off;
+};
+
+// CTA tile of a grouped GEMM launch.
+struct GemmTile {
+  int task;
+  int m0, n0;
+  int pad;
+};
+
+// Diagonal-only output: out[a] = [init[a*init_stride]] + sum_t sign_t
+// sum_b A_t[a][b] * opB_t[b][a]   (a < m).
+struct DiagTask {
+  int m;
+  int init_stride;   // m+1 when init is a full m x m block, 1 for a vector
+  int has_init;
+  int term_begin, term_count;
+  int pad;
+  int64_t out_off;   // vector of m
+  int64_t init_off;
+};
+
+// dst[a][b] = sig[a] * conj(src[a][b]), a < m, b < n (diagonal Sigma^< seed).
+struct ScaleTask {
+  int m, n;
+  int ld_src, ld_dst;
+  int64_t src_off, dst_off, sig_off;
+};
+
+struct InvTask {
+  int m;
+  int cluster;
+  int fold_pos;   // position in fold order (root = nc-1): error precedence
+  int pad;
+  int64_t off;
+};
+
+enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3 };
+
+struct Op {
+  int kind;
+  int begin, count;  // range in the kind's array (tiles for K_GEMM)
+  int task_begin, task_count;  // K_GEMM: task range (for accounting)
+  int phase;         // 0 fold, 1 G, 2 seed, 3 N fold, 4 P
+  int level;
+  double cmul;       // executed complex multiply-adds per energy
+};
+
+struct Ledger {
+  int64_t multiply_ops = 0;
+  int64_t inverse_ops = 0;
+};
+
+struct ClusterInfo {
+  int m = 0;
+  std::vector<int> S;                 // fill set, nearest first (Psi list)
+  std::vector<int64_t> s_col;         // column offset of each S entry in Arow/Psi
+  int K = 0;                          // sum of |S|
+  bool referenced = false, seeded = false, seed_dense = false;
+  bool full_g = false, full_p = false, has_nd = false;
+  std::vector<int> gcols, ncols, pcols;          // anc order
+  std::vector<int64_t> gcol_off, ncol_off, pcol_off;
+  int WG = 0, WN = 0, WP = 0;
+  int64_t off_d = -1, off_arow = -1, off_psi = -1, off_sig = -1;
+  int64_t off_gd = -1, off_grow = -1, off_nd = -1, off_nrow = -1, off_pd = -1, off_prow = -1;
+};
+
+struct Plan {
+  ProblemDesc desc;
+  Tree tree;
+  Graph graph;
+  std::vector<ClusterInfo> ci;
+
+  int64_t arena = 0;         // complex elements per energy
+  int64_t a_region = 0;      // [0, a_region): D + Arow (template copied per energy)
+  int64_t z_begin = 0, z_end = 0;  // region zeroed per energy (Sigma^<, N, root P)
+  std::vector<cplx> a_template;    // a_region values of -H (no E, no Sigma)
+
+  // Per-energy scatter maps.
+  std::vector<int64_t> diag_pos;          // n: A_dd position (E added)
+  // Sigma^r: unique target slots, each summing its pattern entries.
+  std::vector<int64_t> sr_slot_pos;       // slot -> arena position (subtract)
+  std::vector<int> sr_slot_ptr, sr_slot_src;  // CSR slot -> pattern indices
+  // Sigma^<: same, into the Sig blocks.
+  std::vector<int64_t> sl_slot_pos;
+  std::vector<int> sl_slot_ptr, sl_slot_src;
+  std::vector<int> sl_cluster;            // per slot: its cluster
+  std::vector<int> sl_partner;            // per slot: slot of (c,r) or -1
+  std::vector<int> sl_cidx;               // per slot: index into seeded_ids
+  std::vector<int> seeded_ids;            // clusters carrying a Sigma^< block
+  // Output maps: per dof, position of its diagonal entry in Gd / Pd.
+  std::vector<int64_t> out_gr_pos, out_gl_pos;
+  bool any_seed = false;
+
+  std::vector<GemmTask> gemm_tasks;
+  std::vector<GemmTerm> gemm_terms;
+  std::vector<GemmTile> gemm_tiles;
+  std::vector<DiagTask> diag_tasks;
+  std::vector<GemmTerm> diag_terms;
+  std::vector<ScaleTask> scale_tasks;
+  std::vector<InvTask> inv_tasks;
+  std::vector<Op> ops;
+
+  Ledger ref_fold, ref_gless;   // reference ledger per energy (hsc_fold / hsc_gless)
+  double exec_cmul = 0.0;       // executed complex MACs per energy (incl. inversions m^3)
+  double exec_inv_cmul = 0.0;
+  int max_block = 0;
+};
+
+constexpr int kSmemInvMax = 112;  // largest block inverted wholly in shared memory
+constexpr int kTileM = 32;
+constexpr int kTileN = 32;
+
+Plan build_plan(ProblemDesc desc);
+
+}  // namespace negfb

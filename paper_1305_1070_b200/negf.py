@@ -1,0 +1,512 @@
+"""Host-side API of the B200 HSC path, over the C ABI in include/negf_gpu.h.
+
+Mirrors the reference's solver interface for this path (names, argument
+meaning, error types):
+
+* ``nested_dissection`` / ``SeparatorTree``  -- proj/include/negf/partition.hpp:19-87
+* ``HscPlan``  -- build_tree + the structural analysis of hsc_fold/hsc_gless
+  (proj/src/run.cpp:123-133, hsc.cpp), incl. the reference FlopLedger counts
+* ``HscGpuSolver.solve`` -- solve_energy's HSC branch for a batch of energies
+  (run.cpp:141-192): diag G^r, diag G^< per dof, plus the electron_density
+  energy sum (observables.cpp:58-93)
+* exceptions -- proj/include/negf/errors.hpp:15-74
+
+There is no CPU fallback: if ``libnegf_b200.so`` is missing this module fails
+to import, and without a GPU ``HscGpuSolver`` raises ``CudaError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnegf_b200.so")
+
+
+# ---------------------------------------------------------------------------
+# errors (errors.hpp)
+# ---------------------------------------------------------------------------
+class NegfError(RuntimeError):
+    """negf::Error"""
+
+
+class ConfigError(NegfError):
+    pass
+
+
+class ContractViolation(NegfError):
+    pass
+
+
+class SingularBlock(NegfError):
+    def __init__(self, msg: str, pivot_index: int, energy_index: int = -1, cluster: int = -1):
+        super().__init__(msg)
+        self.pivot_index = pivot_index
+        self.energy_index = energy_index
+        self.cluster = cluster
+
+
+class PartitionViolation(NegfError):
+    pass
+
+
+class NonSkewHermitianInput(NegfError):
+    def __init__(self, msg: str, energy_index: int = -1, cluster: int = -1):
+        super().__init__(msg)
+        self.energy_index = energy_index
+        self.cluster = cluster
+
+
+class ResidualTooLarge(NegfError):
+    def __init__(self, msg: str, energy_index: int = -1, dof: int = -1):
+        super().__init__(msg)
+        self.energy_index = energy_index
+        self.dof = dof
+
+
+class CudaError(NegfError):
+    pass
+
+
+class NcclError(NegfError):
+    pass
+
+
+class OutOfMemory(CudaError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# C ABI
+# ---------------------------------------------------------------------------
+class _Status(C.Structure):
+    _fields_ = [
+        ("code", C.c_int),
+        ("energy_index", C.c_int),
+        ("cluster", C.c_int),
+        ("pivot", C.c_int),
+        ("dof", C.c_int),
+        ("msg", C.c_char * 256),
+    ]
+
+
+class _Problem(C.Structure):
+    _fields_ = [
+        ("n_dofs", C.c_int),
+        ("h_nnz", C.c_int64),
+        ("h_rows", C.c_void_p),
+        ("h_cols", C.c_void_p),
+        ("h_vals", C.c_void_p),
+        ("sr_nnz", C.c_int64),
+        ("sr_rows", C.c_void_p),
+        ("sr_cols", C.c_void_p),
+        ("sl_nnz", C.c_int64),
+        ("sl_rows", C.c_void_p),
+        ("sl_cols", C.c_void_p),
+        ("coords", C.c_void_p),
+        ("n_groups", C.c_int),
+        ("group_ptr", C.c_void_p),
+        ("group_dofs", C.c_void_p),
+        ("max_leaf", C.c_int),
+        ("n_tree_clusters", C.c_int),
+        ("tree_parent", C.c_void_p),
+        ("tree_ptr", C.c_void_p),
+        ("tree_dofs", C.c_void_p),
+    ]
+
+
+class _PlanInfo(C.Structure):
+    _fields_ = [
+        ("n_dofs", C.c_int),
+        ("n_clusters", C.c_int),
+        ("levels", C.c_int),
+        ("root", C.c_int),
+        ("max_block", C.c_int),
+        ("arena_bytes_per_energy", C.c_int64),
+        ("ref_fold_mul", C.c_int64),
+        ("ref_fold_inv", C.c_int64),
+        ("ref_gless_mul", C.c_int64),
+        ("ref_gless_inv", C.c_int64),
+        ("exec_cmul", C.c_double),
+        ("exec_inv_cmul", C.c_double),
+        ("n_ops", C.c_int),
+        ("n_gemm_tasks", C.c_int),
+        ("n_gemm_tiles", C.c_int),
+        ("n_inv_tasks", C.c_int),
+    ]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA extension first "
+            "(python -m paper_1305_1070_b200.build or __graft_entry__.build())"
+        )
+    lib = C.CDLL(LIB_PATH)
+    vp, i32, i64, st = C.c_void_p, C.c_int, C.c_int64, C.POINTER(_Status)
+    sig = {
+        "negf_plan_create": ([C.POINTER(_Problem), C.POINTER(vp), st], i32),
+        "negf_plan_info_get": ([vp, C.POINTER(_PlanInfo)], i32),
+        "negf_plan_tree": ([vp, vp, vp, vp, vp, vp], i32),
+        "negf_plan_fill": ([vp, vp, vp], i32),
+        "negf_plan_destroy": ([vp], None),
+        "negf_gpu_create": ([vp, i32, i32, C.POINTER(vp), st], i32),
+        "negf_gpu_batch_capacity": ([vp], i32),
+        "negf_gpu_solve_batch": ([vp, i32, vp, vp, vp, vp, i32, vp, vp, st], i32),
+        "negf_gpu_solve_batch_device": ([vp, i32, vp, vp, vp, vp, i32, vp, vp, i32, st], i32),
+        "negf_gpu_check": ([vp, st], i32),
+        "negf_gpu_density": ([vp, vp, i32, st], i32),
+        "negf_gpu_stream": ([vp], vp),
+        "negf_gpu_density_device": ([vp], vp),
+        "negf_gpu_last_launches": ([vp], i64),
+        "negf_gpu_destroy": ([vp], None),
+        "negf_nccl_unique_id": ([vp, st], i32),
+        "negf_gpu_nccl_init": ([vp, vp, i32, i32, st], i32),
+        "negf_gpu_allreduce_density": ([vp, st], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+_lib = _load()
+ABI_SYMBOLS = (
+    "negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_destroy "
+    "negf_gpu_create negf_gpu_batch_capacity negf_gpu_solve_batch negf_gpu_solve_batch_device "
+    "negf_gpu_check negf_gpu_density negf_gpu_stream negf_gpu_density_device "
+    "negf_gpu_last_launches negf_gpu_destroy negf_nccl_unique_id negf_gpu_nccl_init "
+    "negf_gpu_allreduce_density"
+).split()
+
+
+def _raise(st: _Status) -> None:
+    code, msg = st.code, st.msg.decode(errors="replace")
+    if code == 0:
+        return
+    if code == 1:
+        raise SingularBlock(msg, st.pivot, st.energy_index, st.cluster)
+    if code == 2:
+        raise NonSkewHermitianInput(msg, st.energy_index, st.cluster)
+    if code == 3:
+        raise ContractViolation(msg)
+    if code == 5:
+        raise NcclError(msg)
+    if code == 6:
+        raise OutOfMemory(msg)
+    if code == 7:
+        raise ConfigError(msg)
+    if code == 8:
+        raise PartitionViolation(msg)
+    if code == 9:
+        raise ResidualTooLarge(msg, st.energy_index, st.dof)
+    if code == 4:
+        raise CudaError(msg)
+    raise NegfError(msg)
+
+
+def _ptr(a: np.ndarray | None) -> int | None:
+    return None if a is None else a.ctypes.data
+
+
+# ---------------------------------------------------------------------------
+# problem description
+# ---------------------------------------------------------------------------
+@dataclass
+class Problem:
+    """Inputs of build_tree/solve_energy (run.cpp:123-192).
+
+    A(E) = E I - H - Sigma^r(E); Sigma^r(E) and Sigma^<(E) have fixed patterns
+    (sr_*/sl_*), their values come per energy from ``self_energies``.
+    """
+
+    n: int
+    h_rows: np.ndarray
+    h_cols: np.ndarray
+    h_vals: np.ndarray
+    sr_rows: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    sr_cols: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    sl_rows: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    sl_cols: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    coords: np.ndarray | None = None
+    atomic_groups: Sequence[Sequence[int]] = ()
+    max_leaf: int = 64
+    tree_parent: Sequence[int] | None = None
+    tree_dofs: Sequence[Sequence[int]] | None = None
+    layers: Sequence[Sequence[int]] = ()
+
+    def c_struct(self):
+        keep = []
+
+        def arr(x, dt):
+            if x is None:
+                return None
+            a = np.ascontiguousarray(np.asarray(x), dtype=dt)
+            keep.append(a)
+            return a
+
+        p = _Problem()
+        p.n_dofs = int(self.n)
+        hr, hc = arr(self.h_rows, np.int32), arr(self.h_cols, np.int32)
+        hv = arr(self.h_vals, np.complex128)
+        p.h_nnz, p.h_rows, p.h_cols, p.h_vals = len(hr), _ptr(hr), _ptr(hc), _ptr(hv)
+        sr, sc = arr(self.sr_rows, np.int32), arr(self.sr_cols, np.int32)
+        p.sr_nnz, p.sr_rows, p.sr_cols = len(sr), _ptr(sr), _ptr(sc)
+        lr, lc = arr(self.sl_rows, np.int32), arr(self.sl_cols, np.int32)
+        p.sl_nnz, p.sl_rows, p.sl_cols = len(lr), _ptr(lr), _ptr(lc)
+        p.coords = _ptr(arr(self.coords, np.float64)) if self.coords is not None else None
+        groups = [np.asarray(g, np.int32) for g in self.atomic_groups]
+        gptr = arr(np.cumsum([0] + [len(g) for g in groups]), np.int32)
+        gd = arr(np.concatenate(groups) if groups else np.zeros(0, np.int32), np.int32)
+        p.n_groups, p.group_ptr, p.group_dofs = len(groups), _ptr(gptr), _ptr(gd)
+        p.max_leaf = int(self.max_leaf)
+        if self.tree_parent is not None:
+            tp = arr(self.tree_parent, np.int32)
+            td = [np.asarray(d, np.int32) for d in self.tree_dofs]
+            tptr = arr(np.cumsum([0] + [len(d) for d in td]), np.int32)
+            tdd = arr(np.concatenate(td) if td else np.zeros(0, np.int32), np.int32)
+            p.n_tree_clusters, p.tree_parent, p.tree_ptr, p.tree_dofs = len(tp), _ptr(tp), _ptr(tptr), _ptr(tdd)
+        return p, keep
+
+
+@dataclass
+class SeparatorTree:
+    """partition.hpp:19-68 view of a plan's tree."""
+
+    parent: np.ndarray
+    level: np.ndarray
+    dofs: list
+    fold_order: np.ndarray
+
+    @property
+    def num_clusters(self) -> int:
+        return len(self.parent)
+
+    @property
+    def root(self) -> int:
+        return int(np.nonzero(self.parent == -1)[0][0])
+
+    @property
+    def levels(self) -> int:
+        return int(self.level.max())
+
+    def ancestors(self, c: int) -> list:
+        out = []
+        p = int(self.parent[c])
+        while p != -1:
+            out.append(p)
+            p = int(self.parent[p])
+        return out
+
+    def to_dict(self) -> dict:
+        return {
+            "levels": self.levels,
+            "num_dofs": int(sum(len(d) for d in self.dofs)),
+            "clusters": [
+                {"id": i, "level": int(self.level[i]), "parent": int(self.parent[i]), "dofs": [int(x) for x in self.dofs[i]]}
+                for i in range(self.num_clusters)
+            ],
+        }
+
+
+@dataclass
+class PlanInfo:
+    n_dofs: int
+    n_clusters: int
+    levels: int
+    root: int
+    max_block: int
+    arena_bytes_per_energy: int
+    ref_fold_mul: int
+    ref_fold_inv: int
+    ref_gless_mul: int
+    ref_gless_inv: int
+    exec_cmul: float
+    exec_inv_cmul: float
+    n_ops: int
+    n_gemm_tasks: int
+    n_gemm_tiles: int
+    n_inv_tasks: int
+
+    @property
+    def ref_ledger_flops(self) -> float:
+        """Real FP64 flops per energy under the reference ledger (8 x cmul)."""
+        return 8.0 * (self.ref_fold_mul + self.ref_fold_inv + self.ref_gless_mul + self.ref_gless_inv)
+
+    @property
+    def exec_flops(self) -> float:
+        """Real FP64 flops per energy the GPU executes (needed-only)."""
+        return 8.0 * self.exec_cmul
+
+
+class HscPlan:
+    """Host plan: tree + symbolic structure + schedule (built once)."""
+
+    def __init__(self, problem: Problem):
+        self.problem = problem
+        p, keep = problem.c_struct()
+        h = C.c_void_p()
+        st = _Status()
+        _lib.negf_plan_create(C.byref(p), C.byref(h), C.byref(st))
+        del keep
+        _raise(st)
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.negf_plan_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> PlanInfo:
+        i = _PlanInfo()
+        _lib.negf_plan_info_get(self._h, C.byref(i))
+        return PlanInfo(*[getattr(i, f[0]) for f in _PlanInfo._fields_])
+
+    def tree(self) -> SeparatorTree:
+        info = self.info()
+        nc, n = info.n_clusters, info.n_dofs
+        parent = np.zeros(nc, np.int32)
+        level = np.zeros(nc, np.int32)
+        ptr = np.zeros(nc + 1, np.int32)
+        dofs = np.zeros(n, np.int32)
+        fo = np.zeros(max(nc - 1, 1), np.int32)
+        _lib.negf_plan_tree(self._h, _ptr(parent), _ptr(level), _ptr(ptr), _ptr(dofs), _ptr(fo))
+        return SeparatorTree(parent, level, [dofs[ptr[c] : ptr[c + 1]].copy() for c in range(nc)], fo[: nc - 1])
+
+    def fill_sets(self) -> list:
+        nc = self.info().n_clusters
+        ptr = np.zeros(nc + 1, np.int32)
+        _lib.negf_plan_fill(self._h, _ptr(ptr), None)
+        ids = np.zeros(max(int(ptr[-1]), 1), np.int32)
+        _lib.negf_plan_fill(self._h, _ptr(ptr), _ptr(ids))
+        return [ids[ptr[c] : ptr[c + 1]].tolist() for c in range(nc)]
+
+
+def nested_dissection(n: int, edges: np.ndarray, atomic_groups=(), max_leaf: int = 64, coords=None) -> SeparatorTree:
+    """nested_dissection (partition.hpp:84-87) on an explicit edge list."""
+    e = np.asarray(edges, np.int32).reshape(-1, 2)
+    rows = np.concatenate([e[:, 0], e[:, 1]])
+    cols = np.concatenate([e[:, 1], e[:, 0]])
+    prob = Problem(n=n, h_rows=rows, h_cols=cols, h_vals=np.ones(len(rows), np.complex128),
+                   coords=coords, atomic_groups=atomic_groups, max_leaf=max_leaf)
+    return HscPlan(prob).tree()
+
+
+class HscGpuSolver:
+    """One GPU's arena + schedule (negf_gpu_create) and its batched solves."""
+
+    def __init__(self, plan: HscPlan, device: int = 0, max_energy_batch: int = 0):
+        self.plan = plan
+        self.n = plan.info().n_dofs
+        self.sr_nnz = len(plan.problem.sr_rows)
+        self.sl_nnz = len(plan.problem.sl_rows)
+        h = C.c_void_p()
+        st = _Status()
+        _lib.negf_gpu_create(plan.handle, int(device), int(max_energy_batch), C.byref(h), C.byref(st))
+        _raise(st)
+        self._h = h
+        self.device = device
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.negf_gpu_destroy(h)
+            self._h = None
+
+    @property
+    def capacity(self) -> int:
+        return _lib.negf_gpu_batch_capacity(self._h)
+
+    @property
+    def last_launches(self) -> int:
+        return int(_lib.negf_gpu_last_launches(self._h))
+
+    def solve(self, energies, weights, sigma_r, sigma_lesser, first_energy_index: int = 0,
+              want_diagonals: bool = True, out_gr=None, out_gless=None):
+        """Host arrays in, host arrays out (diag G^r, diag G^< per dof)."""
+        E = np.ascontiguousarray(energies, np.float64)
+        W = np.ascontiguousarray(weights, np.float64)
+        m = len(E)
+        sr = np.ascontiguousarray(sigma_r, np.complex128).reshape(m, self.sr_nnz) if self.sr_nnz else None
+        sl = np.ascontiguousarray(sigma_lesser, np.complex128).reshape(m, self.sl_nnz) if self.sl_nnz else None
+        gr = gl = None
+        if want_diagonals:
+            gr = out_gr if out_gr is not None else np.empty((m, self.n), np.complex128)
+            gl = out_gless if out_gless is not None else np.empty((m, self.n), np.complex128)
+        st = _Status()
+        _lib.negf_gpu_solve_batch(self._h, m, _ptr(E), _ptr(W), _ptr(sr), _ptr(sl), int(first_energy_index),
+                                  _ptr(gr), _ptr(gl), C.byref(st))
+        _raise(st)
+        return gr, gl
+
+    def solve_device(self, energies, weights, sigma_r, sigma_lesser, first_energy_index: int = 0,
+                     out_gr=None, out_gless=None, sync: bool = True) -> None:
+        """torch CUDA tensors in/out (inputs already resident in HBM)."""
+        dp = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+        st = _Status()
+        _lib.negf_gpu_solve_batch_device(self._h, int(energies.numel()), dp(energies), dp(weights),
+                                         dp(sigma_r), dp(sigma_lesser), int(first_energy_index),
+                                         dp(out_gr), dp(out_gless), int(bool(sync)), C.byref(st))
+        _raise(st)
+
+    def check(self) -> None:
+        st = _Status()
+        _lib.negf_gpu_check(self._h, C.byref(st))
+        _raise(st)
+
+    def density(self, reset: bool = False) -> np.ndarray:
+        """(1/2pi) sum_k w_k Im G^<_jj(E_k) over everything solved so far."""
+        out = np.empty(self.n, np.float64)
+        st = _Status()
+        _lib.negf_gpu_density(self._h, _ptr(out), int(bool(reset)), C.byref(st))
+        _raise(st)
+        return out
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(_lib.negf_gpu_stream(self._h) or 0)
+
+    def nccl_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        st = _Status()
+        _lib.negf_gpu_nccl_init(self._h, buf, int(nranks), int(rank), C.byref(st))
+        _raise(st)
+
+    def allreduce_density(self) -> None:
+        st = _Status()
+        _lib.negf_gpu_allreduce_density(self._h, C.byref(st))
+        _raise(st)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = _Status()
+    _lib.negf_nccl_unique_id(buf, C.byref(st))
+    _raise(st)
+    return buf.raw
+
+
+def trapezoid_weights(energies) -> np.ndarray:
+    """make_energy_grid (observables.cpp:14-32)."""
+    e = np.asarray(energies, np.float64)
+    if len(e) == 0:
+        raise ConfigError("energy grid must not be empty")
+    if np.any(np.diff(e) <= 0):
+        raise ConfigError("energy grid must be strictly increasing")
+    if len(e) == 1:
+        return np.ones(1)
+    w = np.empty_like(e)
+    w[0] = 0.5 * (e[1] - e[0])
+    w[1:-1] = 0.5 * (e[2:] - e[:-2])
+    w[-1] = 0.5 * (e[-1] - e[-2])
+    return w
