@@ -111,6 +111,11 @@ int negf_plan_tree(const negf_plan* p, int32_t* parent, int32_t* level, int32_t*
                    int32_t* dofs, int32_t* fold_order);
 /* Fill sets S(i) (the Psi lists, nearest ancestor first): ptr[nc+1], ids. */
 int negf_plan_fill(const negf_plan* p, int32_t* ptr, int32_t* ids);
+/* Schedule introspection: per grouped-GEMM task its m, n, summed k, phase
+ * (0 fold, 1 G^r, 2 seed, 3 N fold, 4 G^<) and level.  Arrays of
+ * n_gemm_tasks entries (negf_plan_info); any pointer may be NULL. */
+int negf_plan_gemm_tasks(const negf_plan* p, int32_t* m, int32_t* n, int64_t* k_total, int32_t* phase,
+                         int32_t* level);
 void negf_plan_destroy(negf_plan* p);
 
 /* Device side: allocates the per-energy arenas for up to max_energy_batch
@@ -144,8 +149,27 @@ int negf_gpu_check(negf_gpu* g, negf_status* st);
 int negf_gpu_density(negf_gpu* g, double* density_out, int reset, negf_status* st);
 void* negf_gpu_stream(negf_gpu* g);       /* cudaStream_t of the handle */
 void* negf_gpu_density_device(negf_gpu* g); /* double[n] accumulator (unscaled) */
+/* electron_density's Re-residual guard (observables.cpp:79-84): mode 1
+ * (default) raises NEGF_RESIDUAL_TOO_LARGE like the reference; mode 0 only
+ * records the largest |Re G^<_jj| / |G^<_jj| (DensityMap::max_real_residual). */
+int negf_gpu_set_residual_check(negf_gpu* g, int mode);
+double negf_gpu_max_real_residual(negf_gpu* g);
+
 /* Kernel launches issued by the last solve call (ours only). */
 int64_t negf_gpu_last_launches(const negf_gpu* g);
+
+/* Optional per-kernel timing: CUDA events recorded on the handle's stream
+ * around every launch of subsequent solves (a host sync is added at the end
+ * of each solve).  Totals accumulate until reset. */
+typedef struct {
+  double ms;            /* summed event time of the launches             */
+  double cmul;          /* executed complex multiply-adds (8 flops each)  */
+  int64_t launches;
+} negf_kernel_stat;
+enum { NEGF_KSTAT_GEMM = 0, NEGF_KSTAT_INVERSE = 1, NEGF_KSTAT_DIAG = 2, NEGF_KSTAT_SCALE = 3,
+       NEGF_KSTAT_ASSEMBLE = 4, NEGF_KSTAT_OUTPUT = 5, NEGF_KSTAT_COUNT = 6 };
+int negf_gpu_profile(negf_gpu* g, int enable);
+int negf_gpu_profile_read(negf_gpu* g, negf_kernel_stat* out /* [NEGF_KSTAT_COUNT] */, int reset);
 void negf_gpu_destroy(negf_gpu* g);
 
 /* NCCL: one communicator per handle, bootstrapped by the caller (e.g. a

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -138,12 +139,78 @@ struct negf_gpu {
   DevStatus* d_status = nullptr;
   void* comm = nullptr;
   int64_t launches = 0;
+  int residual_mode = 1;
+  double max_resid = 0.0;
+  // profiling
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;
+  struct Rec {
+    int kind;
+    double cmul;
+    int64_t launches;
+    int op;
+  };
+  std::vector<Rec> recs;
+  negf_kernel_stat stats[NEGF_KSTAT_COUNT] = {};
 };
 
 namespace {
 
+// Event bracket around one launch group (profiling mode only).
+struct Bracket {
+  negf_gpu* g;
+  int kind;
+  double cmul;
+  int64_t before;
+  int op;
+  Bracket(negf_gpu* gg, int k, double c, int o = -1) : g(gg), kind(k), cmul(c), before(gg->launches), op(o) {
+    if (!g->profiling) return;
+    const size_t i = 2 * g->recs.size();
+    while (g->ev.size() < i + 2) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      g->ev.push_back(e);
+    }
+    cudaEventRecord(g->ev[i], g->stream);
+  }
+  ~Bracket() {
+    if (!g->profiling) return;
+    const size_t i = 2 * g->recs.size();
+    cudaEventRecord(g->ev[i + 1], g->stream);
+    g->recs.push_back({kind, cmul, g->launches - before, op});
+  }
+};
+
+void flush_profile(negf_gpu* g) {
+  if (!g->profiling || g->recs.empty()) return;
+  cudaStreamSynchronize(g->stream);
+  static const bool verbose = [] {
+    const char* e = std::getenv("NEGF_PROFILE_VERBOSE");
+    return e && e[0] == '1';
+  }();
+  for (size_t r = 0; r < g->recs.size(); ++r) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g->ev[2 * r], g->ev[2 * r + 1]);
+    if (verbose && g->recs[r].op >= 0) {
+      const Op& op = g->plan->ops[g->recs[r].op];
+      std::fprintf(stderr, "[negf-prof] op %3d kind %d phase %d level %2d count %6d ms %9.3f TF/s %7.2f\n",
+                   g->recs[r].op, op.kind, op.phase, op.level, op.count, ms,
+                   ms > 0 ? 8.0 * g->recs[r].cmul / (ms * 1e-3) / 1e12 : 0.0);
+    }
+    negf_kernel_stat& s = g->stats[g->recs[r].kind];
+    s.ms += ms;
+    s.cmul += g->recs[r].cmul;
+    s.launches += g->recs[r].launches;
+  }
+  g->recs.clear();
+}
+
+}  // namespace
+
+namespace {
+
 void reset_status(negf_gpu* g) {
-  DevStatus h{~0ull, ~0ull, ~0ull};
+  DevStatus h{~0ull, ~0ull, ~0ull, 0ull};
   ck(cudaMemcpyAsync(g->d_status, &h, sizeof h, cudaMemcpyHostToDevice, g->stream), "status reset");
 }
 
@@ -154,14 +221,20 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
   BatchArgs b{g->arena, P.arena, nE, e_base};
   cudaStream_t s = g->stream;
   int64_t& L = g->launches;
-  launch_assemble(b, P, g->d_template, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr, g->d_sr_src,
-                  static_cast<int64_t>(P.desc.sr_rows.size()), d_sr, g->d_sl_pos, g->d_sl_ptr, g->d_sl_src,
-                  static_cast<int64_t>(P.desc.sl_rows.size()), d_sl, s, L);
-  launch_skew_check(b, d_sl, static_cast<int64_t>(P.desc.sl_rows.size()),
-                    static_cast<int>(P.sl_slot_pos.size()), g->d_sl_ptr, g->d_sl_src, g->d_sl_partner,
-                    g->d_sl_cidx, static_cast<int>(P.seeded_ids.size()), g->d_seeded, g->d_skew,
-                    g->d_status, s, L);
-  for (const Op& op : P.ops) {
+  {
+    Bracket br(g, NEGF_KSTAT_ASSEMBLE, 0.0);
+    launch_assemble(b, P, g->d_template, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr, g->d_sr_src,
+                    static_cast<int64_t>(P.desc.sr_rows.size()), d_sr, g->d_sl_pos, g->d_sl_ptr, g->d_sl_src,
+                    static_cast<int64_t>(P.desc.sl_rows.size()), d_sl, s, L);
+    launch_skew_check(b, d_sl, static_cast<int64_t>(P.desc.sl_rows.size()),
+                      static_cast<int>(P.sl_slot_pos.size()), g->d_sl_ptr, g->d_sl_src, g->d_sl_partner,
+                      g->d_sl_cidx, static_cast<int>(P.seeded_ids.size()), g->d_seeded, g->d_skew,
+                      g->d_status, s, L);
+  }
+  static const int kind_stat[4] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM, NEGF_KSTAT_DIAG, NEGF_KSTAT_SCALE};
+  for (size_t oi = 0; oi < P.ops.size(); ++oi) {
+    const Op& op = P.ops[oi];
+    Bracket br(g, kind_stat[op.kind], op.cmul * nE, static_cast<int>(oi));
     switch (op.kind) {
       case K_INVERSE:
         launch_inverse(b, g->d_inv + op.begin, P.inv_tasks.data() + op.begin, op.count, g->d_status, s, L);
@@ -177,7 +250,10 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         break;
     }
   }
-  launch_output(b, P.desc.n, g->d_gr_pos, g->d_gl_pos, d_w, d_gr, d_gl, g->d_density, g->d_status, s, L);
+  {
+    Bracket br(g, NEGF_KSTAT_OUTPUT, 0.0);
+    launch_output(b, P.desc.n, g->d_gr_pos, g->d_gl_pos, d_w, d_gr, d_gl, g->d_density, g->d_status, s, L);
+  }
   ck(cudaGetLastError(), "kernel launch");
 }
 
@@ -191,6 +267,9 @@ int collect(negf_gpu* g, negf_status* st) {
   ck(cudaMemcpyAsync(&h, g->d_status, sizeof h, cudaMemcpyDeviceToHost, g->stream), "status read");
   ck(cudaStreamSynchronize(g->stream), "stream sync");
   const unsigned long long none = ~0ull;
+  double worst;
+  std::memcpy(&worst, &h.max_resid_bits, sizeof worst);
+  g->max_resid = std::max(g->max_resid, worst);
   const long long es = h.singular_key == none ? -1 : static_cast<long long>(h.singular_key >> 40);
   const long long en = h.nonskew_key == none ? -1 : static_cast<long long>(h.nonskew_key >> 32);
   if (es >= 0 && (en < 0 || es <= en)) {
@@ -212,7 +291,7 @@ int collect(negf_gpu* g, negf_status* st) {
                           std::to_string(cluster) + " is not skew-Hermitian",
                       static_cast<int>(en), cluster);
   }
-  if (h.residual_key != none) {
+  if (h.residual_key != none && g->residual_mode != 0) {
     const int e = static_cast<int>(h.residual_key >> 32);
     const int d = static_cast<int>(h.residual_key & 0xFFFFFFFFull);
     return set_status(st, NEGF_RESIDUAL_TOO_LARGE,
@@ -317,6 +396,26 @@ int negf_plan_fill(const negf_plan* h, int32_t* ptr, int32_t* ids) {
     off += static_cast<int32_t>(ci[c].S.size());
   }
   if (ptr) ptr[ci.size()] = off;
+  return NEGF_OK;
+}
+
+int negf_plan_gemm_tasks(const negf_plan* h, int32_t* m, int32_t* n, int64_t* k_total, int32_t* phase,
+                         int32_t* level) {
+  if (!h) return NEGF_CONTRACT_VIOLATION;
+  const Plan& P = h->plan;
+  for (const Op& op : P.ops) {
+    if (op.kind != K_GEMM) continue;
+    for (int t = op.task_begin; t < op.task_begin + op.task_count; ++t) {
+      const GemmTask& tk = P.gemm_tasks[t];
+      int64_t ks = 0;
+      for (int q = tk.term_begin; q < tk.term_begin + tk.term_count; ++q) ks += P.gemm_terms[q].k;
+      if (m) m[t] = tk.m;
+      if (n) n[t] = tk.n;
+      if (k_total) k_total[t] = ks;
+      if (phase) phase[t] = op.phase;
+      if (level) level[t] = op.level;
+    }
+  }
   return NEGF_OK;
 }
 
@@ -428,6 +527,7 @@ int negf_gpu_solve_batch(negf_gpu* g, int nE, const double* energies, const doub
       DevStatus h;
       ck(cudaMemcpyAsync(&h, g->d_status, sizeof h, cudaMemcpyDeviceToHost, s), "status");
       ck(cudaStreamSynchronize(s), "sync");
+      flush_profile(g);
       if (h.singular_key != ~0ull || h.nonskew_key != ~0ull) break;
     }
     return collect(g, st);
@@ -455,6 +555,7 @@ int negf_gpu_solve_batch_device(negf_gpu* g, int nE, const double* d_E, const do
                 d_gr ? reinterpret_cast<double2*>(d_gr) + size_t(n) * e0 : nullptr,
                 d_gless ? reinterpret_cast<double2*>(d_gless) + size_t(n) * e0 : nullptr);
     }
+    flush_profile(g);
     if (sync) return collect(g, st);
     return ok(st);
   } catch (const CudaFail& f) {
@@ -485,6 +586,30 @@ int negf_gpu_density(negf_gpu* g, double* out, int reset, negf_status* st) {
   }
 }
 
+int negf_gpu_set_residual_check(negf_gpu* g, int mode) {
+  if (!g) return NEGF_CONTRACT_VIOLATION;
+  g->residual_mode = mode;
+  return NEGF_OK;
+}
+
+double negf_gpu_max_real_residual(negf_gpu* g) { return g ? g->max_resid : 0.0; }
+
+int negf_gpu_profile(negf_gpu* g, int enable) {
+  if (!g) return NEGF_CONTRACT_VIOLATION;
+  flush_profile(g);
+  g->profiling = enable != 0;
+  return NEGF_OK;
+}
+
+int negf_gpu_profile_read(negf_gpu* g, negf_kernel_stat* out, int reset) {
+  if (!g || !out) return NEGF_CONTRACT_VIOLATION;
+  flush_profile(g);
+  for (int k = 0; k < NEGF_KSTAT_COUNT; ++k) out[k] = g->stats[k];
+  if (reset)
+    for (auto& s : g->stats) s = negf_kernel_stat{};
+  return NEGF_OK;
+}
+
 void* negf_gpu_stream(negf_gpu* g) { return g ? g->stream : nullptr; }
 void* negf_gpu_density_device(negf_gpu* g) { return g ? g->d_density : nullptr; }
 int64_t negf_gpu_last_launches(const negf_gpu* g) { return g ? g->launches : 0; }
@@ -494,6 +619,7 @@ void negf_gpu_destroy(negf_gpu* g) {
   cudaSetDevice(g->device);
   if (g->comm && nccl().ok) nccl().destroy(g->comm);
   if (g->stream) cudaStreamSynchronize(g->stream);
+  for (cudaEvent_t e : g->ev) cudaEventDestroy(e);
   for (void* p : g->owned) cudaFree(p);
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;

@@ -92,6 +92,12 @@ __global__ void k_scatter_sigma_r(double2* arena, int64_t stride, const int64_t*
   }
 }
 
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
 // ---------------------------------------------------------------------------
 // Batched explicit inverse (Gauss-Jordan, row partial pivoting, in place)
 // ---------------------------------------------------------------------------
@@ -196,6 +202,495 @@ __device__ void gauss_jordan(double2* a, int m, int* perm, double2* colk, double
   }
 }
 
+// Register-resident Gauss-Jordan for m <= TR*R (one CTA per (block, energy)).
+// Thread (tr, tc) of a TR x TC grid owns rows tr + TR*i and columns
+// tc + TC*j of the block in registers; per pivot step only the pivot column
+// and the pivot row travel through shared memory (double-buffered by step
+// parity, two barriers per step).  Same pivots and singular rule as above.
+template <int TR, int R>
+__global__ void __launch_bounds__(TR * TR) k_inverse_reg(double2* arena, int64_t stride,
+                                                         const InvTask* __restrict__ tasks, int e_base,
+                                                         DevStatus* st) {
+  constexpr int NT = TR * TR, MMAX = TR * R;
+  __shared__ double2 colk[2][MMAX];
+  __shared__ double2 prow[2][MMAX], krow[MMAX];
+  __shared__ double red[NT / 32];
+  __shared__ int cur_at[MMAX], pos_of[MMAX], perm[MMAX];
+  const InvTask tk = tasks[blockIdx.x];
+  const int m = tk.m;
+  double2* g = arena + int64_t(blockIdx.y) * stride + tk.off;
+  const int tid = threadIdx.x, tr = tid / TR, tc = tid - (tid / TR) * TR;
+  double2 a[R][R];
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int r = tr + TR * i, c = tc + TR * j;
+      a[i][j] = (r < m && c < m) ? g[int64_t(r) * m + c] : make_double2(0.0, 0.0);
+      mx = fmax(mx, cabs2(a[i][j]));
+    }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((tid & 31) == 0) red[tid >> 5] = mx;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < NT / 32; ++w) mx = fmax(mx, red[w]);
+  const double thresh = 1e-13 * mx;
+  bool failed = false;
+  for (int k = 0; k < m; ++k) {
+    const int par = k & 1;
+    // 1. publish column k
+    if (tc == k % TR) {
+      const int jj = k / TR;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int r = tr + TR * i;
+#pragma unroll
+        for (int j = 0; j < R; ++j)
+          if (j == jj && r < m) colk[par][r] = a[i][j];
+      }
+    }
+    __syncthreads();
+    // 2. pivot: every warp reduces redundantly (largest |a_rk|, lowest row)
+    double best = -1.0;
+    int bi = k;
+    for (int r = k + (tid & 31); r < m; r += 32) {
+      const double v = cabs2(colk[par][r]);
+      if (v > best) {
+        best = v;
+        bi = r;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (best <= thresh) {  // uniform across the CTA
+      if (tid == 0) report_singular(st, e_base + blockIdx.y, tk.fold_pos, k);
+      failed = true;
+      break;
+    }
+    const int p = bi;
+    if (tid == 0) perm[k] = p;
+    // 3. pivot row (old row p) and old row k through shared memory
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = tr + TR * i;
+      if (r == p || r == k)
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const int c = tc + TR * j;
+          if (c < m) {
+            if (r == p) prow[par][c] = a[i][j];
+            if (r == k) krow[c] = a[i][j];
+          }
+        }
+    }
+    __syncthreads();
+    const double2 piv = colk[par][p];
+    const double2 ip = cinv(piv);
+    // 4./5. elimination on the swapped matrix: row k <- normalised old row p,
+    // row p <- old row k, then every other row r: a_r -= a_rk * pivot row.
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int r = tr + TR * i;
+      if (r >= m) continue;
+      double2 f;  // column-k value of (swapped) row r
+      if (r == k) f = piv;
+      else if (r == p) f = colk[par][k];
+      else f = colk[par][r];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int c = tc + TR * j;
+        if (c >= m) continue;
+        const double2 pr = (c == k) ? ip : cmul(prow[par][c], ip);  // normalised pivot row
+        if (r == k) {
+          a[i][j] = pr;
+        } else {
+          const double2 base_v = (r == p) ? krow[c] : a[i][j];
+          if (c == k) a[i][j] = make_double2(-(f.x * ip.x - f.y * ip.y), -(f.x * ip.y + f.y * ip.x));
+          else a[i][j] = csub(base_v, cmul(f, pr));
+        }
+      }
+    }
+    // krow is reused next step: make sure every thread consumed it.
+    __syncthreads();
+  }
+  if (failed) return;
+  // Undo the row interchanges as column interchanges, last first: the column
+  // currently at position q ends at pos_of[original].
+  if (tid == 0) {
+    for (int c = 0; c < m; ++c) cur_at[c] = c;
+    for (int k = m - 1; k >= 0; --k) {
+      const int p = perm[k];
+      const int t2 = cur_at[k];
+      cur_at[k] = cur_at[p];
+      cur_at[p] = t2;
+    }
+    for (int q = 0; q < m; ++q) pos_of[cur_at[q]] = q;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const int r = tr + TR * i, c = tc + TR * j;
+      if (r < m && c < m) g[int64_t(r) * m + pos_of[c]] = a[i][j];
+    }
+}
+
+// Blocked Gauss-Jordan (right-looking, panel width 8) for 32 < m: the same
+// pivots and singular rule as the unblocked elimination, but after each
+// 8-column panel (factored by one warp with only __syncwarp) the rest of the
+// block receives one rank-8 update R += (M_p - I_p) R_p on the FP64 tensor
+// cores (DMMA), where M_p are the panel's accumulated Gauss-Jordan columns and
+// R_p the 8 pivot rows -- three CTA barriers per 8 pivots.
+// kGlobal: the block stays in global memory (L2-resident) for m > kSmemInvMax.
+constexpr int INV_THREADS = 128;
+
+// Panel of NB columns held in registers of warp 0: lane owns rows lane+32*i.
+// Pivot rows travel by shuffles; the pivot loop is fully unrolled so every
+// column index is a compile-time constant (no dynamic register selects), and
+// candidates are compared by |z|^2 (same argmax as |z|).
+__device__ __forceinline__ double cnorm(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+__device__ __forceinline__ double2 crcp(double2 a) {
+  const double s = fmax(fabs(a.x), fabs(a.y));
+  const double x = a.x / s, y = a.y / s;
+  const double d = s * fma(x, x, y * y);
+  return make_double2(x / d, -y / d);
+}
+
+template <int RPL, int NB>
+__device__ __forceinline__ bool panel_regs(double2 (&P)[RPL][NB], int m, int k0, int kb, double thresh,
+                                           int* perm, int lane, DevStatus* st, int e_global, int fold_pos) {
+#pragma unroll
+  for (int kk = 0; kk < NB; ++kk) {
+    if (kk >= kb) break;
+    const int k = k0 + kk;
+    double best = -1.0;
+    int bi = k;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      const double mag = cnorm(P[i][kk]);
+      if (r >= k && r < m && mag > best) {
+        best = mag;
+        bi = r;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    // |u_kk| <= 1e-13 max|a| (dense.cpp:58-75); NaN never trips it.
+    if (sqrt(best) <= thresh) {
+      if (lane == 0) report_singular(st, e_global, fold_pos, k);
+      return false;
+    }
+    const int p = bi;
+    if (lane == 0) perm[k] = p;
+    const int lk = k & 31, sk = k >> 5, lp = p & 31, sp = p >> 5;
+    double2 rk[NB], pr[NB];
+#pragma unroll
+    for (int c = kk; c < NB; ++c) {  // columns < kk of rows k/p are not needed
+      double2 vk = P[0][c], vp = P[0][c];
+#pragma unroll
+      for (int i = 1; i < RPL; ++i) {
+        if (i == sk) vk = P[i][c];
+        if (i == sp) vp = P[i][c];
+      }
+      rk[c].x = __shfl_sync(0xffffffffu, vk.x, lk);
+      rk[c].y = __shfl_sync(0xffffffffu, vk.y, lk);
+      pr[c].x = __shfl_sync(0xffffffffu, vp.x, lp);
+      pr[c].y = __shfl_sync(0xffffffffu, vp.y, lp);
+    }
+#pragma unroll
+    for (int c = 0; c < kk; ++c) {
+      double2 vk = P[0][c], vp = P[0][c];
+#pragma unroll
+      for (int i = 1; i < RPL; ++i) {
+        if (i == sk) vk = P[i][c];
+        if (i == sp) vp = P[i][c];
+      }
+      rk[c].x = __shfl_sync(0xffffffffu, vk.x, lk);
+      rk[c].y = __shfl_sync(0xffffffffu, vk.y, lk);
+      pr[c].x = __shfl_sync(0xffffffffu, vp.x, lp);
+      pr[c].y = __shfl_sync(0xffffffffu, vp.y, lp);
+    }
+    const double2 ip = crcp(pr[kk]);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) pr[c] = (c == kk) ? ip : cmul(pr[c], ip);  // new row k
+    const double2 nip = make_double2(-ip.x, -ip.y);
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      const int r = lane + 32 * i;
+      if (r == k) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) P[i][c] = pr[c];
+        continue;
+      }
+      const bool was_k = (r == p);  // row p receives the old row k
+      const double2 f = was_k ? rk[kk] : P[i][kk];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        const double2 o = was_k ? rk[c] : P[i][c];
+        P[i][c] = (c == kk) ? cmul(f, nip) : csub(o, cmul(f, pr[c]));
+      }
+    }
+  }
+  return true;
+}
+
+template <bool kGlobal, int RPL, int NB>
+__global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* arena, int64_t stride,
+                                                                 const InvTask* __restrict__ tasks, int e_base,
+                                                                 DevStatus* st) {
+  extern __shared__ double2 sm[];
+  const InvTask tk = tasks[blockIdx.x];
+  const int m = tk.m;
+  const int m8 = (m + 7) & ~7;
+  const int ld = kGlobal ? m : m8 + 2;  // smem row pitch: 2 mod 8 -> conflict-free fragments
+  double2* g = arena + int64_t(blockIdx.y) * stride + tk.off;
+  // shared layout: [A (smem variant) | Rs: 8 x m8 | Pn: m8 x 8 (global variant) | ints]
+  double2* A = kGlobal ? g : sm;
+  double2* Rs = kGlobal ? sm : sm + int64_t(m8) * ld;
+  double2* Pn = Rs + 8 * (m8 + 2);
+  int* perm = reinterpret_cast<int*>(Pn + (kGlobal ? 8 * m8 : 0));
+  int* pos_of = perm + m8;
+  double* red = reinterpret_cast<double*>(pos_of + m8 + (m8 & 1));
+  int* flag = reinterpret_cast<int*>(red + INV_THREADS / 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  double mx = 0.0;
+  if (!kGlobal) {
+    for (int i = tid; i < m8 * m8; i += INV_THREADS) {
+      const int r = i / m8, c = i - r * m8;
+      const double2 v = (r < m && c < m) ? g[int64_t(r) * m + c] : make_double2(0.0, 0.0);
+      A[r * ld + c] = v;
+      mx = fmax(mx, cabs2(v));
+    }
+  } else {
+    for (int64_t i = tid; i < int64_t(m) * m; i += INV_THREADS) mx = fmax(mx, cabs2(A[i]));
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  if (tid == 0) *flag = 0;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < INV_THREADS / 32; ++w) mx = fmax(mx, red[w]);
+  const double thresh = 1e-13 * mx;
+  // element (r, c) of the block
+  auto at = [&](int r, int c) -> double2& { return A[int64_t(r) * ld + c]; };
+
+  for (int k0 = 0; k0 < m; k0 += NB) {
+    const int kb = min(NB, m - k0);
+    // ---- panel (columns k0..k0+7, all rows) on warp 0
+    double2* P = kGlobal ? Pn : nullptr;
+    auto pan = [&](int r, int c) -> double2& { return kGlobal ? P[r * 8 + c] : at(r, k0 + c); };
+    if (kGlobal) {
+      for (int i = tid; i < m8 * 8; i += INV_THREADS) {
+        const int r = i >> 3, c = i & 7;
+        P[i] = (r < m && k0 + c < m) ? at(r, k0 + c) : make_double2(0.0, 0.0);
+      }
+      __syncthreads();
+    }
+    if (!kGlobal && warp == 0) {
+      double2 Pr[RPL][NB];
+#pragma unroll
+      for (int i = 0; i < RPL; ++i)
+#pragma unroll
+        for (int c = 0; c < NB; ++c) {
+          const int r = lane + 32 * i;
+          Pr[i][c] = (r < m8) ? pan(r, c) : make_double2(0.0, 0.0);
+        }
+      if (!panel_regs<RPL, NB>(Pr, m, k0, kb, thresh, perm, lane, st, e_base + blockIdx.y, tk.fold_pos)) {
+        if (lane == 0) *flag = 1;
+      } else {
+#pragma unroll
+        for (int i = 0; i < RPL; ++i)
+#pragma unroll
+          for (int c = 0; c < NB; ++c) {
+            const int r = lane + 32 * i;
+            if (r < m) pan(r, c) = Pr[i][c];
+          }
+      }
+    } else if (kGlobal && warp == 0) {
+      for (int kk = 0; kk < kb; ++kk) {
+        const int k = k0 + kk;
+        double best = -1.0;
+        int bi = k;
+        for (int r = k + lane; r < m; r += 32) {
+          const double v = cabs2(pan(r, kk));
+          if (v > best) {
+            best = v;
+            bi = r;
+          }
+        }
+        for (int o = 16; o; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (best <= thresh) {
+          if (lane == 0) {
+            *flag = 1;
+            report_singular(st, e_base + blockIdx.y, tk.fold_pos, k);
+          }
+          break;
+        }
+        const int p = bi;
+        if (lane == 0) perm[k] = p;
+        if (lane < 8 && p != k) {
+          const double2 t2 = pan(k, lane);
+          pan(k, lane) = pan(p, lane);
+          pan(p, lane) = t2;
+        }
+        __syncwarp();
+        const double2 ip = cinv(pan(k, kk));
+        // Each lane owns rows lane, lane+32, ...: read its column-k factor
+        // before row k is rewritten, then update its rows.
+        __syncwarp();
+        if (lane < 8) pan(k, lane) = (lane == kk) ? ip : cmul(pan(k, lane), ip);
+        __syncwarp();
+        for (int r = lane; r < m; r += 32) {
+          if (r == k) continue;
+          const double2 f = pan(r, kk);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (c == kk) pan(r, c) = make_double2(-(f.x * ip.x - f.y * ip.y), -(f.x * ip.y + f.y * ip.x));
+            else pan(r, c) = csub(pan(r, c), cmul(f, pan(k, c)));
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (*flag) return;
+    // ---- row interchanges of this panel on the other columns (column-parallel)
+    for (int c = tid; c < m8; c += INV_THREADS) {
+      if ((c >= k0 && c < k0 + NB) || (kGlobal && c >= m)) {  // panel / no padding in global memory
+#pragma unroll
+        for (int kk = 0; kk < NB; ++kk) Rs[kk * (m8 + 2) + c] = make_double2(0.0, 0.0);
+        continue;
+      }
+      for (int kk = 0; kk < kb; ++kk) {
+        const int k = k0 + kk, p = perm[k];
+        if (p != k) {
+          const double2 t2 = at(k, c);
+          at(k, c) = at(p, c);
+          at(p, c) = t2;
+        }
+      }
+      // stage the (swapped) pivot rows R_p
+#pragma unroll
+      for (int kk = 0; kk < NB; ++kk) Rs[kk * (m8 + 2) + c] = (kk < kb) ? at(k0 + kk, c) : make_double2(0.0, 0.0);
+    }
+    // M_p - I_p in the panel buffer (subtract the identity on the pivot rows)
+    if (tid < kb) {
+      double2& v = pan(k0 + tid, tid);
+      v.x -= 1.0;
+    }
+    __syncthreads();
+    // ---- rank-NB update of every 8x8 subtile (panel columns keep M_p): DMMA
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int nsub_r = m8 / 8, nsub_c = m8 / 8;
+    for (int s = warp; s < nsub_r * nsub_c; s += INV_THREADS / 32) {
+      const int sr = s / nsub_c, sc = s - sr * nsub_c;
+      if (NB == 8 && sc * 8 == k0) continue;
+      const int r = sr * 8 + g8, c = sc * 8 + 2 * t4;
+      const bool in0 = !kGlobal || (r < m && c < m), in1 = !kGlobal || (r < m && c + 1 < m);
+      double cr0 = 0.0, ci0 = 0.0, cr1 = 0.0, ci1 = 0.0;
+      if (in0) {
+        const double2 v = at(r, c);
+        cr0 = v.x;
+        ci0 = v.y;
+      }
+      if (in1) {
+        const double2 v = at(r, c + 1);
+        cr1 = v.x;
+        ci1 = v.y;
+      }
+#pragma unroll
+      for (int q = 0; q < NB / 4; ++q) {
+        const double2 a = pan(r, 4 * q + t4);
+        const double2 b = Rs[(4 * q + t4) * (m8 + 2) + sc * 8 + g8];
+        dmma(cr0, cr1, a.x, b.x);
+        dmma(cr0, cr1, -a.y, b.y);
+        dmma(ci0, ci1, a.x, b.y);
+        dmma(ci0, ci1, a.y, b.x);
+      }
+      const bool pc0 = (c >= k0 && c < k0 + NB), pc1 = (c + 1 >= k0 && c + 1 < k0 + NB);
+      if (in0 && !pc0) at(r, c) = make_double2(cr0, ci0);
+      if (in1 && !pc1) at(r, c + 1) = make_double2(cr1, ci1);
+    }
+    // restore M_p in the panel columns (add the identity back) and, for the
+    // global variant, write the panel columns back
+    __syncthreads();
+    if (tid < kb) {
+      double2& v = pan(k0 + tid, tid);
+      v.x += 1.0;
+    }
+    if (kGlobal) {
+      __syncthreads();
+      for (int i = tid; i < m * 8; i += INV_THREADS) {
+        const int r = i >> 3, c = i & 7;
+        if (k0 + c < m) at(r, k0 + c) = P[i];
+      }
+    }
+    __syncthreads();
+  }
+  // Undo the row interchanges as column interchanges (last first).
+  if (tid == 0) {
+    int* cur_at = pos_of;  // reuse: first the permutation, then its inverse in Rs scratch
+    for (int c = 0; c < m; ++c) cur_at[c] = c;
+    for (int k = m - 1; k >= 0; --k) {
+      const int p = perm[k];
+      const int t2 = cur_at[k];
+      cur_at[k] = cur_at[p];
+      cur_at[p] = t2;
+    }
+    int* inv_pos = reinterpret_cast<int*>(Rs);
+    for (int q = 0; q < m; ++q) inv_pos[cur_at[q]] = q;
+    for (int q = 0; q < m; ++q) pos_of[q] = inv_pos[q];
+  }
+  __syncthreads();
+  if (!kGlobal) {
+    for (int i = tid; i < m * m; i += INV_THREADS) {
+      const int r = i / m, c = i - r * m;
+      g[int64_t(r) * m + pos_of[c]] = at(r, c);
+    }
+  } else {
+    // one warp per row: the row is held in registers while it is permuted
+    for (int r = warp; r < m; r += INV_THREADS / 32) {
+      double2 v[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int c = lane + 32 * j;
+        if (c < m) v[j] = at(r, c);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int c = lane + 32 * j;
+        if (c < m) at(r, pos_of[c]) = v[j];
+      }
+      __syncwarp();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(512) k_inverse_smem(double2* arena, int64_t stride,
                                                       const InvTask* __restrict__ tasks, int e_base,
                                                       DevStatus* st) {
@@ -240,11 +735,6 @@ constexpr int LD_RK = KC + 4;   // (row, k) layouts: stride = 4 mod 8 (conflict-
 constexpr int LD_KR = TM + 2;   // (k, row) layouts: stride = 2 mod 8
 constexpr int OPND = (TM * LD_RK > KC * LD_KR) ? TM * LD_RK : KC * LD_KR;  // complex / operand / stage
 
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -301,15 +791,8 @@ __device__ __forceinline__ void load_chunk(double2* As, double2* Bs, const doubl
   }
 }
 
-__global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride,
-                                              const GemmTask* __restrict__ tasks,
-                                              const GemmTerm* __restrict__ terms,
-                                              const GemmTile* __restrict__ tiles, int tile_begin) {
-  __shared__ __align__(16) double2 smA[2][OPND];
-  __shared__ __align__(16) double2 smB[2][OPND];
-  const GemmTile tl = tiles[tile_begin + blockIdx.x];
-  const GemmTask tk = tasks[tl.task];
-  double2* base = arena + blockIdx.y * stride;
+__device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, const GemmTerm* __restrict__ terms,
+                                          const GemmTile& tl, double2 (*smA)[OPND], double2 (*smB)[OPND]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
@@ -359,33 +842,40 @@ __global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride,
     const bool a_rk = (tm.a_op == OP_N);
     const bool b_kr = (tm.b_op == OP_N || tm.b_op == OP_C);
     const int ksteps = min(KC, tm.k - k0);
+    // Warp-uniform skips: subtiles wholly outside the task's m x n do no DMMA.
+    const int live_i = min(2, max(0, (tk.m - tl.m0 - wm + 7) / 8));
+    const int live_j = min(2, max(0, (tk.n - tl.n0 - wn + 7) / 8));
+    if (live_i > 0 && live_j > 0) {
 #pragma unroll
-    for (int s = 0; s < KC / 4; ++s) {
-      if (4 * s >= ksteps) break;
-      const int kk = 4 * s + t;
-      double2 a[2], b[2];
+      for (int s = 0; s < KC / 4; ++s) {
+        if (4 * s >= ksteps) break;
+        const int kk = 4 * s + t;
+        double2 a[2], b[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int r = wm + 8 * i + g;
-        a[i] = a_rk ? As[r * LD_RK + kk] : As[kk * LD_KR + r];
-        a[i].x *= sg;
-        a[i].y *= sg;
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int c = wn + 8 * j + g;
-        b[j] = b_kr ? Bs[kk * LD_KR + c] : Bs[c * LD_RK + kk];
-        if (conjb) b[j].y = -b[j].y;
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const double nai = -a[i].y;
+        for (int i = 0; i < 2; ++i) {
+          const int r = wm + 8 * i + g;
+          a[i] = a_rk ? As[r * LD_RK + kk] : As[kk * LD_KR + r];
+          a[i].x *= sg;
+          a[i].y *= sg;
+        }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
-          dmma(cr[i][j][0], cr[i][j][1], nai, b[j].y);
-          dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
-          dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+          const int c = wn + 8 * j + g;
+          b[j] = b_kr ? Bs[kk * LD_KR + c] : Bs[c * LD_RK + kk];
+          if (conjb) b[j].y = -b[j].y;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (i >= live_i) break;
+          const double nai = -a[i].y;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (j >= live_j) break;
+            dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+            dmma(cr[i][j][0], cr[i][j][1], nai, b[j].y);
+            dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+            dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+          }
         }
       }
     }
@@ -413,6 +903,25 @@ __global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride,
         *dst = v;
       }
     }
+  }
+}
+
+// Persistent launch: CTAs stride over (tile, energy) items, energy fastest;
+// tiles are pre-sorted by decreasing cost (longest first) in the plan.
+__global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride, int nE,
+                                              const GemmTask* __restrict__ tasks,
+                                              const GemmTerm* __restrict__ terms,
+                                              const GemmTile* __restrict__ tiles, int tile_begin,
+                                              int64_t items) {
+  __shared__ __align__(16) double2 smA[2][OPND];
+  __shared__ __align__(16) double2 smB[2][OPND];
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    const int64_t ti = w / nE;
+    const int e = static_cast<int>(w - ti * nE);
+    const GemmTile tl = tiles[tile_begin + ti];
+    const GemmTask tk = tasks[tl.task];
+    gemm_item(arena + e * stride, tk, terms, tl, smA, smB);
+    __syncthreads();
   }
 }
 
@@ -464,6 +973,7 @@ __global__ void k_output(const double2* __restrict__ arena, int64_t stride, int 
   if (d >= n) return;
   const int64_t pr = gr_pos[d], pl = gl_pos[d];
   double acc = density[d];
+  double worst = 0.0;
   for (int e = 0; e < nE; ++e) {
     const double2* a = arena + int64_t(e) * stride;
     if (gr) gr[int64_t(e) * n + d] = a[pr];
@@ -473,9 +983,11 @@ __global__ void k_output(const double2* __restrict__ arena, int64_t stride, int 
     if (fabs(v.x) > 1e-8 * mag)
       atomicMin(&st->residual_key, (static_cast<unsigned long long>(e_base + e) << 32) |
                                        static_cast<unsigned long long>(d));
+    if (mag > 0.0) worst = fmax(worst, fabs(v.x) / mag);
     acc += weights[e] * v.y;
   }
   density[d] = acc;
+  if (worst > 0.0) atomicMax(&st->max_resid_bits, static_cast<unsigned long long>(__double_as_longlong(worst)));
 }
 
 // Sigma^< skewness per cluster block (validate_sigma, hsc.cpp:108-112 with
@@ -556,30 +1068,48 @@ void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_templat
 
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
                     DevStatus* st, cudaStream_t s, int64_t& launches) {
-  // Split the level's tasks into the shared-memory and global-memory variants
-  // (tasks are pre-sorted so each variant is a contiguous range).
+  // Tasks of a level are pre-sorted by size class (see plan.cpp), so each
+  // variant below covers one contiguous range.
+  auto cls = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : m <= kSmemInvMax ? 3 : 4; };
   int i = 0;
   while (i < count) {
-    const bool small = h_tasks[i].m <= kSmemInvMax;
+    const int c = cls(h_tasks[i].m);
     int j = i;
     int mmax = 0;
-    while (j < count && (h_tasks[j].m <= kSmemInvMax) == small) {
+    while (j < count && cls(h_tasks[j].m) == c) {
       mmax = std::max(mmax, h_tasks[j].m);
       ++j;
     }
     dim3 grid(j - i, b.nE);
-    if (small) {
-      const size_t smem = 256 + size_t(mmax) * mmax * 16 + size_t(mmax) * 16 + size_t(mmax) * 4 + 16;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_inverse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
+    const int m8 = (mmax + 7) & ~7;
+    const size_t tail = size_t(8) * (m8 + 2) * 16 + size_t(2 * m8 + 2) * 4 + 64;
+    switch (c) {
+      case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st); break;
+      case 1: k_inverse_reg<8, 4><<<grid, 64, 0, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st); break;
+      case 2:
+      case 3: {
+        const size_t smem = size_t(m8) * (m8 + 2) * 16 + tail;
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_inverse_blocked<false, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+          cudaFuncSetAttribute(k_inverse_blocked<false, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+          attr = true;
+        }
+        if (mmax <= 64)
+          k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+        else
+          k_inverse_blocked<false, 4, 4><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+        break;
       }
-      const int threads = mmax <= 32 ? 128 : (mmax <= 64 ? 256 : 512);
-      k_inverse_smem<<<grid, threads, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
-    } else {
-      const size_t smem = 256 + size_t(mmax) * 16 + size_t(mmax) * 4 + 16;
-      k_inverse_global<<<grid, 1024, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+      default: {
+        const size_t smem = tail + size_t(8) * m8 * 16;
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_inverse_blocked<true, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+          attr = true;
+        }
+        k_inverse_blocked<true, 1, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+      }
     }
     ++launches;
     i = j;
@@ -590,8 +1120,17 @@ void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_
                  const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s,
                  int64_t& launches) {
   if (tile_count <= 0) return;
-  dim3 grid(tile_count, b.nE);
-  k_gemm<<<grid, 128, 0, s>>>(b.arena, b.stride, d_tasks, d_terms, d_tiles, tile_begin);
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm, 128, 0);
+    slots = std::max(1, sms * std::max(1, per_sm));
+  }
+  const int64_t items = int64_t(tile_count) * b.nE;
+  const int grid = static_cast<int>(std::min<int64_t>(items, slots));
+  k_gemm<<<grid, 128, 0, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
   ++launches;
 }
 

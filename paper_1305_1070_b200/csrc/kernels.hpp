@@ -13,6 +13,7 @@ struct DevStatus {
   unsigned long long singular_key;   // energy<<40 | fold_pos<<20 | pivot
   unsigned long long residual_key;   // energy<<32 | dof
   unsigned long long nonskew_key;    // energy<<32 | cluster
+  unsigned long long max_resid_bits; // max |Re g<|/|g<| as non-negative double bits
 };
 
 struct BatchArgs {

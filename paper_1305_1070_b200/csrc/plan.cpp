@@ -86,6 +86,19 @@ struct Builder {
       case K_DIAG: cur.count = static_cast<int>(P.diag_tasks.size()) - cur.begin; break;
       default: cur.count = static_cast<int>(P.scale_tasks.size()) - cur.begin; break;
     }
+    if (cur.kind == K_GEMM && cur.count > 1) {
+      // Longest-processing-time first: the persistent kernel strides over
+      // tiles in this order (8-granular live area x summed k).
+      auto cost = [&](const GemmTile& tl) {
+        const GemmTask& tk = P.gemm_tasks[tl.task];
+        int64_t ks = 0;
+        for (int q = tk.term_begin; q < tk.term_begin + tk.term_count; ++q) ks += P.gemm_terms[q].k;
+        const int64_t lm = std::min(kTileM, tk.m - tl.m0), ln = std::min(kTileN, tk.n - tl.n0);
+        return ((lm + 7) / 8) * ((ln + 7) / 8) * (ks + 16);
+      };
+      std::stable_sort(P.gemm_tiles.begin() + cur.begin, P.gemm_tiles.end(),
+                       [&](const GemmTile& a, const GemmTile& b) { return cost(a) > cost(b); });
+    }
     if (cur.count > 0) {
       P.ops.push_back(cur);
       P.exec_cmul += cur.cmul;
@@ -406,9 +419,10 @@ Plan build_plan(ProblemDesc desc) {
   for (int l = 1; l <= t.levels() - 1; ++l) {
     const auto& xs = by_level[l];
     B.open(K_INVERSE, 0, l);
-    for (int pass = 0; pass < 2; ++pass)  // shared-memory-sized blocks first
+    auto size_class = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : m <= kSmemInvMax ? 3 : 4; };
+    for (int pass = 0; pass < 5; ++pass)  // grouped by kernel variant
       for (int x : xs)
-        if (B.msz(x) > 0 && (B.msz(x) <= kSmemInvMax) == (pass == 0)) {
+        if (B.msz(x) > 0 && size_class(B.msz(x)) == pass) {
           P.inv_tasks.push_back(InvTask{B.msz(x), x, fold_pos[x], 0, B.I(x).off_d});
           B.cur.cmul += double(B.msz(x)) * B.msz(x) * B.msz(x);
         }

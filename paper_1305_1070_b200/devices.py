@@ -1,0 +1,293 @@
+"""Seeded synthetic devices for the BASELINE.json configurations.
+
+Input generation only (outside the drop-in boundary): each builder returns a
+``Workload`` whose ``problem`` goes to the C ABI unchanged and whose
+``self_energies(idx)`` yields the per-energy Sigma^r / Sigma^< pattern values.
+
+Conventions fixed here (the reference leaves them open):
+* dof = x * Ny + y with x the transport coordinate (layers are columns x),
+  coords = (x, y): the top separator of config 4 is then the 1024-dof column
+  the BASELINE names;
+* A(E) uses the real energy; eta lives only in the leads, as in the
+  reference (block.cpp:141-146, device.cpp:206-207);
+* random draws: std::mt19937_64(seed) + uniform01 (synthetic.hpp:18-20), onsite
+  potential first in dof order, then any further draws;
+* effective-mass leads: analytic semi-infinite uniform lead,
+  Sigma = -t sum_m phi_m phi_m^T lambda_m, lambda_m = e^{i k_m a};
+* the CNT lead: Sancho-Rubio decimation of the ideal tube (tolerance 1e-12);
+* Sigma^< = -f (Sigma - Sigma^dagger) per contact (= i f Gamma), phonon
+  Sigma^<_ph = -f_eq (s - conj s) (device.cpp:322-360); phonon self-energy is
+  zero on the two boundary layers (device.cpp:313-318).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .negf import Problem, trapezoid_weights
+from .rng import MT19937_64
+
+HBAR2_OVER_2M0 = 0.0380998  # eV nm^2 (device.hpp:20)
+
+
+def fermi(e, mu, kT):
+    x = (np.asarray(e, np.float64) - mu) / kT
+    with np.errstate(over="ignore"):
+        f = 1.0 / (1.0 + np.exp(np.clip(x, -700.0, 700.0)))
+    f = np.where(x > 700.0, 0.0, np.where(x < -700.0, 1.0, f))
+    return f
+
+
+def uniform_grid(emin: float, emax: float, count: int) -> np.ndarray:
+    """uniform_energy_grid (observables.cpp:34-49)."""
+    if count == 1:
+        return np.array([emin], np.float64)
+    step = (emax - emin) / (count - 1)
+    e = emin + step * np.arange(count, dtype=np.float64)
+    e[-1] = emax
+    return e
+
+
+@dataclass
+class Workload:
+    name: str
+    problem: Problem
+    energies: np.ndarray
+    weights: np.ndarray
+    self_energies: Callable[[np.ndarray], tuple]
+    nx: int
+    ny: int
+    description: str = ""
+
+    @property
+    def n(self) -> int:
+        return self.problem.n
+
+
+def _lead_modes(ny: int, t: float):
+    y = np.arange(1, ny + 1)
+    m = np.arange(1, ny + 1)
+    phi = np.sqrt(2.0 / (ny + 1)) * np.sin(np.outer(y, m) * np.pi / (ny + 1))  # (y, m)
+    eps = 4.0 * t - 2.0 * t * np.cos(m * np.pi / (ny + 1))
+    return phi, eps
+
+
+def analytic_lead_sigma(energy: float, eta: float, t: float, phi: np.ndarray, eps: np.ndarray) -> np.ndarray:
+    """Retarded surface self-energy of a uniform semi-infinite 2D lead."""
+    z = (eps - (energy + 1j * eta)) / (2.0 * t)
+    s = np.sqrt(z * z - 1.0 + 0j)
+    lam = z - s
+    flip = np.abs(lam) > 1.0
+    lam[flip] = (z + s)[flip]
+    sig = (phi * (-t * lam)) @ phi.T
+    return 0.5 * (sig + sig.T)  # exactly complex symmetric
+
+
+def effective_mass_device(name: str, nx: int, ny: int, a_nm: float, m_eff: float, potential: np.ndarray,
+                          energies: np.ndarray, eta: float, mu_l: float, mu_r: float, kT: float,
+                          phonon_gamma: np.ndarray | None = None, max_leaf: int = 64,
+                          description: str = "") -> Workload:
+    t = HBAR2_OVER_2M0 / (m_eff * a_nm * a_nm)
+    n = nx * ny
+    idx = np.arange(n).reshape(nx, ny)  # dof = x*ny + y
+    rows = [idx.ravel()]
+    cols = [idx.ravel()]
+    vals = [4.0 * t + potential.reshape(n)]
+    for a, b in ((idx[:-1, :], idx[1:, :]), (idx[:, :-1], idx[:, 1:])):
+        rows += [a.ravel(), b.ravel()]
+        cols += [b.ravel(), a.ravel()]
+        vals += [np.full(a.size, -t), np.full(a.size, -t)]
+    h_rows = np.concatenate(rows).astype(np.int32)
+    h_cols = np.concatenate(cols).astype(np.int32)
+    h_vals = np.concatenate(vals).astype(np.complex128)
+    coords = np.stack([np.repeat(np.arange(nx), ny), np.tile(np.arange(ny), nx)], 1).astype(np.float64)
+    left, right = idx[0], idx[-1]
+    lr, lc = np.meshgrid(left, left, indexing="ij")
+    rr, rc = np.meshgrid(right, right, indexing="ij")
+    sr_rows = [lr.ravel(), rr.ravel()]
+    sr_cols = [lc.ravel(), rc.ravel()]
+    interior = idx[1:-1].ravel()
+    if phonon_gamma is not None:
+        sr_rows.append(interior)
+        sr_cols.append(interior)
+    sr_rows = np.concatenate(sr_rows).astype(np.int32)
+    sr_cols = np.concatenate(sr_cols).astype(np.int32)
+    prob = Problem(n=n, h_rows=h_rows, h_cols=h_cols, h_vals=h_vals, sr_rows=sr_rows, sr_cols=sr_cols,
+                   sl_rows=sr_rows.copy(), sl_cols=sr_cols.copy(), coords=coords,
+                   atomic_groups=[left.tolist(), right.tolist()], max_leaf=max_leaf,
+                   layers=[idx[x].tolist() for x in range(nx)])
+    phi, eps = _lead_modes(ny, t)
+    w2 = ny * ny
+    gam = None if phonon_gamma is None else np.asarray(phonon_gamma).reshape(n)[interior]
+    mu_ph = 0.5 * (mu_l + mu_r)
+
+    def self_energies(sel):
+        sel = np.atleast_1d(np.asarray(sel))
+        nnz = len(sr_rows)
+        sr = np.zeros((len(sel), nnz), np.complex128)
+        sl = np.zeros((len(sel), nnz), np.complex128)
+        for q, k in enumerate(sel):
+            e = float(energies[k])
+            sig = analytic_lead_sigma(e, eta, t, phi, eps)  # same uniform lead on both sides
+            sr[q, :w2] = sig.ravel()
+            sr[q, w2:2 * w2] = sig.ravel()
+            for side, mu in ((0, mu_l), (1, mu_r)):
+                sl[q, side * w2:(side + 1) * w2] = (-fermi(e, mu, kT) * (sig - sig.conj().T)).ravel()
+            if gam is not None:
+                s = -1j * gam
+                sr[q, 2 * w2:] = s
+                sl[q, 2 * w2:] = -fermi(e, mu_ph, kT) * (s - np.conj(s))
+        return sr, sl
+
+    return Workload(name, prob, energies, trapezoid_weights(energies), self_energies, nx, ny, description)
+
+
+def config1() -> Workload:
+    """Single-energy ballistic 2D effective-mass device, 64 x 32 (BASELINE configs[0])."""
+    nx, ny = 64, 32
+    v = 0.1 * MT19937_64(0).uniform01(nx * ny)
+    return effective_mass_device("cfg1_em_64x32", nx, ny, 0.5, 0.067, v, np.array([0.05]), 1e-6, 0.1, 0.0,
+                                 0.025, description="2D effective mass 64x32, V~U[0,0.1] seed 0, E=0.05")
+
+
+def config2(n_energies: int = 256) -> Workload:
+    """Quantum-well superlattice 400 x 100, 256 energies in [0, 0.4] (configs[1])."""
+    nx, ny = 400, 100
+    x = np.arange(nx)
+    barrier = np.where((x // 10) % 2 == 1, 0.3, 0.0)  # 5 nm = 10 points, wells at the leads
+    v = np.repeat(barrier, ny) + (MT19937_64(1).uniform01(nx * ny) - 0.5) * 0.01
+    e = uniform_grid(0.0, 0.4, n_energies)
+    return effective_mass_device("cfg2_superlattice_400x100", nx, ny, 0.5, 0.067, v, e, 1e-6, 0.1, 0.0, 0.025,
+                                 description="superlattice 400x100, 0.3 eV barriers/wells of 5 nm, "
+                                             "+-5 meV disorder seed 1, 256 E in [0,0.4]")
+
+
+def config4(n_energies: int = 1024, nx: int = 1024, ny: int = 1024) -> Workload:
+    """Wide 1024 x 1024 device, sum of 16 Gaussians (configs[3])."""
+    r = MT19937_64(3)
+    cx = r.uniform01(16) * nx
+    cy = r.uniform01(16) * ny
+    X, Y = np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij")
+    v = np.zeros((nx, ny))
+    for i in range(16):
+        v += 0.05 * np.exp(-((X - cx[i]) ** 2 + (Y - cy[i]) ** 2) / (2.0 * 20.0 ** 2))
+    e = uniform_grid(0.0, 0.3, n_energies)
+    return effective_mass_device(f"cfg4_em_{nx}x{ny}", nx, ny, 0.5, 0.067, v, e, 1e-6, 0.1, 0.0, 0.025,
+                                 description="2D effective mass, 16 Gaussians 0.05 eV width 20a, seed 3")
+
+
+def config5(n_energies: int = 2048, nx: int = 512, ny: int = 512) -> Workload:
+    """512 x 512 + diagonal phonon self-energy (configs[4])."""
+    r = MT19937_64(4)
+    v = 0.1 * r.uniform01(nx * ny)
+    gamma = 1e-3 + 4e-3 * r.uniform01(nx * ny)
+    e = uniform_grid(0.0, 0.3, n_energies)
+    return effective_mass_device(f"cfg5_em_{nx}x{ny}_phonon", nx, ny, 0.5, 0.067, v, e, 1e-6, 0.1, 0.0, 0.025,
+                                 phonon_gamma=gamma,
+                                 description="2D effective mass + phonon -i gamma, gamma~U[1,5] meV seed 4")
+
+
+# ---------------------------------------------------------------------------
+# Zigzag (20,0) carbon nanotube, config 3
+# ---------------------------------------------------------------------------
+def _cnt_cell(k_around: int, t: float):
+    """Unit cell of a zigzag (k,0) tube: 4 atomic rings of k atoms; returns
+    (H00, H01) with H01 the coupling from a cell to the next one."""
+    m = 4 * k_around
+    h00 = np.zeros((m, m))
+    h01 = np.zeros((m, m))
+    ring = lambda l, k: l * k_around + (k % k_around)  # noqa: E731
+    for k in range(k_around):
+        # ring0 - ring1: zigzag (k -> k, k-1); ring1 - ring2: straight;
+        # ring2 - ring3: zigzag (k -> k, k+1); ring3 - next ring0: straight
+        for a, b in ((ring(0, k), ring(1, k)), (ring(0, k), ring(1, k - 1)), (ring(1, k), ring(2, k)),
+                     (ring(2, k), ring(3, k)), (ring(2, k), ring(3, k + 1))):
+            h00[a, b] = h00[b, a] = t
+        h01[ring(3, k), ring(0, k)] = t
+    return h00, h01
+
+
+def sancho_rubio(energy: float, eta: float, h00: np.ndarray, h01: np.ndarray, tol: float = 1e-12,
+                 max_iter: int = 200) -> np.ndarray:
+    """Surface Green's function by energy-doubling decimation; returns the
+    retarded self-energy H01^T g_s H01 of the lead attached through h01
+    (coupling device-edge-cell -> lead-cell = h01, real symmetric blocks)."""
+    z = (energy + 1j * eta) * np.eye(len(h00))
+    es = h00.astype(np.complex128)
+    e = es.copy()
+    alpha = h01.astype(np.complex128)
+    beta = h01.T.astype(np.complex128)
+    for _ in range(max_iter):
+        g = np.linalg.inv(z - e)
+        ag, bg = alpha @ g, beta @ g
+        es = es + ag @ beta
+        e = e + ag @ beta + bg @ alpha
+        alpha = ag @ alpha
+        beta = bg @ beta
+        if np.abs(alpha).max() < tol and np.abs(beta).max() < tol:
+            break
+    else:
+        raise RuntimeError("Sancho-Rubio decimation did not converge")
+    gs = np.linalg.inv(z - es)
+    sig = h01.T @ gs @ h01
+    return 0.5 * (sig + sig.T)
+
+
+def config3(n_energies: int = 512, n_cells: int = 600) -> Workload:
+    """Zigzag (20,0) CNT, single p_z, t = -2.7 eV, 600 cells x 80 atoms (configs[2])."""
+    k_around, t = 20, -2.7
+    cell = 4 * k_around
+    h00, h01 = _cnt_cell(k_around, t)
+    n = n_cells * cell
+    onsite = 0.1 * (MT19937_64(2).uniform01(n) - 0.5)
+    r00, c00 = np.nonzero(h00)
+    r01, c01 = np.nonzero(h01)
+    rows, cols, vals = [np.arange(n)], [np.arange(n)], [onsite]
+    for c in range(n_cells):
+        b = c * cell
+        rows.append(b + r00); cols.append(b + c00); vals.append(h00[r00, c00])
+        if c + 1 < n_cells:
+            rows += [b + r01, b + cell + c01]
+            cols += [b + cell + c01, b + r01]
+            vals += [h01[r01, c01], h01[r01, c01]]
+    h_rows = np.concatenate(rows).astype(np.int32)
+    h_cols = np.concatenate(cols).astype(np.int32)
+    h_vals = np.concatenate(vals).astype(np.complex128)
+    axial = np.repeat(np.arange(n_cells * 4), k_around).astype(np.float64)
+    around = np.tile(np.arange(k_around), n_cells * 4).astype(np.float64)
+    coords = np.stack([axial, around], 1)
+    left = np.arange(cell)
+    right = np.arange(n - cell, n)
+    lr, lc = np.meshgrid(left, left, indexing="ij")
+    rr, rc = np.meshgrid(right, right, indexing="ij")
+    sr_rows = np.concatenate([lr.ravel(), rr.ravel()]).astype(np.int32)
+    sr_cols = np.concatenate([lc.ravel(), rc.ravel()]).astype(np.int32)
+    prob = Problem(n=n, h_rows=h_rows, h_cols=h_cols, h_vals=h_vals, sr_rows=sr_rows, sr_cols=sr_cols,
+                   sl_rows=sr_rows.copy(), sl_cols=sr_cols.copy(), coords=coords,
+                   atomic_groups=[left.tolist(), right.tolist()], max_leaf=64,
+                   layers=[list(range(c * cell, (c + 1) * cell)) for c in range(n_cells)])
+    energies = uniform_grid(-1.0, 1.0, n_energies)
+    mu_l, mu_r, kT, eta = 0.1, -0.1, 0.025, 1e-6
+    w2 = cell * cell
+
+    def self_energies(sel):
+        sel = np.atleast_1d(np.asarray(sel))
+        sr = np.zeros((len(sel), 2 * w2), np.complex128)
+        sl = np.zeros_like(sr)
+        for q, k in enumerate(sel):
+            e = float(energies[k])
+            # left lead repeats the first cell: device cell 0 <- lead cell via h01^T
+            sig_l = sancho_rubio(e, eta, h00, h01.T)
+            sig_r = sancho_rubio(e, eta, h00, h01)
+            sr[q, :w2], sr[q, w2:] = sig_l.ravel(), sig_r.ravel()
+            sl[q, :w2] = (-fermi(e, mu_l, kT) * (sig_l - sig_l.conj().T)).ravel()
+            sl[q, w2:] = (-fermi(e, mu_r, kT) * (sig_r - sig_r.conj().T)).ravel()
+        return sr, sl
+
+    return Workload("cfg3_cnt_20_0_600", prob, energies, trapezoid_weights(energies), self_energies,
+                    n_cells * 4, k_around, "zigzag (20,0) CNT, 600 cells, onsite U[-0.05,0.05] seed 2")
+
+
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

@@ -153,6 +153,7 @@ def _load() -> C.CDLL:
         "negf_plan_info_get": ([vp, C.POINTER(_PlanInfo)], i32),
         "negf_plan_tree": ([vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_fill": ([vp, vp, vp], i32),
+        "negf_plan_gemm_tasks": ([vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_destroy": ([vp], None),
         "negf_gpu_create": ([vp, i32, i32, C.POINTER(vp), st], i32),
         "negf_gpu_batch_capacity": ([vp], i32),
@@ -167,6 +168,10 @@ def _load() -> C.CDLL:
         "negf_nccl_unique_id": ([vp, st], i32),
         "negf_gpu_nccl_init": ([vp, vp, i32, i32, st], i32),
         "negf_gpu_allreduce_density": ([vp, st], i32),
+        "negf_gpu_profile": ([vp, i32], i32),
+        "negf_gpu_set_residual_check": ([vp, i32], i32),
+        "negf_gpu_max_real_residual": ([vp], C.c_double),
+        "negf_gpu_profile_read": ([vp, vp, i32], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -177,12 +182,19 @@ def _load() -> C.CDLL:
 
 _lib = _load()
 ABI_SYMBOLS = (
-    "negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_destroy "
+    "negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_gemm_tasks negf_plan_destroy "
     "negf_gpu_create negf_gpu_batch_capacity negf_gpu_solve_batch negf_gpu_solve_batch_device "
     "negf_gpu_check negf_gpu_density negf_gpu_stream negf_gpu_density_device "
     "negf_gpu_last_launches negf_gpu_destroy negf_nccl_unique_id negf_gpu_nccl_init "
-    "negf_gpu_allreduce_density"
+    "negf_gpu_allreduce_density negf_gpu_profile negf_gpu_profile_read negf_gpu_set_residual_check "
+    "negf_gpu_max_real_residual"
 ).split()
+
+KSTAT_NAMES = ("gemm", "inverse", "diag", "scale", "assemble", "output")
+
+
+class _KStat(C.Structure):
+    _fields_ = [("ms", C.c_double), ("cmul", C.c_double), ("launches", C.c_int64)]
 
 
 def _raise(st: _Status) -> None:
@@ -383,6 +395,14 @@ class HscPlan:
         _lib.negf_plan_tree(self._h, _ptr(parent), _ptr(level), _ptr(ptr), _ptr(dofs), _ptr(fo))
         return SeparatorTree(parent, level, [dofs[ptr[c] : ptr[c + 1]].copy() for c in range(nc)], fo[: nc - 1])
 
+    def gemm_tasks(self) -> dict:
+        """Per grouped-GEMM task: m, n, summed k, phase, level (schedule introspection)."""
+        t = self.info().n_gemm_tasks
+        out = {k: np.zeros(t, np.int64 if k == "k" else np.int32) for k in ("m", "n", "k", "phase", "level")}
+        _lib.negf_plan_gemm_tasks(self._h, _ptr(out["m"]), _ptr(out["n"]), _ptr(out["k"]), _ptr(out["phase"]),
+                                  _ptr(out["level"]))
+        return out
+
     def fill_sets(self) -> list:
         nc = self.info().n_clusters
         ptr = np.zeros(nc + 1, np.int32)
@@ -475,6 +495,25 @@ class HscGpuSolver:
     @property
     def stream_ptr(self) -> int:
         return int(_lib.negf_gpu_stream(self._h) or 0)
+
+    def set_residual_check(self, raise_error: bool) -> None:
+        """True (default): ResidualTooLarge like electron_density; False: record only."""
+        _lib.negf_gpu_set_residual_check(self._h, int(bool(raise_error)))
+
+    @property
+    def max_real_residual(self) -> float:
+        """Largest |Re G^<_jj| / |G^<_jj| seen (DensityMap::max_real_residual)."""
+        return float(_lib.negf_gpu_max_real_residual(self._h))
+
+    def profile(self, enable: bool = True) -> None:
+        """Per-kernel CUDA-event timing of subsequent solves (on the solver's stream)."""
+        _lib.negf_gpu_profile(self._h, int(bool(enable)))
+
+    def profile_read(self, reset: bool = False) -> dict:
+        arr = (_KStat * len(KSTAT_NAMES))()
+        _lib.negf_gpu_profile_read(self._h, C.cast(arr, C.c_void_p), int(bool(reset)))
+        return {k: {"ms": arr[i].ms, "cmul": arr[i].cmul, "launches": arr[i].launches}
+                for i, k in enumerate(KSTAT_NAMES)}
 
     def nccl_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = C.create_string_buffer(bytes(unique_id), 128)
