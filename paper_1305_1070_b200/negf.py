@@ -271,6 +271,8 @@ class Problem:
         p.sr_nnz, p.sr_rows, p.sr_cols = len(sr), _ptr(sr), _ptr(sc)
         lr, lc = arr(self.sl_rows, np.int32), arr(self.sl_cols, np.int32)
         p.sl_nnz, p.sl_rows, p.sl_cols = len(lr), _ptr(lr), _ptr(lc)
+        if self.coords is not None and np.asarray(self.coords).size != 2 * int(self.n):
+            raise ContractViolation("nested_dissection: coordinate count mismatch")
         p.coords = _ptr(arr(self.coords, np.float64)) if self.coords is not None else None
         groups = [np.asarray(g, np.int32) for g in self.atomic_groups]
         gptr = arr(np.cumsum([0] + [len(g) for g in groups]), np.int32)

@@ -35,6 +35,8 @@ SYNTHETIC = [
     ("syn_24x20_s5_fuzz", 24, 20, 5, True, 1.0, 16, [0.1, 0.4, 0.9]),
     ("syn_40x36_s6", 40, 36, 6, False, 1.0, 64, [0.0, 0.5]),
     ("syn_120x14_s7_fuzz", 120, 14, 7, True, 1.0, 64, [0.3]),
+    # cmd_bench's HSC row (run.cpp:385-406): 4x4 synthetic at E = 0, seed 1
+    ("syn_4x4_s1_bench", 4, 4, 1, False, 1.0, 64, [0.0]),
 ]
 
 SUPERLATTICE_DIAG = {

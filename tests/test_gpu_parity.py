@@ -31,3 +31,57 @@ def test_golden_hsc_parity(name, cuda_ok):
     want = (rp.weights[:, None] * hsc.gless.imag).sum(0) / (2 * np.pi)
     got = solver.density()
     assert np.abs(got - want).max() <= 1e-10 * max(np.abs(want).max(), 1e-300)
+
+
+def _oracle_energy(w, plan_tree, e):
+    from oracle import hsc_numpy as hn
+
+    p = w.problem
+    sr, sl = w.self_energies([e])
+    tree = hn.Tree(plan_tree.parent, plan_tree.dofs, p.n)
+    return hn.solve_energy(tree, p.n, p.h_rows, p.h_cols, p.h_vals, p.sr_rows, p.sr_cols, sr[0], p.sl_rows, p.sl_cols,
+                           sl[0], w.energies[e])
+
+
+@pytest.mark.gpu
+def test_config1_full_size(cuda_ok):
+    """BASELINE configs[0] (64x32, n = 2048) at full size: GPU vs the numpy
+    restatement and the dense oracle (n <= 2500, oracle.hpp:14)."""
+    from oracle import hsc_numpy as hn
+    from paper_1305_1070_b200 import devices
+
+    w = devices.config1()
+    plan = negf.HscPlan(w.problem)
+    sr, sl = w.self_energies([0])
+    gr, gl = negf.HscGpuSolver(plan).solve(w.energies, w.weights, sr, sl)
+    ogr, ogl, _ = _oracle_energy(w, plan.tree(), 0)
+    assert rel_err(gr[0], ogr) <= TOL and rel_err(gl[0], ogl) <= TOL
+    p = w.problem
+    dgr, dgl = hn.dense_solve(p.n, p.h_rows, p.h_cols, p.h_vals, p.sr_rows, p.sr_cols, sr[0], p.sl_rows, p.sl_cols,
+                              sl[0], w.energies[0])
+    assert rel_err(gr[0], dgr) <= 1e-9 and rel_err(gl[0], dgl) <= 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_config2_full_size_parity_and_properties(cuda_ok):
+    """BASELINE configs[1] (400x100, n = 40000): the full 256-point sweep on
+    the GPU; parity vs the numpy restatement at a well-conditioned energy
+    (1e-10) and size-independent properties at every energy."""
+    from paper_1305_1070_b200 import devices
+
+    w = devices.config2()
+    plan = negf.HscPlan(w.problem)
+    s = negf.HscGpuSolver(plan)
+    s.set_residual_check(False)
+    sr, sl = w.self_energies(np.arange(len(w.energies)))
+    gr, gl = s.solve(w.energies, w.weights, sr, sl)
+    ogr, ogl, _ = _oracle_energy(w, plan.tree(), 0)
+    assert rel_err(gr[0], ogr) <= TOL and rel_err(gl[0], ogl) <= TOL
+    # -Im G^r_jj >= 0 (LDOS), Im G^<_jj >= 0 (occupation), finite everywhere
+    assert np.isfinite(gr).all() and np.isfinite(gl).all()
+    assert (-gr.imag).min() >= -1e-12 * np.abs(gr).max()
+    assert gl.imag.min() >= -1e-12 * np.abs(gl).max()
+    # density is the weighted sum of the returned diagonals
+    d = s.density()
+    assert np.allclose(d, (w.weights[:, None] * gl.imag).sum(0) / (2 * np.pi), rtol=1e-12, atol=1e-300)

@@ -1,0 +1,122 @@
+"""CPU: the host plan behind the C ABI (tree, symbolic fold, ledger, errors)
+and the C ABI surface itself.  No GPU needed: plan creation is host-only."""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1305_1070_b200 import negf
+from tests.helpers import GOLDEN, golden_names, load_golden
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_tree_and_ledger_match_reference(name):
+    """Bit-exact nested dissection (partition.cpp:159-326) and the exact lean
+    ledger of hsc_fold + hsc_gless (dense.hpp:69-82), per golden problem."""
+    rp, prob, hsc, _ = load_golden(name)
+    plan = negf.HscPlan(prob)
+    t = plan.tree()
+    assert t.num_clusters == len(hsc.parent)
+    assert np.array_equal(t.parent, hsc.parent)
+    assert np.array_equal(t.level, hsc.level)
+    for a, b in zip(t.dofs, hsc.dofs):
+        assert np.array_equal(a, b)
+    i = plan.info()
+    ne = len(rp.energies)
+    assert (i.ref_fold_mul + i.ref_gless_mul) * ne == hsc.mul_ops
+    assert (i.ref_fold_inv + i.ref_gless_inv) * ne == hsc.inv_ops
+    assert i.exec_cmul <= i.ref_fold_mul + i.ref_fold_inv + i.ref_gless_mul  # needed-only never exceeds
+
+
+def test_cli_partition_tree_json():
+    """proj/cli_test_tmp/partition/tree.json: the 3x8 superlattice, max_leaf 2,
+    diagonal contacts (no atomic groups), device coordinates."""
+    rp, prob, _, _ = load_golden("superlattice_3x8_diag")
+    want = json.load(open(os.path.join(GOLDEN, "cli_partition_tree.json")))
+    got = negf.HscPlan(prob).tree().to_dict()
+    assert got == want
+
+
+def _chain_problem(edges, n, **kw):
+    e = np.asarray(edges, np.int32).reshape(-1, 2)
+    rows = np.concatenate([e[:, 0], e[:, 1], np.arange(n)])
+    cols = np.concatenate([e[:, 1], e[:, 0], np.arange(n)])
+    vals = np.concatenate([-np.ones(2 * len(e)), 4.0 * np.ones(n)]).astype(complex)
+    return negf.Problem(n=n, h_rows=rows, h_cols=cols, h_vals=vals, **kw)
+
+
+def test_nested_dissection_errors():
+    edges = [(i, i + 1) for i in range(9)]
+    with pytest.raises(negf.ConfigError):
+        negf.HscPlan(_chain_problem(edges, 10, max_leaf=0))
+    with pytest.raises(negf.ConfigError):
+        negf.HscPlan(_chain_problem(edges, 10, atomic_groups=[[0, 1], [1, 2]]))
+    with pytest.raises(negf.ConfigError):
+        negf.HscPlan(_chain_problem(edges, 10, atomic_groups=[[0, 11]]))
+    with pytest.raises(negf.ContractViolation):
+        negf.HscPlan(_chain_problem(edges, 10, coords=np.zeros((3, 2))))
+
+
+def test_explicit_tree_errors():
+    edges = [(0, 2), (1, 2)]
+    with pytest.raises(negf.ContractViolation):  # two roots
+        negf.HscPlan(_chain_problem(edges, 3, tree_parent=[-1, -1, 0], tree_dofs=[[0], [1], [2]]))
+    with pytest.raises(negf.ContractViolation):  # dof missing
+        negf.HscPlan(_chain_problem(edges, 3, tree_parent=[1, -1], tree_dofs=[[0], [1]]))
+    with pytest.raises(negf.PartitionViolation):  # sibling leaves coupled (rule 1)
+        negf.HscPlan(_chain_problem([(0, 1)], 3, tree_parent=[2, 2, -1], tree_dofs=[[0], [1], [2]]))
+    with pytest.raises(negf.ContractViolation):  # Sigma^< joining two clusters
+        negf.HscPlan(_chain_problem(edges, 3, sl_rows=[0], sl_cols=[2], tree_parent=[2, 2, -1],
+                                    tree_dofs=[[0], [1], [2]]))
+
+
+def test_grandparent_only_psi_list():
+    """A leaf coupled only to its grandparent folds straight past its parent:
+    exactly one Psi entry (test_hsc.cpp:727-790)."""
+    prob = _chain_problem([(0, 4), (1, 5), (2, 4), (3, 5)], 6, tree_parent=[1, 2, -1],
+                          tree_dofs=[[0, 1], [2, 3], [4, 5]])
+    fills = negf.HscPlan(prob).fill_sets()
+    assert fills[0] == [2]
+    assert fills[1] == [2]
+
+
+def test_fill_is_transitive():
+    """Schur fill (hsc.cpp:501-511): a leaf coupled to parent and grandparent
+    makes the parent's S contain the grandparent."""
+    prob = _chain_problem([(0, 1), (0, 2)], 3, tree_parent=[1, 2, -1], tree_dofs=[[0], [1], [2]])
+    fills = negf.HscPlan(prob).fill_sets()
+    assert fills == [[1, 2], [2], []]
+
+
+def test_disconnected_graph_gets_empty_root():
+    """Disconnected inputs: an artificial empty root separator (partition.hpp:73-75)."""
+    coords = np.array([[0.0, 0.0], [1.0, 0.0], [10.0, 0.0], [11.0, 0.0]])
+    prob = _chain_problem([(0, 1), (2, 3)], 4, max_leaf=2, coords=coords)
+    t = negf.HscPlan(prob).tree()
+    assert len(t.dofs[t.root]) == 0
+    assert sorted(np.concatenate(t.dofs).tolist()) == [0, 1, 2, 3]
+
+
+def test_abi_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "negf_gpu.h")).read()
+    declared = set(re.findall(r"\b(negf_[a-z_0-9]+)\s*\(", header))
+    assert declared, "no declarations found"
+    lib = negf._lib
+    for sym in sorted(declared):
+        assert hasattr(lib, sym), sym
+    assert declared <= set(negf.ABI_SYMBOLS) | {"negf_plan_info_get"}
+
+
+def test_gpu_handle_fails_loudly_without_device():
+    """No silent CPU fallback: without a GPU the device handle cannot be made."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    rp, prob, _, _ = load_golden("syn_5x6_s24")
+    with pytest.raises(negf.CudaError):
+        negf.HscGpuSolver(negf.HscPlan(prob))
