@@ -49,6 +49,9 @@ class SingularBlock(NegfError):
         self.energy_index = energy_index
         self.cluster = cluster
 
+    def __reduce__(self):
+        return (SingularBlock, (str(self), self.pivot_index, self.energy_index, self.cluster))
+
 
 class PartitionViolation(NegfError):
     pass
@@ -60,12 +63,18 @@ class NonSkewHermitianInput(NegfError):
         self.energy_index = energy_index
         self.cluster = cluster
 
+    def __reduce__(self):
+        return (NonSkewHermitianInput, (str(self), self.energy_index, self.cluster))
+
 
 class ResidualTooLarge(NegfError):
     def __init__(self, msg: str, energy_index: int = -1, dof: int = -1):
         super().__init__(msg)
         self.energy_index = energy_index
         self.dof = dof
+
+    def __reduce__(self):
+        return (ResidualTooLarge, (str(self), self.energy_index, self.dof))
 
 
 class CudaError(NegfError):

@@ -1,0 +1,112 @@
+"""CPU, world_size 2 over gloo: energy sharding, the density reduction and the
+cross-rank error rule of the distributed sweep (dist.py), with the numpy
+restatement standing in for the GPU solver (tests only)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import hsc_numpy as hn
+from paper_1305_1070_b200 import dist as pdist
+from paper_1305_1070_b200 import negf
+from tests.helpers import load_golden
+
+
+class OracleSolver:
+    """CPU stand-in with the HscGpuSolver surface (test infrastructure)."""
+
+    def __init__(self, name, fail_at=None):
+        self.rp, self.prob, self.hsc, _ = load_golden(name)
+        self.tree = hn.Tree(self.hsc.parent, self.hsc.dofs, self.rp.n)
+        self.acc = np.zeros(self.rp.n)
+        self.fail_at = fail_at or set()
+        self.capacity = 2
+
+    def solve(self, E, W, sr, sl, first_energy_index=0, want_diagonals=True):
+        grs, gls = [], []
+        for q, e in enumerate(E):
+            gi = first_energy_index + q
+            if gi in self.fail_at:
+                raise negf.SingularBlock(f"energy point {gi}: synthetic failure", 0, gi, 0)
+            p = self.prob
+            gr, gl, _ = hn.solve_energy(self.tree, self.rp.n, p.h_rows, p.h_cols, p.h_vals, p.sr_rows, p.sr_cols,
+                                        sr[q], p.sl_rows, p.sl_cols, sl[q], e)
+            self.acc += W[q] * gl.imag
+            grs.append(gr)
+            gls.append(gl)
+        return np.array(grs), np.array(gls)
+
+    def density(self):
+        return self.acc / (2.0 * np.pi)
+
+
+def _grid():
+    rp, _, _, _ = load_golden("syn_24x20_s5_fuzz")
+    E = np.linspace(0.1, 0.9, 7)
+    W = negf.trapezoid_weights(E)
+
+    def se(sel):
+        sr, sl = rp.values(np.zeros(len(sel), int))
+        return sr, sl
+
+    return E, W, se
+
+
+def _worker(rank, world, port, fail_at, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        E, W, se = _grid()
+        solver = OracleSolver("syn_24x20_s5_fuzz", fail_at)
+        try:
+            res = pdist.sweep(solver, E, W, se)
+            q.put((rank, "ok", res.indices.tolist(), res.density))
+        except negf.NegfError as exc:
+            q.put((rank, "err", exc.energy_index, str(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, fail_at=None):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fail_at, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    return sorted(out, key=lambda x: x[0])
+
+
+def test_shard_is_a_balanced_partition():
+    for n in (1, 7, 256, 1024):
+        for world in (1, 2, 3, 8):
+            parts = [pdist.shard(n, world, r) for r in range(world)]
+            allidx = np.concatenate(parts)
+            assert np.array_equal(allidx, np.arange(n))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_two_ranks_match_single_process():
+    E, W, se = _grid()
+    ref = OracleSolver("syn_24x20_s5_fuzz")
+    single = pdist.sweep(ref, E, W, se)
+    out = _run(2)
+    assert [o[1] for o in out] == ["ok", "ok"]
+    assert out[0][2] + out[1][2] == list(range(len(E)))
+    for o in out:
+        assert np.allclose(o[3], single.density, rtol=1e-13, atol=1e-300)
+
+
+def test_lowest_failing_energy_wins_across_ranks():
+    out = _run(2, fail_at={5, 2})  # rank 0 owns 0..3, rank 1 owns 4..6
+    assert [o[1] for o in out] == ["err", "err"]
+    assert all(o[2] == 2 for o in out)
