@@ -240,7 +240,7 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         launch_inverse(b, g->d_inv + op.begin, P.inv_tasks.data() + op.begin, op.count, g->d_status, s, L);
         break;
       case K_GEMM:
-        launch_gemm(b, g->d_tasks, g->d_terms, g->d_tiles, op.begin, op.count, s, L);
+        launch_gemm(b, g->d_tasks, g->d_terms, g->d_tiles, P.gemm_tiles.data(), op.begin, op.count, s, L);
         break;
       case K_DIAG:
         launch_diag(b, g->d_diag, g->d_diag_terms, op.begin, op.count, s, L);

@@ -730,11 +730,20 @@ __global__ void __launch_bounds__(1024) k_inverse_global(double2* arena, int64_t
 // ---------------------------------------------------------------------------
 // Grouped multi-term complex GEMM on DMMA (mma.sync.m8n8k4.f64)
 // ---------------------------------------------------------------------------
-constexpr int TM = kTileM, TN = kTileN, KC = 16;
-constexpr int LD_RK = KC + 4;   // (row, k) layouts: stride = 4 mod 8 (conflict-free frags)
-constexpr int LD_KR = TM + 2;   // (k, row) layouts: stride = 2 mod 8
-constexpr int OPND = (TM * LD_RK > KC * LD_KR) ? TM * LD_RK : KC * LD_KR;  // complex / operand / stage
+constexpr int KC = 16;
+constexpr int LD_RK = KC + 4;  // (row, k) smem layouts: pitch = 4 mod 8 -> conflict-free fragments
 
+// CTA of 4 warps, each owning a 16x16 output region (2x2 DMMA subtiles),
+// arranged WR x WC (2x2, 1x4 or 4x1) so that skinny tasks keep every warp
+// busy; the CTA tile is (16 WR) x (16 WC).
+template <int WR, int WC>
+struct Arr {
+  static constexpr int TM = 16 * WR, TN = 16 * WC;
+  static constexpr int LDA_KR = TM + 2, LDB_KR = TN + 2;  // (k, row|col) pitch = 2 mod 8
+  static constexpr int OPA = (TM * LD_RK > KC * LDA_KR) ? TM * LD_RK : KC * LDA_KR;
+  static constexpr int OPB = (TN * LD_RK > KC * LDB_KR) ? TN * LD_RK : KC * LDB_KR;
+  static constexpr int STAGE = OPA + OPB;  // complex elements per pipeline stage
+};
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -745,57 +754,58 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-struct ChunkCursor {
-  int term, k0;
-};
-
-__device__ __forceinline__ void load_chunk(double2* As, double2* Bs, const double2* base,
-                                           const GemmTerm& tm, int k0, int m, int n, int m0, int n0) {
+// Stage one K-chunk of op(A) (TM x KC) and op(B) (KC x TN) in the layout of
+// their global source (row- or k-contiguous); zero-fill outside the task.
+template <int WR, int WC>
+__device__ __forceinline__ void load_chunk(double2* st, const double2* base, const GemmTerm& tm, int k0, int m,
+                                           int n, int m0, int n0) {
+  using A = Arr<WR, WC>;
+  double2* As = st;
+  double2* Bs = st + A::OPA;
   const int tid = threadIdx.x;
   const int k = tm.k;
-  // A: TM x KC elements
   if (tm.a_op == OP_N) {
 #pragma unroll
-    for (int i = 0; i < (TM * KC) / 128; ++i) {
+    for (int i = 0; i < (A::TM * KC) / 128; ++i) {
       const int idx = tid + i * 128, r = idx / KC, kk = idx % KC;
       const bool v = (m0 + r < m) && (k0 + kk < k);
-      const double2* src = v ? base + tm.a_off + int64_t(m0 + r) * tm.lda + (k0 + kk) : base;
-      cp_async16(As + r * LD_RK + kk, src, v);
+      cp_async16(As + r * LD_RK + kk, v ? base + tm.a_off + int64_t(m0 + r) * tm.lda + (k0 + kk) : base, v);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < (TM * KC) / 128; ++i) {
-      const int idx = tid + i * 128, kk = idx / TM, r = idx % TM;
+    for (int i = 0; i < (A::TM * KC) / 128; ++i) {
+      const int idx = tid + i * 128, kk = idx / A::TM, r = idx % A::TM;
       const bool v = (m0 + r < m) && (k0 + kk < k);
-      const double2* src = v ? base + tm.a_off + int64_t(k0 + kk) * tm.lda + (m0 + r) : base;
-      cp_async16(As + kk * LD_KR + r, src, v);
+      cp_async16(As + kk * A::LDA_KR + r, v ? base + tm.a_off + int64_t(k0 + kk) * tm.lda + (m0 + r) : base, v);
     }
   }
-  // B: KC x TN elements
   if (tm.b_op == OP_N || tm.b_op == OP_C) {
 #pragma unroll
-    for (int i = 0; i < (TN * KC) / 128; ++i) {
-      const int idx = tid + i * 128, kk = idx / TN, c = idx % TN;
+    for (int i = 0; i < (A::TN * KC) / 128; ++i) {
+      const int idx = tid + i * 128, kk = idx / A::TN, c = idx % A::TN;
       const bool v = (n0 + c < n) && (k0 + kk < k);
-      const double2* src = v ? base + tm.b_off + int64_t(k0 + kk) * tm.ldb + (n0 + c) : base;
-      cp_async16(Bs + kk * LD_KR + c, src, v);
+      cp_async16(Bs + kk * A::LDB_KR + c, v ? base + tm.b_off + int64_t(k0 + kk) * tm.ldb + (n0 + c) : base, v);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < (TN * KC) / 128; ++i) {
+    for (int i = 0; i < (A::TN * KC) / 128; ++i) {
       const int idx = tid + i * 128, c = idx / KC, kk = idx % KC;
       const bool v = (n0 + c < n) && (k0 + kk < k);
-      const double2* src = v ? base + tm.b_off + int64_t(n0 + c) * tm.ldb + (k0 + kk) : base;
-      cp_async16(Bs + c * LD_RK + kk, src, v);
+      cp_async16(Bs + c * LD_RK + kk, v ? base + tm.b_off + int64_t(n0 + c) * tm.ldb + (k0 + kk) : base, v);
     }
   }
 }
 
+template <int WR, int WC>
 __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, const GemmTerm* __restrict__ terms,
-                                          const GemmTile& tl, double2 (*smA)[OPND], double2 (*smB)[OPND]) {
+                                          const GemmTile& tl, double2* smem) {
+  using A = Arr<WR, WC>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 16, wn = (warp & 1) * 16;
+  const int wm = (warp / WC) * 16, wn = (warp % WC) * 16;
+  // Warp-uniform live subtiles (8-granular skip of padding).
+  const int live_i = min(2, max(0, (tk.m - tl.m0 - wm + 7) / 8));
+  const int live_j = min(2, max(0, (tk.n - tl.n0 - wn + 7) / 8));
 
   double cr[2][2][2], ci[2][2][2];
 #pragma unroll
@@ -805,46 +815,42 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
 #pragma unroll
       for (int q = 0; q < 2; ++q) cr[i][j][q] = ci[i][j][q] = 0.0;
 
-  // Flattened (term, k-chunk) sequence, double-buffered with cp.async.
+  // Flattened (term, k-chunk) sequence through a 2-stage cp.async ring, one
+  // barrier per chunk.
   const int tend = tk.term_begin + tk.term_count;
-  ChunkCursor cur{tk.term_begin, 0};
-  while (cur.term < tend && terms[cur.term].k <= 0) ++cur.term;
-  int stage = 0;
-  GemmTerm tm_load;
-  if (cur.term < tend) {
-    tm_load = terms[cur.term];
-    load_chunk(smA[0], smB[0], base, tm_load, 0, tk.m, tk.n, tl.m0, tl.n0);
+  int lt = tk.term_begin, lk0 = 0;
+  while (lt < tend && terms[lt].k <= 0) ++lt;
+  int ct = lt, ck0 = 0;
+  auto advance = [&](int& term, int& kq) {
+    kq += KC;
+    if (kq >= terms[term].k) {
+      kq = 0;
+      ++term;
+      while (term < tend && terms[term].k <= 0) ++term;
+    }
+  };
+  if (lt < tend) {
+    load_chunk<WR, WC>(smem, base, terms[lt], lk0, tk.m, tk.n, tl.m0, tl.n0);
+    advance(lt, lk0);
   }
   cp_async_commit();
-  while (cur.term < tend) {
-    const GemmTerm tm = terms[cur.term];
-    const int k0 = cur.k0;
-    // Advance the cursor and prefetch the next chunk into the other stage.
-    ChunkCursor nxt = cur;
-    nxt.k0 += KC;
-    if (nxt.k0 >= tm.k) {
-      nxt.k0 = 0;
-      ++nxt.term;
-      while (nxt.term < tend && terms[nxt.term].k <= 0) ++nxt.term;
-    }
-    if (nxt.term < tend) {
-      const GemmTerm tn = terms[nxt.term];
-      load_chunk(smA[stage ^ 1], smB[stage ^ 1], base, tn, nxt.k0, tk.m, tk.n, tl.m0, tl.n0);
+  int stage = 0;
+  while (ct < tend) {
+    cp_async_wait<0>();
+    __syncthreads();
+    if (lt < tend) {
+      load_chunk<WR, WC>(smem + (stage ^ 1) * A::STAGE, base, terms[lt], lk0, tk.m, tk.n, tl.m0, tl.n0);
+      advance(lt, lk0);
     }
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-
-    const double2* As = smA[stage];
-    const double2* Bs = smB[stage];
+    const GemmTerm tm = terms[ct];
+    const double2* As = smem + stage * A::STAGE;
+    const double2* Bs = As + A::OPA;
     const double sg = static_cast<double>(tm.sign);
     const bool conjb = (tm.b_op == OP_C || tm.b_op == OP_H);
     const bool a_rk = (tm.a_op == OP_N);
     const bool b_kr = (tm.b_op == OP_N || tm.b_op == OP_C);
-    const int ksteps = min(KC, tm.k - k0);
-    // Warp-uniform skips: subtiles wholly outside the task's m x n do no DMMA.
-    const int live_i = min(2, max(0, (tk.m - tl.m0 - wm + 7) / 8));
-    const int live_j = min(2, max(0, (tk.n - tl.n0 - wn + 7) / 8));
+    const int ksteps = min(KC, tm.k - ck0);
     if (live_i > 0 && live_j > 0) {
 #pragma unroll
       for (int s = 0; s < KC / 4; ++s) {
@@ -854,14 +860,14 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int r = wm + 8 * i + g;
-          a[i] = a_rk ? As[r * LD_RK + kk] : As[kk * LD_KR + r];
+          a[i] = a_rk ? As[r * LD_RK + kk] : As[kk * A::LDA_KR + r];
           a[i].x *= sg;
           a[i].y *= sg;
         }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int c = wn + 8 * j + g;
-          b[j] = b_kr ? Bs[kk * LD_KR + c] : Bs[c * LD_RK + kk];
+          b[j] = b_kr ? Bs[kk * A::LDB_KR + c] : Bs[c * LD_RK + kk];
           if (conjb) b[j].y = -b[j].y;
         }
 #pragma unroll
@@ -879,9 +885,8 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         }
       }
     }
-    __syncthreads();
     stage ^= 1;
-    cur = nxt;
+    advance(ct, ck0);
   }
   cp_async_wait<0>();
 
@@ -907,20 +912,20 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
 }
 
 // Persistent launch: CTAs stride over (tile, energy) items, energy fastest;
-// tiles are pre-sorted by decreasing cost (longest first) in the plan.
+// tiles of one arrangement are pre-sorted by decreasing cost in the plan.
+template <int WR, int WC>
 __global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride, int nE,
                                               const GemmTask* __restrict__ tasks,
                                               const GemmTerm* __restrict__ terms,
                                               const GemmTile* __restrict__ tiles, int tile_begin,
                                               int64_t items) {
-  __shared__ __align__(16) double2 smA[2][OPND];
-  __shared__ __align__(16) double2 smB[2][OPND];
+  extern __shared__ double2 gsm[];
   for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
     const int64_t ti = w / nE;
     const int e = static_cast<int>(w - ti * nE);
     const GemmTile tl = tiles[tile_begin + ti];
     const GemmTask tk = tasks[tl.task];
-    gemm_item(arena + e * stride, tk, terms, tl, smA, smB);
+    gemm_item<WR, WC>(arena + e * stride, tk, terms, tl, gsm);
     __syncthreads();
   }
 }
@@ -1116,22 +1121,40 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
   }
 }
 
-void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
-                 const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s,
-                 int64_t& launches) {
-  if (tile_count <= 0) return;
+template <int WR, int WC>
+static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
+                            const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
+  constexpr size_t smem = sizeof(double2) * 2 * Arr<WR, WC>::STAGE;
   static int slots = 0;
   if (!slots) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
+    cudaFuncSetAttribute(k_gemm<WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm<WR, WC>, 128, smem);
     slots = std::max(1, sms * std::max(1, per_sm));
   }
   const int64_t items = int64_t(tile_count) * b.nE;
   const int grid = static_cast<int>(std::min<int64_t>(items, slots));
-  k_gemm<<<grid, 128, 0, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
-  ++launches;
+  k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
+}
+
+void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
+                 const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
+                 cudaStream_t s, int64_t& launches) {
+  // Tiles of one op are grouped by warp arrangement (plan.cpp): one launch each.
+  int i = tile_begin;
+  const int end = tile_begin + tile_count;
+  while (i < end) {
+    const int arr = h_tiles[i].arr;
+    int j = i;
+    while (j < end && h_tiles[j].arr == arr) ++j;
+    if (arr == 1) launch_gemm_arr<1, 4>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
+    else if (arr == 2) launch_gemm_arr<4, 1>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
+    else launch_gemm_arr<2, 2>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
+    ++launches;
+    i = j;
+  }
 }
 
 void launch_diag(const BatchArgs& b, const DiagTask* d_tasks, const GemmTerm* d_terms, int begin,

@@ -32,8 +32,8 @@ void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_templat
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
                     DevStatus* st, cudaStream_t s, int64_t& launches);
 void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
-                 const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s,
-                 int64_t& launches);
+                 const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
+                 cudaStream_t s, int64_t& launches);
 void launch_diag(const BatchArgs& b, const DiagTask* d_tasks, const GemmTerm* d_terms, int begin,
                  int count, cudaStream_t s, int64_t& launches);
 void launch_scale(const BatchArgs& b, const ScaleTask* d_tasks, int begin, int count,

@@ -93,11 +93,15 @@ struct Builder {
         const GemmTask& tk = P.gemm_tasks[tl.task];
         int64_t ks = 0;
         for (int q = tk.term_begin; q < tk.term_begin + tk.term_count; ++q) ks += P.gemm_terms[q].k;
-        const int64_t lm = std::min(kTileM, tk.m - tl.m0), ln = std::min(kTileN, tk.n - tl.n0);
+        const int64_t lm = std::min(kArrTM[tl.arr], tk.m - tl.m0), ln = std::min(kArrTN[tl.arr], tk.n - tl.n0);
         return ((lm + 7) / 8) * ((ln + 7) / 8) * (ks + 16);
       };
+      // grouped by arrangement (one launch each), longest first within one
       std::stable_sort(P.gemm_tiles.begin() + cur.begin, P.gemm_tiles.end(),
-                       [&](const GemmTile& a, const GemmTile& b) { return cost(a) > cost(b); });
+                       [&](const GemmTile& a, const GemmTile& b) {
+                         if (a.arr != b.arr) return a.arr < b.arr;
+                         return cost(a) > cost(b);
+                       });
     }
     if (cur.count > 0) {
       P.ops.push_back(cur);
@@ -125,8 +129,19 @@ struct Builder {
     P.gemm_tasks.push_back(tk);
     for (int t2 = tk.term_begin; t2 < tk.term_begin + tk.term_count; ++t2)
       cur.cmul += static_cast<double>(m) * n * P.gemm_terms[t2].k;
-    for (int m0 = 0; m0 < m; m0 += kTileM)
-      for (int n0 = 0; n0 < n; n0 += kTileN) P.gemm_tiles.push_back(GemmTile{id, m0, n0, 0});
+    // Warp arrangement with the fewest live-warp slots (each warp owns a
+    // 16x16 region); ties prefer the square 2x2 CTA.
+    int best = 0;
+    int64_t best_slots = -1;
+    for (int a : {0, 1, 2}) {
+      const int64_t slots = int64_t((m + kArrTM[a] - 1) / kArrTM[a]) * ((n + kArrTN[a] - 1) / kArrTN[a]) * 4;
+      if (best_slots < 0 || slots < best_slots) {
+        best_slots = slots;
+        best = a;
+      }
+    }
+    for (int m0 = 0; m0 < m; m0 += kArrTM[best])
+      for (int n0 = 0; n0 < n; n0 += kArrTN[best]) P.gemm_tiles.push_back(GemmTile{id, m0, n0, best});
   }
 };
 
@@ -415,9 +430,43 @@ Plan build_plan(ProblemDesc desc) {
   for (std::size_t k = 0; k < t.fold_order().size(); ++k) fold_pos[t.fold_order()[k]] = static_cast<int>(k);
   auto& T = P.gemm_terms;
 
-  // Fold (hsc.cpp:473-526), level by level.
+  // Fold (hsc.cpp:473-526), level by level, in left-looking form: right
+  // before the clusters of level l are inverted, every Schur contribution
+  // they will ever receive is gathered in one task per target block,
+  //   A_{x,q} += sum_{y : x,q in S(y)} Psi_{y,x}^T A_{y,q}     (q = x or q in S(x)),
+  // with the contributors y (all below x, already folded, rows final) in
+  // fold order.  The sum is the reference's right-looking update
+  // (hsc.cpp:501-511) reassociated: the same terms, each target written once.
+  std::vector<std::map<std::pair<int, int>, std::vector<std::array<int, 3>>>> schur(
+      static_cast<std::size_t>(t.levels()) + 1);
+  for (int y : t.fold_order()) {
+    const auto& js = B.I(y).S;
+    for (std::size_t p = 0; p < js.size(); ++p)
+      for (std::size_t q = p; q < js.size(); ++q)
+        schur[B.lev(js[p])][{js[p], js[q]}].push_back({y, static_cast<int>(p), static_cast<int>(q)});
+  }
+  auto gather_schur = [&](int l) {
+    B.open(K_GEMM, 0, l);
+    for (const auto& kv : schur[l]) {
+      const int jp = kv.first.first, jq = kv.first.second;
+      const ClusterInfo& J = B.I(jp);
+      const int tb = static_cast<int>(T.size());
+      for (const auto& c3 : kv.second) {
+        const ClusterInfo& X = B.I(c3[0]);
+        B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N, X.off_arow + X.s_col[c3[2]], X.K, +1);
+      }
+      if (jp == jq) B.gemm_task(J.m, J.m, J.off_d, J.m, MODE_ADD, 0, 0, tb);
+      else {
+        const int p = find_pos(J.S, jq);
+        if (p < 0) fail(kInternal, "plan: fill block missing from S");
+        B.gemm_task(J.m, B.msz(jq), J.off_arow + J.s_col[p], J.K, MODE_ADD, 0, 0, tb);
+      }
+    }
+    B.close();
+  };
   for (int l = 1; l <= t.levels() - 1; ++l) {
     const auto& xs = by_level[l];
+    gather_schur(l);
     B.open(K_INVERSE, 0, l);
     auto size_class = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : m <= kSmemInvMax ? 3 : 4; };
     for (int pass = 0; pass < 5; ++pass)  // grouped by kernel variant
@@ -436,34 +485,8 @@ Plan build_plan(ProblemDesc desc) {
       B.gemm_task(I.m, I.K, I.off_psi, I.K, MODE_SET, 0, 0, tb);
     }
     B.close();
-    // Schur: A_{jp,jq} += Psi_{x,jp}^T A_{x,jq}, p <= q; one task per target,
-    // contributions in ascending x (fold order within the level).
-    std::map<std::pair<int, int>, std::vector<std::array<int, 3>>> targets;
-    for (int x : xs) {
-      const auto& js = B.I(x).S;
-      for (std::size_t p = 0; p < js.size(); ++p)
-        for (std::size_t q = p; q < js.size(); ++q)
-          targets[{js[p], js[q]}].push_back({x, static_cast<int>(p), static_cast<int>(q)});
-    }
-    B.open(K_GEMM, 0, l);
-    for (const auto& kv : targets) {
-      const int jp = kv.first.first, jq = kv.first.second;
-      const ClusterInfo& J = B.I(jp);
-      const int tb = static_cast<int>(T.size());
-      for (const auto& c3 : kv.second) {
-        const ClusterInfo& X = B.I(c3[0]);
-        B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N, X.off_arow + X.s_col[c3[2]],
-                   X.K, +1);
-      }
-      if (jp == jq) B.gemm_task(J.m, J.m, J.off_d, J.m, MODE_ADD, 0, 0, tb);
-      else {
-        const int p = find_pos(J.S, jq);
-        if (p < 0) fail(kInternal, "plan: fill block missing from S");
-        B.gemm_task(J.m, B.msz(jq), J.off_arow + J.s_col[p], J.K, MODE_ADD, 0, 0, tb);
-      }
-    }
-    B.close();
   }
+  gather_schur(t.levels());
   B.open(K_INVERSE, 0, t.levels());
   if (B.msz(root) > 0) {
     P.inv_tasks.push_back(InvTask{B.msz(root), root, nc - 1, 0, B.I(root).off_d});
@@ -558,28 +581,31 @@ Plan build_plan(ProblemDesc desc) {
       }
     }
     B.close();
-    // N fold bottom-up (hsc.cpp:246-266).
-    for (int l = 1; l <= t.levels() - 1; ++l) {
-      std::map<std::pair<int, int>, std::vector<std::array<int, 3>>> targets;
-      for (int x : by_level[l]) {
-        const ClusterInfo& X = B.I(x);
-        if (X.ncols.empty()) continue;
-        for (std::size_t jj = 0; jj < X.S.size(); ++jj)
-          for (std::size_t kk = 0; kk < X.ncols.size(); ++kk) {
-            const int j = X.S[jj], k = X.ncols[kk];
-            if (B.lev(k) < B.lev(j)) continue;
-            targets[{j, k}].push_back({x, static_cast<int>(jj), static_cast<int>(kk)});
-          }
-      }
+    // N fold bottom-up (hsc.cpp:246-266), left-looking like the Schur fold:
+    // N_{j,k} += sum_{y : j in S(y)} Psi_{y,j}^T N_{y,k}, level(k) >= level(j),
+    // gathered per target right after the targets' own contributors are final.
+    std::vector<std::map<std::pair<int, int>, std::vector<std::array<int, 3>>>> nf(
+        static_cast<std::size_t>(t.levels()) + 1);
+    for (int y : t.fold_order()) {
+      const ClusterInfo& Y = B.I(y);
+      if (Y.ncols.empty()) continue;
+      for (std::size_t jj = 0; jj < Y.S.size(); ++jj)
+        for (std::size_t kk = 0; kk < Y.ncols.size(); ++kk) {
+          const int j = Y.S[jj], k = Y.ncols[kk];
+          if (B.lev(k) < B.lev(j)) continue;
+          nf[B.lev(j)][{j, k}].push_back({y, static_cast<int>(jj), static_cast<int>(kk)});
+        }
+    }
+    for (int l = 2; l <= t.levels(); ++l) {
       B.open(K_GEMM, 3, l);
-      for (const auto& kv : targets) {
+      for (const auto& kv : nf[l]) {
         const int j = kv.first.first, k = kv.first.second;
         const ClusterInfo& J = B.I(j);
         const int tb = static_cast<int>(T.size());
         for (const auto& c3 : kv.second) {
           const ClusterInfo& X = B.I(c3[0]);
-          B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N,
-                     X.off_nrow + X.ncol_off[c3[2]], X.WN, +1);
+          B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N, X.off_nrow + X.ncol_off[c3[2]], X.WN,
+                     +1);
         }
         if (k == j) B.gemm_task(J.m, J.m, J.off_nd, J.m, MODE_ADD, 0, 0, tb);
         else B.gemm_task(J.m, B.msz(k), J.off_nrow + B.col_of(J.ncols, J.ncol_off, k), J.WN, MODE_ADD, 0, 0, tb);

@@ -75,7 +75,7 @@ struct GemmTerm {
 struct GemmTile {
   int task;
   int m0, n0;
-  int pad;
+  int arr;  // warp arrangement of the CTA: 0 = 2x2 (32x32), 1 = 1x4 (16x64), 2 = 4x1 (64x16)
 };
 
 // Diagonal-only output: out[a] = [init[a*init_stride]] + sum_t sign_t
@@ -178,8 +178,9 @@ struct Plan {
 };
 
 constexpr int kSmemInvMax = 112;  // largest block inverted wholly in shared memory
-constexpr int kTileM = 32;
-constexpr int kTileN = 32;
+// CTA tile extents per warp arrangement (see GemmTile::arr).
+constexpr int kArrTM[3] = {32, 16, 64};
+constexpr int kArrTN[3] = {32, 64, 16};
 
 Plan build_plan(ProblemDesc desc);
 

@@ -14,6 +14,7 @@ int main(int argc, char** argv) {
   const int M = atoi(argv[1]), N = atoi(argv[2]), K = atoi(argv[3]), T = atoi(argv[4]), nE = atoi(argv[5]);
   const int opa = argc > 6 ? atoi(argv[6]) : OP_N, opb = argc > 7 ? atoi(argv[7]) : OP_N;
   const int kterm = argc > 8 ? atoi(argv[8]) : K;  // split K into terms of this size
+  const int ARR = argc > 9 ? atoi(argv[9]) : 0;
   const int64_t per_task = int64_t(M) * K + int64_t(K) * N + int64_t(M) * N;
   const int64_t stride = per_task * T;
   std::vector<GemmTask> tasks;
@@ -43,8 +44,8 @@ int main(int argc, char** argv) {
     tk.term_begin = tb;
     tk.term_count = static_cast<int>(terms.size()) - tb;
     tasks.push_back(tk);
-    for (int m0 = 0; m0 < M; m0 += 32)
-      for (int n0 = 0; n0 < N; n0 += 32) tiles[0].push_back(GemmTile{t, m0, n0, 0});
+    for (int m0 = 0; m0 < M; m0 += kArrTM[ARR])
+      for (int n0 = 0; n0 < N; n0 += kArrTN[ARR]) tiles[0].push_back(GemmTile{t, m0, n0, ARR});
   }
   double2* arena;
   cudaMalloc(&arena, sizeof(double2) * stride * nE);
@@ -74,15 +75,15 @@ int main(int argc, char** argv) {
     float best = 1e30f;
     for (int rep = 0; rep < 5; ++rep) {
       cudaEventRecord(e0);
-      launch_gemm(b, dt, dm, dl[sh], 0, static_cast<int>(tiles[sh].size()), 0, L);
+      launch_gemm(b, dt, dm, dl[0], tiles[0].data(), 0, static_cast<int>(tiles[0].size()), 0, L);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       if (rep > 0 && ms < best) best = ms;
     }
-    printf("M=%d N=%d K=%d T=%d nE=%d ops=%d/%d tile=%d: %.3f ms  %.2f TF/s  (%s)\n", M, N, K, T, nE, opa, opb,
-           32, best, flops / best / 1e9, cudaGetErrorString(cudaGetLastError()));
+    printf("M=%d N=%d K=%d T=%d nE=%d ops=%d/%d arr=%d: %.3f ms  %.2f TF/s  (%s)\n", M, N, K, T, nE, opa, opb,
+           ARR, best, flops / best / 1e9, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
