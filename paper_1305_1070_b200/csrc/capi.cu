@@ -120,10 +120,12 @@ struct negf_gpu {
   int capacity = 1;
   double2* arena = nullptr;
   double2* d_template = nullptr;
+  InitRegion *d_init_copy = nullptr, *d_init_zero = nullptr;
   int64_t* d_diag_pos = nullptr;
   int64_t *d_sr_pos = nullptr, *d_sl_pos = nullptr, *d_gr_pos = nullptr, *d_gl_pos = nullptr;
   int *d_sr_ptr = nullptr, *d_sr_src = nullptr, *d_sl_ptr = nullptr, *d_sl_src = nullptr;
   int *d_sl_partner = nullptr, *d_sl_cidx = nullptr, *d_seeded = nullptr;
+  int *d_cslots = nullptr, *d_cslot_ptr = nullptr;
   GemmTask* d_tasks = nullptr;
   GemmTerm* d_terms = nullptr;
   GemmTile* d_tiles = nullptr;
@@ -223,13 +225,12 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
   int64_t& L = g->launches;
   {
     Bracket br(g, NEGF_KSTAT_ASSEMBLE, 0.0);
-    launch_assemble(b, P, g->d_template, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr, g->d_sr_src,
+    launch_assemble(b, P, g->d_template, g->d_init_copy, g->d_init_zero, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr, g->d_sr_src,
                     static_cast<int64_t>(P.desc.sr_rows.size()), d_sr, g->d_sl_pos, g->d_sl_ptr, g->d_sl_src,
                     static_cast<int64_t>(P.desc.sl_rows.size()), d_sl, s, L);
-    launch_skew_check(b, d_sl, static_cast<int64_t>(P.desc.sl_rows.size()),
-                      static_cast<int>(P.sl_slot_pos.size()), g->d_sl_ptr, g->d_sl_src, g->d_sl_partner,
-                      g->d_sl_cidx, static_cast<int>(P.seeded_ids.size()), g->d_seeded, g->d_skew,
-                      g->d_status, s, L);
+    launch_skew_check(b, d_sl, static_cast<int64_t>(P.desc.sl_rows.size()), g->d_cslots, g->d_cslot_ptr,
+                      g->d_sl_ptr, g->d_sl_src, g->d_sl_partner, static_cast<int>(P.seeded_ids.size()), g->d_seeded,
+                      g->d_skew, g->d_status, s, L);
   }
   static const int kind_stat[4] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM, NEGF_KSTAT_DIAG, NEGF_KSTAT_SCALE};
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
@@ -434,6 +435,8 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     auto& o = g->owned;
     g->d_template = reinterpret_cast<double2*>(dev_upload(P.a_template, o));
     g->d_diag_pos = dev_upload(P.diag_pos, o);
+    g->d_init_copy = dev_upload(P.init_copy, o);
+    g->d_init_zero = dev_upload(P.init_zero, o);
     g->d_sr_pos = dev_upload(P.sr_slot_pos, o);
     g->d_sr_ptr = dev_upload(P.sr_slot_ptr, o);
     g->d_sr_src = dev_upload(P.sr_slot_src, o);
@@ -443,6 +446,8 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     g->d_sl_partner = dev_upload(P.sl_partner, o);
     g->d_sl_cidx = dev_upload(P.sl_cidx, o);
     g->d_seeded = dev_upload(P.seeded_ids, o);
+    g->d_cslots = dev_upload(P.cslots, o);
+    g->d_cslot_ptr = dev_upload(P.cslot_ptr, o);
     g->d_gr_pos = dev_upload(P.out_gr_pos, o);
     g->d_gl_pos = dev_upload(P.out_gl_pos, o);
     g->d_tasks = dev_upload(P.gemm_tasks, o);

@@ -47,13 +47,23 @@ __device__ __forceinline__ double2 cinv(double2 a) {
 // ---------------------------------------------------------------------------
 // Assembly
 // ---------------------------------------------------------------------------
-__global__ void k_copy_template(double2* arena, int64_t stride, const double2* __restrict__ tmpl,
-                                int64_t len, int64_t z_begin, int64_t z_end) {
+// Per-energy initialisation of the regions listed by the plan: copy from the
+// template (D blocks, original-entry prefix of each Arow row) or zero
+// (Sigma^< blocks).  One CTA strides over regions; rows are coalesced.
+__global__ void k_init(double2* arena, int64_t stride, const double2* __restrict__ tmpl,
+                       const InitRegion* __restrict__ copy, int ncopy, const InitRegion* __restrict__ zero,
+                       int nzero) {
   double2* a = arena + blockIdx.y * stride;
-  const int64_t step = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < len; i += step) a[i] = tmpl[i];
-  for (int64_t i = z_begin + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < z_end; i += step)
-    a[i] = make_double2(0.0, 0.0);
+  for (int r = blockIdx.x; r < ncopy + nzero; r += gridDim.x) {
+    const bool z = r >= ncopy;
+    const InitRegion g = z ? zero[r - ncopy] : copy[r];
+    const int64_t total = int64_t(g.rows) * g.cols;
+    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+      const int row = static_cast<int>(i / g.cols), col = static_cast<int>(i - int64_t(row) * g.cols);
+      const int64_t o = g.off + int64_t(row) * g.pitch + col;
+      a[o] = z ? make_double2(0.0, 0.0) : tmpl[o];
+    }
+  }
 }
 
 // E on the diagonal and the Sigma^< slots (which live outside the A region).
@@ -491,6 +501,9 @@ __global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* are
   // element (r, c) of the block
   auto at = [&](int r, int c) -> double2& { return A[int64_t(r) * ld + c]; };
 
+#ifdef NEGF_INV_CLOCKS
+  long long clk_panel = 0, clk_swap = 0, clk_upd = 0, c0 = clock64();
+#endif
   for (int k0 = 0; k0 < m; k0 += NB) {
     const int kb = min(NB, m - k0);
     // ---- panel (columns k0..k0+7, all rows) on warp 0
@@ -578,6 +591,9 @@ __global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* are
     }
     __syncthreads();
     if (*flag) return;
+#ifdef NEGF_INV_CLOCKS
+    { const long long c1 = clock64(); clk_panel += c1 - c0; c0 = c1; }
+#endif
     // ---- row interchanges of this panel on the other columns (column-parallel)
     for (int c = tid; c < m8; c += INV_THREADS) {
       if ((c >= k0 && c < k0 + NB) || (kGlobal && c >= m)) {  // panel / no padding in global memory
@@ -603,6 +619,9 @@ __global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* are
       v.x -= 1.0;
     }
     __syncthreads();
+#ifdef NEGF_INV_CLOCKS
+    { const long long c1 = clock64(); clk_swap += c1 - c0; c0 = c1; }
+#endif
     // ---- rank-NB update of every 8x8 subtile (panel columns keep M_p): DMMA
     const int g8 = lane >> 2, t4 = lane & 3;
     const int nsub_r = m8 / 8, nsub_c = m8 / 8;
@@ -635,6 +654,9 @@ __global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* are
       if (in0 && !pc0) at(r, c) = make_double2(cr0, ci0);
       if (in1 && !pc1) at(r, c + 1) = make_double2(cr1, ci1);
     }
+#ifdef NEGF_INV_CLOCKS
+    { __syncthreads(); const long long c1 = clock64(); clk_upd += c1 - c0; c0 = c1; }
+#endif
     // restore M_p in the panel columns (add the identity back) and, for the
     // global variant, write the panel columns back
     __syncthreads();
@@ -651,6 +673,10 @@ __global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* are
     }
     __syncthreads();
   }
+#ifdef NEGF_INV_CLOCKS
+  if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0)
+    printf("[inv clocks] m=%d panel %lld swap %lld update %lld\n", m, clk_panel, clk_swap, clk_upd);
+#endif
   // Undo the row interchanges as column interchanges (last first).
   if (tid == 0) {
     int* cur_at = pos_of;  // reuse: first the permutation, then its inverse in Rs scratch
@@ -933,6 +959,8 @@ __global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride, in
 // ---------------------------------------------------------------------------
 // Diagonal-only products, diagonal seeds, outputs
 // ---------------------------------------------------------------------------
+// One thread per output row (rows of never-referenced clusters are short;
+// a thread walks its row of Psi and of the row-stored block, L1-cached).
 __global__ void k_diag(double2* arena, int64_t stride, const DiagTask* __restrict__ tasks,
                        const GemmTerm* __restrict__ terms, int begin) {
   const DiagTask tk = tasks[begin + blockIdx.x];
@@ -1004,26 +1032,45 @@ __device__ __forceinline__ double2 slot_value(const double2* sl, const int* ptr,
   return v;
 }
 
-__global__ void k_skew_accum(const double2* __restrict__ sigma_l, int64_t sl_nnz, int slots,
-                             const int* __restrict__ ptr, const int* __restrict__ src,
-                             const int* __restrict__ partner, const int* __restrict__ cidx, int nsc,
-                             double* acc) {
-  const int e = blockIdx.y;
+// One CTA per (seeded cluster, energy): block reduction over the cluster's
+// slots (plan: slots grouped per cluster), no contended atomics.
+__global__ void k_skew_accum(const double2* __restrict__ sigma_l, int64_t sl_nnz, const int* __restrict__ cslots,
+                             const int* __restrict__ cslot_ptr, const int* __restrict__ ptr,
+                             const int* __restrict__ src, const int* __restrict__ partner, int nsc, double* acc) {
+  const int c = blockIdx.x, e = blockIdx.y;
   const double2* sl = sigma_l + e * sl_nnz;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < slots; s += gridDim.x * blockDim.x) {
+  double num = 0.0, den = 0.0;
+  for (int q = cslot_ptr[c] + threadIdx.x; q < cslot_ptr[c + 1]; q += blockDim.x) {
+    const int s = cslots[q];
     const double2 v = slot_value(sl, ptr, src, s);
-    double num;
     const int p = partner[s];
     if (p >= 0) {
       const double2 w = slot_value(sl, ptr, src, p);
       const double re = v.x + w.x, im = v.y - w.y;
-      num = re * re + im * im;
+      num += re * re + im * im;
     } else {
-      num = 2.0 * (v.x * v.x + v.y * v.y);
+      num += 2.0 * (v.x * v.x + v.y * v.y);
     }
-    double* a = acc + (int64_t(e) * nsc + cidx[s]) * 2;
-    atomicAdd(a, num);
-    atomicAdd(a + 1, v.x * v.x + v.y * v.y);
+    den += v.x * v.x + v.y * v.y;
+  }
+  __shared__ double red[2][8];
+  for (int o = 16; o; o >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = num;
+    red[1][threadIdx.x >> 5] = den;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double n2 = 0.0, d2 = 0.0;
+    for (int w = 0; w < (blockDim.x >> 5); ++w) {
+      n2 += red[0][w];
+      d2 += red[1][w];
+    }
+    acc[(int64_t(e) * nsc + c) * 2] = n2;
+    acc[(int64_t(e) * nsc + c) * 2 + 1] = d2;
   }
 }
 
@@ -1049,14 +1096,15 @@ int grid_for(int64_t work, int threads, int cap) {
 }  // namespace
 
 void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_template,
-                     const int64_t* d_diag_pos, const double* d_energies, const int64_t* d_sr_pos,
+                     const InitRegion* d_init_copy, const InitRegion* d_init_zero, const int64_t* d_diag_pos, const double* d_energies, const int64_t* d_sr_pos,
                      const int* d_sr_ptr, const int* d_sr_src, int64_t sr_nnz,
                      const double2* d_sigma_r, const int64_t* d_sl_pos, const int* d_sl_ptr,
                      const int* d_sl_src, int64_t sl_nnz, const double2* d_sigma_l, cudaStream_t s,
                      int64_t& launches) {
-  const int64_t len = std::max<int64_t>(p.a_region, p.z_end - p.z_begin);
-  dim3 g1(grid_for(len, 256, 2048), b.nE);
-  k_copy_template<<<g1, 256, 0, s>>>(b.arena, b.stride, d_template, p.a_region, p.z_begin, p.z_end);
+  const int nreg = static_cast<int>(p.init_copy.size() + p.init_zero.size());
+  dim3 g1(std::max(1, std::min(nreg, 1024)), b.nE);
+  k_init<<<g1, 256, 0, s>>>(b.arena, b.stride, d_template, d_init_copy, static_cast<int>(p.init_copy.size()),
+                            d_init_zero, static_cast<int>(p.init_zero.size()));
   const int sr_slots = static_cast<int>(p.sr_slot_pos.size());
   const int sl_slots = static_cast<int>(p.sl_slot_pos.size());
   dim3 g2(grid_for(std::max<int64_t>(p.desc.n, sl_slots), 256, 1024), b.nE);
@@ -1173,14 +1221,13 @@ void launch_scale(const BatchArgs& b, const ScaleTask* d_tasks, int begin, int c
   ++launches;
 }
 
-void launch_skew_check(const BatchArgs& b, const double2* d_sigma_l, int64_t sl_nnz, int sl_slots,
-                       const int* d_sl_ptr, const int* d_sl_src, const int* d_sl_partner,
-                       const int* d_sl_cidx, int n_seeded, const int* d_seeded_ids, double* d_acc,
-                       DevStatus* st, cudaStream_t s, int64_t& launches) {
-  if (sl_slots <= 0 || n_seeded <= 0) return;
-  cudaMemsetAsync(d_acc, 0, sizeof(double) * 2 * size_t(n_seeded) * b.nE, s);
-  dim3 g(grid_for(sl_slots, 256, 1024), b.nE);
-  k_skew_accum<<<g, 256, 0, s>>>(d_sigma_l, sl_nnz, sl_slots, d_sl_ptr, d_sl_src, d_sl_partner, d_sl_cidx,
+void launch_skew_check(const BatchArgs& b, const double2* d_sigma_l, int64_t sl_nnz, const int* d_cslots,
+                       const int* d_cslot_ptr, const int* d_sl_ptr, const int* d_sl_src, const int* d_sl_partner,
+                       int n_seeded, const int* d_seeded_ids, double* d_acc, DevStatus* st, cudaStream_t s,
+                       int64_t& launches) {
+  if (n_seeded <= 0 || sl_nnz <= 0) return;
+  dim3 g(n_seeded, b.nE);
+  k_skew_accum<<<g, 256, 0, s>>>(d_sigma_l, sl_nnz, d_cslots, d_cslot_ptr, d_sl_ptr, d_sl_src, d_sl_partner,
                                  n_seeded, d_acc);
   const int tot = n_seeded * b.nE;
   k_skew_flag<<<(tot + 255) / 256, 256, 0, s>>>(d_acc, n_seeded, d_seeded_ids, b.nE, b.e_base, st);

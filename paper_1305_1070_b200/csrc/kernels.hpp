@@ -24,7 +24,7 @@ struct BatchArgs {
 };
 
 void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_template,
-                     const int64_t* d_diag_pos, const double* d_energies,
+                     const InitRegion* d_init_copy, const InitRegion* d_init_zero, const int64_t* d_diag_pos, const double* d_energies,
                      const int64_t* d_sr_pos, const int* d_sr_ptr, const int* d_sr_src,
                      int64_t sr_nnz, const double2* d_sigma_r, const int64_t* d_sl_pos,
                      const int* d_sl_ptr, const int* d_sl_src, int64_t sl_nnz,
@@ -38,10 +38,10 @@ void launch_diag(const BatchArgs& b, const DiagTask* d_tasks, const GemmTerm* d_
                  int count, cudaStream_t s, int64_t& launches);
 void launch_scale(const BatchArgs& b, const ScaleTask* d_tasks, int begin, int count,
                   cudaStream_t s, int64_t& launches);
-void launch_skew_check(const BatchArgs& b, const double2* d_sigma_l, int64_t sl_nnz, int sl_slots,
-                       const int* d_sl_ptr, const int* d_sl_src, const int* d_sl_partner,
-                       const int* d_sl_cidx, int n_seeded, const int* d_seeded_ids, double* d_acc,
-                       DevStatus* st, cudaStream_t s, int64_t& launches);
+void launch_skew_check(const BatchArgs& b, const double2* d_sigma_l, int64_t sl_nnz, const int* d_cslots,
+                       const int* d_cslot_ptr, const int* d_sl_ptr, const int* d_sl_src, const int* d_sl_partner,
+                       int n_seeded, const int* d_seeded_ids, double* d_acc, DevStatus* st, cudaStream_t s,
+                       int64_t& launches);
 void launch_output(const BatchArgs& b, int n, const int64_t* d_gr_pos, const int64_t* d_gl_pos,
                    const double* d_weights, double2* d_gr, double2* d_gl, double* d_density,
                    DevStatus* st, cudaStream_t s, int64_t& launches);

@@ -226,14 +226,24 @@ Plan build_plan(ProblemDesc desc) {
     for (std::size_t p = 0; p < js.size(); ++p)
       for (std::size_t q = p + 1; q < js.size(); ++q) insert_anc_order(B.I(js[p]).S, t, js[q]);
   }
+  // Column layout of Arow_x / Psi_x: blocks holding original entries of A
+  // first (initialised per energy), pure fill blocks after them (written by
+  // their gather task, never initialised).  S itself stays in ancestor order.
   for (int c = 0; c < nc; ++c) {
     ClusterInfo& ci = B.I(c);
+    ci.s_col.assign(ci.S.size(), 0);
+    ci.s_orig.assign(ci.S.size(), 0);
     int64_t off = 0;
-    for (int j : ci.S) {
-      ci.s_col.push_back(off);
-      off += B.msz(j);
-      B.I(j).referenced = true;
-    }
+    for (int pass = 0; pass < 2; ++pass)
+      for (std::size_t q = 0; q < ci.S.size(); ++q) {
+        const bool orig = S0[c].count(ci.S[q]) != 0;
+        if (orig != (pass == 0)) continue;
+        ci.s_col[q] = off;
+        ci.s_orig[q] = orig ? 1 : 0;
+        off += B.msz(ci.S[q]);
+        if (orig) ci.K0 = static_cast<int>(off);
+      }
+    for (int j : ci.S) B.I(j).referenced = true;
     ci.K = static_cast<int>(off);
   }
 
@@ -348,6 +358,18 @@ Plan build_plan(ProblemDesc desc) {
     if (P.any_seed && ci.WP) ci.off_prow = take(int64_t(ci.m) * ci.WP);
   }
   P.arena = std::max<int64_t>(cur, 8);
+  // Per-energy initialisation: D blocks and the original-entry prefix of each
+  // Arow row come from the template; Sigma^< blocks and (without N_rr) the
+  // root's P block are zeroed.  Everything else is written before it is read.
+  for (int c = 0; c < nc; ++c) {
+    const ClusterInfo& I = B.I(c);
+    if (I.m == 0) continue;
+    P.init_copy.push_back(InitRegion{I.off_d, 1, I.m * I.m, I.m * I.m});
+    if (I.K0 > 0) P.init_copy.push_back(InitRegion{I.off_arow, I.m, I.K0, I.K});
+    if (I.seeded) P.init_zero.push_back(InitRegion{I.off_sig, 1, I.seed_dense ? I.m * I.m : I.m, 0});
+  }
+  if (P.any_seed && !B.I(root).has_nd && B.msz(root) > 0)
+    P.init_zero.push_back(InitRegion{B.I(root).off_pd, 1, B.msz(root) * B.msz(root), 0});
 
   // ---- template of the A region: -H scattered into the descendant-row
   // orientation (the only one the lean fold reads, hsc.cpp:483-490).
@@ -412,6 +434,12 @@ Plan build_plan(ProblemDesc desc) {
         P.seeded_ids.push_back(c);
       }
     for (int c : P.sl_cluster) P.sl_cidx.push_back(cidx[c]);
+    P.cslot_ptr.assign(P.seeded_ids.size() + 1, 0);
+    for (int ci2 : P.sl_cidx) ++P.cslot_ptr[ci2 + 1];
+    for (std::size_t q = 1; q < P.cslot_ptr.size(); ++q) P.cslot_ptr[q] += P.cslot_ptr[q - 1];
+    P.cslots.assign(P.sl_cidx.size(), 0);
+    std::vector<int> fillp(P.cslot_ptr.begin(), P.cslot_ptr.end() - 1);
+    for (std::size_t s2 = 0; s2 < P.sl_cidx.size(); ++s2) P.cslots[fillp[P.sl_cidx[s2]]++] = static_cast<int>(s2);
   }
   P.out_gr_pos.resize(static_cast<std::size_t>(n));
   P.out_gl_pos.resize(static_cast<std::size_t>(n));
@@ -459,7 +487,8 @@ Plan build_plan(ProblemDesc desc) {
       else {
         const int p = find_pos(J.S, jq);
         if (p < 0) fail(kInternal, "plan: fill block missing from S");
-        B.gemm_task(J.m, B.msz(jq), J.off_arow + J.s_col[p], J.K, MODE_ADD, 0, 0, tb);
+        // a pure fill block is produced by this single gather task
+        B.gemm_task(J.m, B.msz(jq), J.off_arow + J.s_col[p], J.K, J.s_orig[p] ? MODE_ADD : MODE_SET, 0, 0, tb);
       }
     }
     B.close();
@@ -607,8 +636,11 @@ Plan build_plan(ProblemDesc desc) {
           B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N, X.off_nrow + X.ncol_off[c3[2]], X.WN,
                      +1);
         }
-        if (k == j) B.gemm_task(J.m, J.m, J.off_nd, J.m, MODE_ADD, 0, 0, tb);
-        else B.gemm_task(J.m, B.msz(k), J.off_nrow + B.col_of(J.ncols, J.ncol_off, k), J.WN, MODE_ADD, 0, 0, tb);
+        // seeded targets already hold their seed; otherwise this task is the
+        // block's only writer
+        const int mode = J.seeded ? MODE_ADD : MODE_SET;
+        if (k == j) B.gemm_task(J.m, J.m, J.off_nd, J.m, mode, 0, 0, tb);
+        else B.gemm_task(J.m, B.msz(k), J.off_nrow + B.col_of(J.ncols, J.ncol_off, k), J.WN, mode, 0, 0, tb);
       }
       B.close();
     }

@@ -125,6 +125,8 @@ struct ClusterInfo {
   int m = 0;
   std::vector<int> S;                 // fill set, nearest first (Psi list)
   std::vector<int64_t> s_col;         // column offset of each S entry in Arow/Psi
+  std::vector<char> s_orig;           // S entry holds original entries of A (else pure fill)
+  int K0 = 0;                         // width of the original-entry column prefix
   int K = 0;                          // sum of |S|
   bool referenced = false, seeded = false, seed_dense = false;
   bool full_g = false, full_p = false, has_nd = false;
@@ -133,6 +135,12 @@ struct ClusterInfo {
   int WG = 0, WN = 0, WP = 0;
   int64_t off_d = -1, off_arow = -1, off_psi = -1, off_sig = -1;
   int64_t off_gd = -1, off_grow = -1, off_nd = -1, off_nrow = -1, off_pd = -1, off_prow = -1;
+};
+
+// Region [off, off + rows*pitch) with `cols` leading elements per row.
+struct InitRegion {
+  int64_t off;
+  int rows, cols, pitch;
 };
 
 struct Plan {
@@ -145,6 +153,8 @@ struct Plan {
   int64_t a_region = 0;      // [0, a_region): D + Arow (template copied per energy)
   int64_t z_begin = 0, z_end = 0;  // region zeroed per energy (Sigma^<, N, root P)
   std::vector<cplx> a_template;    // a_region values of -H (no E, no Sigma)
+  std::vector<InitRegion> init_copy;  // copied from the template per energy
+  std::vector<InitRegion> init_zero;  // zeroed per energy
 
   // Per-energy scatter maps.
   std::vector<int64_t> diag_pos;          // n: A_dd position (E added)
@@ -158,6 +168,7 @@ struct Plan {
   std::vector<int> sl_partner;            // per slot: slot of (c,r) or -1
   std::vector<int> sl_cidx;               // per slot: index into seeded_ids
   std::vector<int> seeded_ids;            // clusters carrying a Sigma^< block
+  std::vector<int> cslot_ptr, cslots;     // CSR: seeded cluster index -> its slots
   // Output maps: per dof, position of its diagonal entry in Gd / Pd.
   std::vector<int64_t> out_gr_pos, out_gl_pos;
   bool any_seed = false;

@@ -1,0 +1,63 @@
+// Micro-benchmark of the batched inverse kernels: inv_bench m blocks energies
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1305_1070_b200/csrc/kernels.cu"
+
+using namespace negfb;
+
+int main(int argc, char** argv) {
+  const int m = atoi(argv[1]), nb = atoi(argv[2]), nE = atoi(argv[3]);
+  const int64_t stride = int64_t(m) * m * nb;
+  std::vector<double2> h(stride);
+  for (int b = 0; b < nb; ++b)
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j)
+        h[int64_t(b) * m * m + i * m + j] = make_double2(drand48() - 0.5 + (i == j ? 2.0 * m : 0.0), drand48() - 0.5);
+  double2* arena;
+  cudaMalloc(&arena, sizeof(double2) * stride * nE);
+  for (int e = 0; e < nE; ++e) cudaMemcpy(arena + e * stride, h.data(), sizeof(double2) * stride, cudaMemcpyHostToDevice);
+  std::vector<InvTask> t(nb);
+  for (int b = 0; b < nb; ++b) t[b] = InvTask{m, b, b, 0, int64_t(b) * m * m};
+  InvTask* dt;
+  cudaMalloc(&dt, sizeof(InvTask) * nb);
+  cudaMemcpy(dt, t.data(), sizeof(InvTask) * nb, cudaMemcpyHostToDevice);
+  DevStatus* st;
+  cudaMalloc(&st, sizeof(DevStatus));
+  cudaMemset(st, 0xff, sizeof(DevStatus));
+  BatchArgs b{arena, stride, nE, 0};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int64_t L = 0;
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    for (int e = 0; e < nE; ++e) cudaMemcpy(arena + e * stride, h.data(), sizeof(double2) * stride, cudaMemcpyHostToDevice);
+    cudaEventRecord(e0);
+    launch_inverse(b, dt, t.data(), nb, st, 0, L);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rep > 0 && ms < best) best = ms;
+  }
+  std::vector<double2> out(m * m);
+  cudaMemcpy(out.data(), arena, sizeof(double2) * m * m, cudaMemcpyDeviceToHost);
+  // residual of block 0: max |A * X - I|
+  double res = 0;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < m; ++j) {
+      double re = (i == j) ? -1.0 : 0.0, im = 0.0;
+      for (int k = 0; k < m; ++k) {
+        const double2 a = h[i * m + k], x = out[k * m + j];
+        re += a.x * x.x - a.y * x.y;
+        im += a.x * x.y + a.y * x.x;
+      }
+      res = std::max(res, std::hypot(re, im));
+    }
+  const double fl = 8.0 * m * double(m) * m * nb * nE;
+  printf("m=%d blocks=%dx%d: %.3f ms  %.2f TF/s  residual %.2e (%s)\n", m, nb, nE, best, fl / best / 1e9, res,
+         cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
