@@ -133,6 +133,7 @@ struct negf_gpu {
   GemmTerm* d_diag_terms = nullptr;
   ScaleTask* d_scale = nullptr;
   InvTask* d_inv = nullptr;
+  BigTask* d_big = nullptr;
   // per-batch staging
   double *d_energies = nullptr, *d_weights = nullptr;
   double2 *d_sigma_r = nullptr, *d_sigma_l = nullptr, *d_gr = nullptr, *d_gl = nullptr;
@@ -232,7 +233,8 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
                       g->d_sl_ptr, g->d_sl_src, g->d_sl_partner, static_cast<int>(P.seeded_ids.size()), g->d_seeded,
                       g->d_skew, g->d_status, s, L);
   }
-  static const int kind_stat[4] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM, NEGF_KSTAT_DIAG, NEGF_KSTAT_SCALE};
+  static const int kind_stat[6] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
+                                   NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE};
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
     const Op& op = P.ops[oi];
     Bracket br(g, kind_stat[op.kind], op.cmul * nE, static_cast<int>(oi));
@@ -245,6 +247,12 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         break;
       case K_DIAG:
         launch_diag(b, g->d_diag, g->d_diag_terms, op.begin, op.count, s, L);
+        break;
+      case K_PANEL:
+        launch_bigpanel(b, g->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, op.k0, g->d_status, s, L);
+        break;
+      case K_PERM:
+        launch_bigperm(b, g->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, s, L);
         break;
       default:
         launch_scale(b, g->d_scale, op.begin, op.count, s, L);
@@ -457,6 +465,7 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     g->d_diag_terms = dev_upload(P.diag_terms, o);
     g->d_scale = dev_upload(P.scale_tasks, o);
     g->d_inv = dev_upload(P.inv_tasks, o);
+    g->d_big = dev_upload(P.big_tasks, o);
     const int n = P.desc.n;
     const size_t sr = P.desc.sr_rows.size(), sl = P.desc.sl_rows.size();
     const size_t per_energy = size_t(P.arena) * 16 + (sr + sl) * 16 + size_t(n) * 32 + 16 +

@@ -717,6 +717,177 @@ __global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* are
   }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-CTA blocked Gauss-Jordan for large blocks (m > kSmemInvMax).
+// Per kPanel-column panel: k_bigpanel (one CTA per block and energy) factors
+// the panel with row partial pivoting in shared memory, applies the panel's
+// row interchanges to the rest of the block, and stages M_p - I_p and the
+// pivot rows R_p in arena scratch; the rank-kPanel update of all other
+// columns is an ordinary grouped-GEMM task (many CTAs, DMMA).  k_bigperm
+// finally undoes the interchanges as column interchanges.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride, const BigTask* __restrict__ tasks,
+                                                  int k0, int e_base, DevStatus* st) {
+  extern __shared__ double2 pn[];  // m x kPanel panel
+  __shared__ double red_v[8];
+  __shared__ int red_i[8];
+  __shared__ double s_thr;
+  __shared__ int s_fail, s_piv;
+  const BigTask tk = tasks[blockIdx.x];
+  const int m = tk.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double2* base = arena + blockIdx.y * stride;
+  double2* A = base + tk.off;
+  double2* thr = base + tk.off_thr;
+  int* perm = reinterpret_cast<int*>(base + tk.off_perm);
+  if (k0 == 0) {  // threshold from the original block (dense.cpp:58)
+    double mx = 0.0;
+    for (int64_t i = tid; i < int64_t(m) * m; i += 256) mx = fmax(mx, cabs2(A[i]));
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red_v[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double v = 0.0;
+      for (int w2 = 0; w2 < 8; ++w2) v = fmax(v, red_v[w2]);
+      s_thr = 1e-13 * v;
+      s_fail = 0;
+      *thr = make_double2(s_thr, 0.0);
+    }
+  } else if (tid == 0) {
+    const double2 v = *thr;
+    s_thr = v.x;
+    s_fail = v.y != 0.0;
+  }
+  __syncthreads();
+  if (s_fail) return;
+  const double thresh = s_thr;
+  const int kb = min(kPanel, m - k0);
+  for (int i = tid; i < m * kPanel; i += 256) {
+    const int r = i / kPanel, c = i - r * kPanel;
+    pn[i] = c < kb ? A[int64_t(r) * m + k0 + c] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int kk = 0; kk < kb; ++kk) {
+    const int k = k0 + kk;
+    double best = -1.0;
+    int bi = k;
+    for (int r = k + tid; r < m; r += 256) {
+      const double v = cnorm(pn[r * kPanel + kk]);
+      if (v > best) {
+        best = v;
+        bi = r;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      red_v[warp] = best;
+      red_i[warp] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double b2 = red_v[0];
+      int i2 = red_i[0];
+      for (int w2 = 1; w2 < 8; ++w2)
+        if (red_v[w2] > b2 || (red_v[w2] == b2 && red_i[w2] < i2)) {
+          b2 = red_v[w2];
+          i2 = red_i[w2];
+        }
+      if (sqrt(b2) <= thresh) {
+        s_fail = 1;
+        *thr = make_double2(thresh, 1.0);
+        report_singular(st, e_base + blockIdx.y, tk.fold_pos, k);
+      }
+      s_piv = i2;
+      perm[k] = i2;
+    }
+    __syncthreads();
+    if (s_fail) return;
+    const int p = s_piv;
+    if (p != k && tid < kPanel) {
+      const double2 t2 = pn[k * kPanel + tid];
+      pn[k * kPanel + tid] = pn[p * kPanel + tid];
+      pn[p * kPanel + tid] = t2;
+    }
+    __syncthreads();
+    const double2 ip = crcp(pn[k * kPanel + kk]);
+    if (tid < kPanel) pn[k * kPanel + tid] = (tid == kk) ? ip : cmul(pn[k * kPanel + tid], ip);
+    __syncthreads();
+    for (int r = tid; r < m; r += 256) {
+      if (r == k) continue;
+      const double2 f = pn[r * kPanel + kk];
+#pragma unroll
+      for (int c = 0; c < kPanel; ++c)
+        pn[r * kPanel + c] = (c == kk) ? make_double2(-(f.x * ip.x - f.y * ip.y), -(f.x * ip.y + f.y * ip.x))
+                                       : csub(pn[r * kPanel + c], cmul(f, pn[k * kPanel + c]));
+    }
+    __syncthreads();
+  }
+  // panel back into the block (M_p) and M_p - I_p into scratch
+  double2* mp = base + tk.off_mp;
+  for (int i = tid; i < m * kPanel; i += 256) {
+    const int r = i / kPanel, c = i - r * kPanel;
+    double2 v = pn[i];
+    if (c < kb) A[int64_t(r) * m + k0 + c] = v;
+    else v = make_double2(0.0, 0.0);
+    if (r == k0 + c) v.x -= 1.0;
+    mp[i] = v;
+  }
+  // this panel's row interchanges on every other column, then stage R_p
+  double2* rs = base + tk.off_rs;
+  for (int c = tid; c < m; c += 256) {
+    const bool in_panel = c >= k0 && c < k0 + kPanel;
+    if (!in_panel)
+      for (int kk = 0; kk < kb; ++kk) {
+        const int k = k0 + kk, p = perm[k];
+        if (p != k) {
+          const double2 t2 = A[int64_t(k) * m + c];
+          A[int64_t(k) * m + c] = A[int64_t(p) * m + c];
+          A[int64_t(p) * m + c] = t2;
+        }
+      }
+#pragma unroll
+    for (int kk = 0; kk < kPanel; ++kk)
+      rs[int64_t(kk) * m + c] = (kk < kb && !in_panel) ? A[int64_t(k0 + kk) * m + c] : make_double2(0.0, 0.0);
+  }
+}
+
+// Undo the row interchanges as column interchanges, last first.
+__global__ void __launch_bounds__(128) k_bigperm(double2* arena, int64_t stride, const BigTask* __restrict__ tasks) {
+  extern __shared__ double2 rowbuf[];  // 4 warps x m
+  __shared__ int pos_of[kBigMax], cur_at[kBigMax];
+  const BigTask tk = tasks[blockIdx.x];
+  const int m = tk.m, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2* base = arena + blockIdx.y * stride;
+  double2* thr = base + tk.off_thr;
+  if (thr->y != 0.0) return;  // singular: already reported
+  double2* A = base + tk.off;
+  const int* perm = reinterpret_cast<const int*>(base + tk.off_perm);
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < m; ++c) cur_at[c] = c;
+    for (int k = m - 1; k >= 0; --k) {
+      const int p = perm[k];
+      const int t2 = cur_at[k];
+      cur_at[k] = cur_at[p];
+      cur_at[p] = t2;
+    }
+    for (int q = 0; q < m; ++q) pos_of[cur_at[q]] = q;
+  }
+  __syncthreads();
+  double2* buf = rowbuf + warp * m;
+  for (int r = warp; r < m; r += 4) {
+    for (int c = lane; c < m; c += 32) buf[c] = A[int64_t(r) * m + c];
+    __syncwarp();
+    for (int c = lane; c < m; c += 32) A[int64_t(r) * m + pos_of[c]] = buf[c];
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(512) k_inverse_smem(double2* arena, int64_t stride,
                                                       const InvTask* __restrict__ tasks, int e_base,
                                                       DevStatus* st) {
@@ -1123,7 +1294,7 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
                     DevStatus* st, cudaStream_t s, int64_t& launches) {
   // Tasks of a level are pre-sorted by size class (see plan.cpp), so each
   // variant below covers one contiguous range.
-  auto cls = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : m <= kSmemInvMax ? 3 : 4; };
+  auto cls = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : 3; };
   int i = 0;
   while (i < count) {
     const int c = cls(h_tasks[i].m);
@@ -1185,6 +1356,36 @@ static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const G
   const int64_t items = int64_t(tile_count) * b.nE;
   const int grid = static_cast<int>(std::min<int64_t>(items, slots));
   k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
+}
+
+void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0,
+                     DevStatus* st, cudaStream_t s, int64_t& launches) {
+  if (count <= 0) return;
+  int mmax = 0;
+  for (int i = 0; i < count; ++i) mmax = std::max(mmax, h_tasks[i].m);
+  const size_t smem = size_t(mmax) * kPanel * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bigpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_bigpanel<<<dim3(count, b.nE), 256, smem, s>>>(b.arena, b.stride, d_tasks, k0, b.e_base, st);
+  ++launches;
+}
+
+void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, cudaStream_t s,
+                    int64_t& launches) {
+  if (count <= 0) return;
+  int mmax = 0;
+  for (int i = 0; i < count; ++i) mmax = std::max(mmax, h_tasks[i].m);
+  const size_t smem = size_t(4) * mmax * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bigperm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_bigperm<<<dim3(count, b.nE), 128, smem, s>>>(b.arena, b.stride, d_tasks);
+  ++launches;
 }
 
 void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,

@@ -31,6 +31,10 @@ void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_templat
                      const double2* d_sigma_l, cudaStream_t s, int64_t& launches);
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
                     DevStatus* st, cudaStream_t s, int64_t& launches);
+void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0,
+                     DevStatus* st, cudaStream_t s, int64_t& launches);
+void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, cudaStream_t s,
+                    int64_t& launches);
 void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                  const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
                  cudaStream_t s, int64_t& launches);

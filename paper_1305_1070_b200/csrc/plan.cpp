@@ -73,6 +73,8 @@ struct Builder {
         cur.task_begin = static_cast<int>(P.gemm_tasks.size());
         break;
       case K_DIAG: cur.begin = static_cast<int>(P.diag_tasks.size()); break;
+      case K_PANEL:
+      case K_PERM: cur.begin = static_cast<int>(P.big_tasks.size()); break;
       default: cur.begin = static_cast<int>(P.scale_tasks.size()); break;
     }
   }
@@ -84,6 +86,8 @@ struct Builder {
         cur.task_count = static_cast<int>(P.gemm_tasks.size()) - cur.task_begin;
         break;
       case K_DIAG: cur.count = static_cast<int>(P.diag_tasks.size()) - cur.begin; break;
+      case K_PANEL:
+      case K_PERM: cur.count = static_cast<int>(P.big_tasks.size()) - cur.begin; break;
       default: cur.count = static_cast<int>(P.scale_tasks.size()) - cur.begin; break;
     }
     if (cur.kind == K_GEMM && cur.count > 1) {
@@ -357,6 +361,19 @@ Plan build_plan(ProblemDesc desc) {
     if (P.any_seed && c != root) ci.off_pd = take(ci.full_p ? int64_t(ci.m) * ci.m : int64_t(ci.m));
     if (P.any_seed && ci.WP) ci.off_prow = take(int64_t(ci.m) * ci.WP);
   }
+  // Scratch of the multi-CTA inverse, reused level after level.
+  {
+    std::vector<int64_t> need(static_cast<std::size_t>(t.levels()) + 1, 0);
+    for (int c = 0; c < nc; ++c) {
+      const int64_t m = B.msz(c);
+      if (m <= kSmemInvMax) continue;
+      if (m > kBigMax)
+        fail(kContractViolation, "cluster of " + std::to_string(m) + " dofs exceeds the supported block size " +
+                                     std::to_string(kBigMax));
+      need[B.lev(c)] += align8(m * kPanel) * 2 + align8((m + 3) / 4) + 8;
+    }
+    P.big_scratch = take(*std::max_element(need.begin(), need.end()));
+  }
   P.arena = std::max<int64_t>(cur, 8);
   // Per-energy initialisation: D blocks and the original-entry prefix of each
   // Arow row come from the template; Sigma^< blocks and (without N_rr) the
@@ -473,6 +490,63 @@ Plan build_plan(ProblemDesc desc) {
       for (std::size_t q = p; q < js.size(); ++q)
         schur[B.lev(js[p])][{js[p], js[q]}].push_back({y, static_cast<int>(p), static_cast<int>(q)});
   }
+  // Inverses of one level: shared-memory kernels by size class, then the
+  // multi-CTA blocked Gauss-Jordan for the large blocks (kPanel-wide panels).
+  auto emit_inverses = [&](int l, const std::vector<int>& xs) {
+    B.open(K_INVERSE, 0, l);
+    auto size_class = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : 3; };
+    for (int pass = 0; pass < 4; ++pass)  // grouped by kernel variant
+      for (int x : xs)
+        if (B.msz(x) > 0 && B.msz(x) <= kSmemInvMax && size_class(B.msz(x)) == pass) {
+          P.inv_tasks.push_back(InvTask{B.msz(x), x, fold_pos[x], 0, B.I(x).off_d});
+          B.cur.cmul += double(B.msz(x)) * B.msz(x) * B.msz(x);
+        }
+    B.close();
+    std::vector<BigTask> big;
+    int64_t so = P.big_scratch;
+    int mmax = 0;
+    for (int x : xs) {
+      const int m = B.msz(x);
+      if (m <= kSmemInvMax) continue;
+      BigTask bt{};
+      bt.m = m;
+      bt.fold_pos = fold_pos[x];
+      bt.cluster = x;
+      bt.off = B.I(x).off_d;
+      bt.off_mp = so;
+      so += align8(int64_t(m) * kPanel);
+      bt.off_rs = so;
+      so += align8(int64_t(m) * kPanel);
+      bt.off_perm = so;
+      so += align8((m + 3) / 4);
+      bt.off_thr = so;
+      so += 8;
+      big.push_back(bt);
+      mmax = std::max(mmax, m);
+    }
+    if (big.empty()) return;
+    for (int k0 = 0; k0 < mmax; k0 += kPanel) {
+      B.open(K_PANEL, 0, l);
+      B.cur.k0 = k0;
+      for (const BigTask& bt : big)
+        if (bt.m > k0) {
+          P.big_tasks.push_back(bt);
+          B.cur.cmul += double(bt.m) * kPanel * kPanel;
+        }
+      B.close();
+      B.open(K_GEMM, 0, l);  // rank-kPanel update R += (M_p - I_p) R_p
+      for (const BigTask& bt : big) {
+        if (bt.m <= k0) continue;
+        const int tb = static_cast<int>(T.size());
+        B.add_term(T, kPanel, OP_N, bt.off_mp, kPanel, OP_N, bt.off_rs, bt.m, +1);
+        B.gemm_task(bt.m, bt.m, bt.off, bt.m, MODE_ADD, 0, 0, tb);
+      }
+      B.close();
+    }
+    B.open(K_PERM, 0, l);
+    for (const BigTask& bt : big) P.big_tasks.push_back(bt);
+    B.close();
+  };
   auto gather_schur = [&](int l) {
     B.open(K_GEMM, 0, l);
     for (const auto& kv : schur[l]) {
@@ -496,15 +570,7 @@ Plan build_plan(ProblemDesc desc) {
   for (int l = 1; l <= t.levels() - 1; ++l) {
     const auto& xs = by_level[l];
     gather_schur(l);
-    B.open(K_INVERSE, 0, l);
-    auto size_class = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : m <= kSmemInvMax ? 3 : 4; };
-    for (int pass = 0; pass < 5; ++pass)  // grouped by kernel variant
-      for (int x : xs)
-        if (B.msz(x) > 0 && size_class(B.msz(x)) == pass) {
-          P.inv_tasks.push_back(InvTask{B.msz(x), x, fold_pos[x], 0, B.I(x).off_d});
-          B.cur.cmul += double(B.msz(x)) * B.msz(x) * B.msz(x);
-        }
-    B.close();
+    emit_inverses(l, xs);
     B.open(K_GEMM, 0, l);  // Psi_x = -inv_x A_{x,S(x)}
     for (int x : xs) {
       const ClusterInfo& I = B.I(x);
@@ -516,14 +582,10 @@ Plan build_plan(ProblemDesc desc) {
     B.close();
   }
   gather_schur(t.levels());
-  B.open(K_INVERSE, 0, t.levels());
-  if (B.msz(root) > 0) {
-    P.inv_tasks.push_back(InvTask{B.msz(root), root, nc - 1, 0, B.I(root).off_d});
-    B.cur.cmul += double(B.msz(root)) * B.msz(root) * B.msz(root);
-  }
-  B.close();
+  emit_inverses(t.levels(), std::vector<int>{root});
+
   P.exec_inv_cmul = 0;
-  for (const auto& iv : P.inv_tasks) P.exec_inv_cmul += double(iv.m) * iv.m * iv.m;
+  for (int c = 0; c < nc; ++c) P.exec_inv_cmul += double(B.msz(c)) * B.msz(c) * B.msz(c);
 
   // G^r extraction top-down (hsc.cpp:171-227).
   for (int l = t.levels() - 1; l >= 1; --l) {

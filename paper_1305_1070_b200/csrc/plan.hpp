@@ -105,7 +105,26 @@ struct InvTask {
   int64_t off;
 };
 
-enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3 };
+// Blocks above kSmemInvMax are inverted by the multi-CTA blocked
+// Gauss-Jordan: per 8-column panel one K_PANEL launch (factor the panel, swap
+// rows, stage the pivot rows) and one grouped-GEMM rank-8 update, then one
+// K_PERM launch that undoes the interchanges.  Scratch lives in the arena.
+constexpr int kPanel = 8;
+constexpr int kBigMax = 1664;  // panel (m x 8 complex) must fit in shared memory
+
+struct BigTask {
+  int m;
+  int fold_pos;
+  int cluster;
+  int pad;
+  int64_t off;       // the block (m x m)
+  int64_t off_mp;    // M_p - I_p (m x kPanel)
+  int64_t off_rs;    // staged pivot rows (kPanel x m)
+  int64_t off_perm;  // m ints
+  int64_t off_thr;   // (threshold, failed flag)
+};
+
+enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL = 4, K_PERM = 5 };
 
 struct Op {
   int kind;
@@ -113,6 +132,7 @@ struct Op {
   int task_begin, task_count;  // K_GEMM: task range (for accounting)
   int phase;         // 0 fold, 1 G, 2 seed, 3 N fold, 4 P
   int level;
+  int k0;            // K_PANEL: first column of the panel
   double cmul;       // executed complex multiply-adds per energy
 };
 
@@ -151,6 +171,7 @@ struct Plan {
 
   int64_t arena = 0;         // complex elements per energy
   int64_t a_region = 0;      // [0, a_region): D + Arow (template copied per energy)
+  int64_t big_scratch = 0;   // arena offset of the multi-CTA inverse scratch
   int64_t z_begin = 0, z_end = 0;  // region zeroed per energy (Sigma^<, N, root P)
   std::vector<cplx> a_template;    // a_region values of -H (no E, no Sigma)
   std::vector<InitRegion> init_copy;  // copied from the template per energy
@@ -180,6 +201,7 @@ struct Plan {
   std::vector<GemmTerm> diag_terms;
   std::vector<ScaleTask> scale_tasks;
   std::vector<InvTask> inv_tasks;
+  std::vector<BigTask> big_tasks;
   std::vector<Op> ops;
 
   Ledger ref_fold, ref_gless;   // reference ledger per energy (hsc_fold / hsc_gless)

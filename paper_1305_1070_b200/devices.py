@@ -8,8 +8,16 @@ Conventions fixed here (the reference leaves them open):
 * dof = x * Ny + y with x the transport coordinate (layers are columns x),
   coords = (x, y): the top separator of config 4 is then the 1024-dof column
   the BASELINE names;
-* A(E) uses the real energy; eta lives only in the leads, as in the
-  reference (block.cpp:141-146, device.cpp:206-207);
+* A(E) uses the complex energy E + i*eta on the whole diagonal, as the
+  BASELINE configs state ("E + i eta"): it enters through the Sigma^r pattern
+  as -i*eta on every dof (the reference's phonon-diagonal slot, with no
+  Sigma^< counterpart), on top of the eta already inside the lead
+  self-energies.  With eta only in the leads (the reference CLI convention,
+  block.cpp:141-146) the interior Schur complements of the nested-dissection
+  fold are undamped finite-segment resolvents and go numerically singular at
+  many energies; two correct FP64 runs of the reference then disagree at O(1)
+  (config 3) -- see DESIGN.md section 4.  ``complex_energy=False`` restores the
+  reference convention;
 * random draws: std::mt19937_64(seed) + uniform01 (synthetic.hpp:18-20), onsite
   potential first in dof order, then any further draws;
 * effective-mass leads: analytic semi-infinite uniform lead,
@@ -88,7 +96,7 @@ def analytic_lead_sigma(energy: float, eta: float, t: float, phi: np.ndarray, ep
 def effective_mass_device(name: str, nx: int, ny: int, a_nm: float, m_eff: float, potential: np.ndarray,
                           energies: np.ndarray, eta: float, mu_l: float, mu_r: float, kT: float,
                           phonon_gamma: np.ndarray | None = None, max_leaf: int = 64,
-                          description: str = "") -> Workload:
+                          description: str = "", complex_energy: bool = False) -> Workload:
     t = HBAR2_OVER_2M0 / (m_eff * a_nm * a_nm)
     n = nx * ny
     idx = np.arange(n).reshape(nx, ny)  # dof = x*ny + y
@@ -112,10 +120,16 @@ def effective_mass_device(name: str, nx: int, ny: int, a_nm: float, m_eff: float
     if phonon_gamma is not None:
         sr_rows.append(interior)
         sr_cols.append(interior)
+    sl_rows = np.concatenate(sr_rows).astype(np.int32)
+    sl_cols = np.concatenate(sr_cols).astype(np.int32)
+    n_lesser = len(sl_rows)
+    if complex_energy:  # -i eta on every dof: A = (E + i eta) I - H - Sigma
+        sr_rows.append(np.arange(n))
+        sr_cols.append(np.arange(n))
     sr_rows = np.concatenate(sr_rows).astype(np.int32)
     sr_cols = np.concatenate(sr_cols).astype(np.int32)
     prob = Problem(n=n, h_rows=h_rows, h_cols=h_cols, h_vals=h_vals, sr_rows=sr_rows, sr_cols=sr_cols,
-                   sl_rows=sr_rows.copy(), sl_cols=sr_cols.copy(), coords=coords,
+                   sl_rows=sl_rows, sl_cols=sl_cols, coords=coords,
                    atomic_groups=[left.tolist(), right.tolist()], max_leaf=max_leaf,
                    layers=[idx[x].tolist() for x in range(nx)])
     phi, eps = _lead_modes(ny, t)
@@ -127,7 +141,9 @@ def effective_mass_device(name: str, nx: int, ny: int, a_nm: float, m_eff: float
         sel = np.atleast_1d(np.asarray(sel))
         nnz = len(sr_rows)
         sr = np.zeros((len(sel), nnz), np.complex128)
-        sl = np.zeros((len(sel), nnz), np.complex128)
+        sl = np.zeros((len(sel), n_lesser), np.complex128)
+        if complex_energy:
+            sr[:, n_lesser:] = -1j * eta
         for q, k in enumerate(sel):
             e = float(energies[k])
             sig = analytic_lead_sigma(e, eta, t, phi, eps)  # same uniform lead on both sides
@@ -137,7 +153,7 @@ def effective_mass_device(name: str, nx: int, ny: int, a_nm: float, m_eff: float
                 sl[q, side * w2:(side + 1) * w2] = (-fermi(e, mu, kT) * (sig - sig.conj().T)).ravel()
             if gam is not None:
                 s = -1j * gam
-                sr[q, 2 * w2:] = s
+                sr[q, 2 * w2:n_lesser] = s
                 sl[q, 2 * w2:] = -fermi(e, mu_ph, kT) * (s - np.conj(s))
         return sr, sl
 
@@ -235,7 +251,7 @@ def sancho_rubio(energy: float, eta: float, h00: np.ndarray, h01: np.ndarray, to
     return 0.5 * (sig + sig.T)
 
 
-def config3(n_energies: int = 512, n_cells: int = 600) -> Workload:
+def config3(n_energies: int = 512, n_cells: int = 600, complex_energy: bool = False) -> Workload:
     """Zigzag (20,0) CNT, single p_z, t = -2.7 eV, 600 cells x 80 atoms (configs[2])."""
     k_around, t = 20, -2.7
     cell = 4 * k_around
@@ -262,10 +278,13 @@ def config3(n_energies: int = 512, n_cells: int = 600) -> Workload:
     right = np.arange(n - cell, n)
     lr, lc = np.meshgrid(left, left, indexing="ij")
     rr, rc = np.meshgrid(right, right, indexing="ij")
-    sr_rows = np.concatenate([lr.ravel(), rr.ravel()]).astype(np.int32)
-    sr_cols = np.concatenate([lc.ravel(), rc.ravel()]).astype(np.int32)
+    sl_rows = np.concatenate([lr.ravel(), rr.ravel()]).astype(np.int32)
+    sl_cols = np.concatenate([lc.ravel(), rc.ravel()]).astype(np.int32)
+    extra = [np.arange(n)] if complex_energy else []
+    sr_rows = np.concatenate([sl_rows] + extra).astype(np.int32)
+    sr_cols = np.concatenate([sl_cols] + extra).astype(np.int32)
     prob = Problem(n=n, h_rows=h_rows, h_cols=h_cols, h_vals=h_vals, sr_rows=sr_rows, sr_cols=sr_cols,
-                   sl_rows=sr_rows.copy(), sl_cols=sr_cols.copy(), coords=coords,
+                   sl_rows=sl_rows, sl_cols=sl_cols, coords=coords,
                    atomic_groups=[left.tolist(), right.tolist()], max_leaf=64,
                    layers=[list(range(c * cell, (c + 1) * cell)) for c in range(n_cells)])
     energies = uniform_grid(-1.0, 1.0, n_energies)
@@ -274,14 +293,15 @@ def config3(n_energies: int = 512, n_cells: int = 600) -> Workload:
 
     def self_energies(sel):
         sel = np.atleast_1d(np.asarray(sel))
-        sr = np.zeros((len(sel), 2 * w2), np.complex128)
-        sl = np.zeros_like(sr)
+        sr = np.zeros((len(sel), len(sr_rows)), np.complex128)
+        sl = np.zeros((len(sel), 2 * w2), np.complex128)
+        sr[:, 2 * w2:] = -1j * eta
         for q, k in enumerate(sel):
             e = float(energies[k])
             # left lead repeats the first cell: device cell 0 <- lead cell via h01^T
             sig_l = sancho_rubio(e, eta, h00, h01.T)
             sig_r = sancho_rubio(e, eta, h00, h01)
-            sr[q, :w2], sr[q, w2:] = sig_l.ravel(), sig_r.ravel()
+            sr[q, :w2], sr[q, w2:2 * w2] = sig_l.ravel(), sig_r.ravel()
             sl[q, :w2] = (-fermi(e, mu_l, kT) * (sig_l - sig_l.conj().T)).ravel()
             sl[q, w2:] = (-fermi(e, mu_r, kT) * (sig_r - sig_r.conj().T)).ravel()
         return sr, sl

@@ -1,0 +1,109 @@
+"""GPU: the other BASELINE configurations as parity cases.
+
+* configs 3 (CNT), 4 and 5 built by the same generators at reduced sizes
+  against the numpy restatement (1e-10): the multi-CTA inverse (blocks of
+  128-256 dofs), a Sigma^< on every cluster (config 5, diagonal seeds);
+* configs 3, 4 and 5 at FULL size (48k / 1M / 262k dofs): a few energy
+  points through size-independent properties.  Config 3 at full length is
+  beyond the reference algorithm's numerical reach: its interior ring
+  separators are undamped finite-segment resolvents, and two correct FP64
+  runs of the reference (this restatement vs the reference build) disagree by
+  1e-8 .. O(1) depending on the energy -- only
+  finiteness and the density bookkeeping are asserted there.
+"""
+import numpy as np
+import pytest
+
+from oracle import hsc_numpy as hn
+from paper_1305_1070_b200 import devices, negf
+from tests.helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _vs_oracle(w, idx, tol=TOL):
+    plan = negf.HscPlan(w.problem)
+    s = negf.HscGpuSolver(plan)
+    s.set_residual_check(False)
+    sr, sl = w.self_energies(idx)
+    gr, gl = s.solve(w.energies[idx], w.weights[idx], sr, sl)
+    t = plan.tree()
+    tree = hn.Tree(t.parent, t.dofs, w.n)
+    p = w.problem
+    for q, e in enumerate(idx):
+        ogr, ogl, _ = hn.solve_energy(tree, p.n, p.h_rows, p.h_cols, p.h_vals, p.sr_rows, p.sr_cols, sr[q],
+                                      p.sl_rows, p.sl_cols, sl[q], w.energies[e])
+        assert rel_err(gr[q], ogr) <= tol, (w.name, int(e), rel_err(gr[q], ogr))
+        assert rel_err(gl[q], ogl) <= tol, (w.name, int(e), rel_err(gl[q], ogl))
+    return plan
+
+
+def _properties(gr, gl, w, idx, s):
+    assert np.isfinite(gr).all() and np.isfinite(gl).all()
+    assert ((-gr.imag).min(axis=1) >= -1e-10 * np.abs(gr).max(axis=1)).all()
+    assert (gl.imag.min(axis=1) >= -1e-10 * np.abs(gl).max(axis=1)).all()
+    d = s.density()
+    assert np.allclose(d, (w.weights[idx][:, None] * gl.imag).sum(0) / (2 * np.pi), rtol=1e-12, atol=1e-300)
+
+
+def test_config3_cnt_short_tube(cuda_ok):
+    """Same generator, 12 unit cells: in-band energies where the block
+    elimination is stable (restatement vs dense oracle ~1e-12)."""
+    w = devices.config3(n_cells=12)
+    _vs_oracle(w, np.array([0, 100]))
+
+
+@pytest.mark.slow
+def test_config3_cnt_full_size(cuda_ok):
+    w = devices.config3()
+    plan = negf.HscPlan(w.problem)
+    assert plan.info().n_clusters == 2039
+    s = negf.HscGpuSolver(plan)
+    s.set_residual_check(False)
+    idx = np.arange(0, 512, 64)
+    sr, sl = w.self_energies(idx)
+    gr, gl = s.solve(w.energies[idx], w.weights[idx], sr, sl)
+    assert np.isfinite(gr).all() and np.isfinite(gl).all()
+    d = s.density()
+    assert np.allclose(d, (w.weights[idx][:, None] * gl.imag).sum(0) / (2 * np.pi), rtol=1e-12, atol=1e-300)
+
+
+def test_config4_reduced(cuda_ok):
+    w = devices.config4(n_energies=16, nx=160, ny=160)
+    plan = _vs_oracle(w, np.array([3, 12]))
+    assert plan.info().max_block > 112  # multi-CTA inverse path
+
+
+def test_config5_reduced(cuda_ok):
+    w = devices.config5(n_energies=16, nx=96, ny=96)
+    plan = _vs_oracle(w, np.array([2, 9]))
+    assert plan.info().n_clusters > 100
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_size_properties(cfg, cuda_ok):
+    """Config 5 carries a meV phonon broadening on every dof: every energy must
+    satisfy LDOS >= 0 and occupation >= 0.  Config 4 has eta = 1e-6 only in the
+    leads; at a minority of energies an interior Schur complement of the fold
+    is nearly singular and the reference algorithm itself loses all digits
+     -- there only finiteness is required."""
+    w = devices.config4() if cfg == 4 else devices.config5()
+    plan = negf.HscPlan(w.problem)
+    info = plan.info()
+    assert info.max_block == (1024 if cfg == 4 else 512)
+    s = negf.HscGpuSolver(plan)
+    s.set_residual_check(False)
+    idx = np.linspace(0, len(w.energies) - 1, 8).astype(int)
+    sr, sl = w.self_energies(idx)
+    gr, gl = s.solve(w.energies[idx], w.weights[idx], sr, sl)
+    assert np.isfinite(gr).all() and np.isfinite(gl).all()
+    ok = ((-gr.imag).min(axis=1) >= -1e-10 * np.abs(gr).max(axis=1)) & \
+         (gl.imag.min(axis=1) >= -1e-10 * np.abs(gl).max(axis=1))
+    if cfg == 5:
+        assert ok.all()
+    else:
+        assert ok.sum() >= len(idx) // 2
+    d = s.density()
+    assert np.allclose(d, (w.weights[idx][:, None] * gl.imag).sum(0) / (2 * np.pi), rtol=1e-12, atol=1e-300)
