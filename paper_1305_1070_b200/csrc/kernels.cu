@@ -374,92 +374,6 @@ __device__ __forceinline__ double2 crcp(double2 a) {
   return make_double2(x / d, -y / d);
 }
 
-template <int RPL, int NB>
-__device__ __forceinline__ bool panel_regs(double2 (&P)[RPL][NB], int m, int k0, int kb, double thresh,
-                                           int* perm, int lane, DevStatus* st, int e_global, int fold_pos) {
-#pragma unroll
-  for (int kk = 0; kk < NB; ++kk) {
-    if (kk >= kb) break;
-    const int k = k0 + kk;
-    double best = -1.0;
-    int bi = k;
-#pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = lane + 32 * i;
-      const double mag = cnorm(P[i][kk]);
-      if (r >= k && r < m && mag > best) {
-        best = mag;
-        bi = r;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) {
-        best = ob;
-        bi = oi;
-      }
-    }
-    // |u_kk| <= 1e-13 max|a| (dense.cpp:58-75); NaN never trips it.
-    if (sqrt(best) <= thresh) {
-      if (lane == 0) report_singular(st, e_global, fold_pos, k);
-      return false;
-    }
-    const int p = bi;
-    if (lane == 0) perm[k] = p;
-    const int lk = k & 31, sk = k >> 5, lp = p & 31, sp = p >> 5;
-    double2 rk[NB], pr[NB];
-#pragma unroll
-    for (int c = kk; c < NB; ++c) {  // columns < kk of rows k/p are not needed
-      double2 vk = P[0][c], vp = P[0][c];
-#pragma unroll
-      for (int i = 1; i < RPL; ++i) {
-        if (i == sk) vk = P[i][c];
-        if (i == sp) vp = P[i][c];
-      }
-      rk[c].x = __shfl_sync(0xffffffffu, vk.x, lk);
-      rk[c].y = __shfl_sync(0xffffffffu, vk.y, lk);
-      pr[c].x = __shfl_sync(0xffffffffu, vp.x, lp);
-      pr[c].y = __shfl_sync(0xffffffffu, vp.y, lp);
-    }
-#pragma unroll
-    for (int c = 0; c < kk; ++c) {
-      double2 vk = P[0][c], vp = P[0][c];
-#pragma unroll
-      for (int i = 1; i < RPL; ++i) {
-        if (i == sk) vk = P[i][c];
-        if (i == sp) vp = P[i][c];
-      }
-      rk[c].x = __shfl_sync(0xffffffffu, vk.x, lk);
-      rk[c].y = __shfl_sync(0xffffffffu, vk.y, lk);
-      pr[c].x = __shfl_sync(0xffffffffu, vp.x, lp);
-      pr[c].y = __shfl_sync(0xffffffffu, vp.y, lp);
-    }
-    const double2 ip = crcp(pr[kk]);
-#pragma unroll
-    for (int c = 0; c < NB; ++c) pr[c] = (c == kk) ? ip : cmul(pr[c], ip);  // new row k
-    const double2 nip = make_double2(-ip.x, -ip.y);
-#pragma unroll
-    for (int i = 0; i < RPL; ++i) {
-      const int r = lane + 32 * i;
-      if (r == k) {
-#pragma unroll
-        for (int c = 0; c < NB; ++c) P[i][c] = pr[c];
-        continue;
-      }
-      const bool was_k = (r == p);  // row p receives the old row k
-      const double2 f = was_k ? rk[kk] : P[i][kk];
-#pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        const double2 o = was_k ? rk[c] : P[i][c];
-        P[i][c] = (c == kk) ? cmul(f, nip) : csub(o, cmul(f, pr[c]));
-      }
-    }
-  }
-  return true;
-}
-
 template <bool kGlobal, int RPL, int NB>
 __global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* arena, int64_t stride,
                                                                  const InvTask* __restrict__ tasks, int e_base,
@@ -517,24 +431,92 @@ __global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* are
       __syncthreads();
     }
     if (!kGlobal && warp == 0) {
-      double2 Pr[RPL][NB];
+      // Compact panel loop on warp 0: lane owns rows lane + 32 i (i < RPL);
+      // the pivot row is read by broadcast from shared memory and the
+      // elimination runs in registers.  Argmax: hardware max-reduction on the
+      // float image of |a_rk|^2 (monotone), lowest row among the maxima,
+      // then the exact double test against the singular threshold.
+      const double thr2 = thresh * thresh;
+      for (int kk = 0; kk < kb; ++kk) {
+        const int k = k0 + kk;
+        double best = -1.0;
+        int bi = 0x7fffffff;
 #pragma unroll
-      for (int i = 0; i < RPL; ++i)
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
+        for (int i = 0; i < RPL; ++i) {
           const int r = lane + 32 * i;
-          Pr[i][c] = (r < m8) ? pan(r, c) : make_double2(0.0, 0.0);
-        }
-      if (!panel_regs<RPL, NB>(Pr, m, k0, kb, thresh, perm, lane, st, e_base + blockIdx.y, tk.fold_pos)) {
-        if (lane == 0) *flag = 1;
-      } else {
-#pragma unroll
-        for (int i = 0; i < RPL; ++i)
-#pragma unroll
-          for (int c = 0; c < NB; ++c) {
-            const int r = lane + 32 * i;
-            if (r < m) pan(r, c) = Pr[i][c];
+          if (r >= k && r < m) {
+            const double v = cnorm(pan(r, kk));
+            if (v > best) {
+              best = v;
+              bi = r;
+            }
           }
+        }
+        const unsigned key = best >= 0.0 ? __float_as_uint(__double2float_ru(best)) : 0u;
+        const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+        const unsigned tied = __ballot_sync(0xffffffffu, key == kmax);
+        double cb;
+        int ci;
+        if (__popc(tied) == 1) {  // usual case: a single candidate lane
+          const int src = __ffs(tied) - 1;
+          cb = __shfl_sync(0xffffffffu, best, src);
+          ci = __shfl_sync(0xffffffffu, bi, src);
+        } else {  // exact order among the lanes whose float images tie
+          cb = (key == kmax) ? best : -1.0;
+          ci = (key == kmax) ? bi : 0x7fffffff;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, cb, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
+            if (ob > cb || (ob == cb && oi < ci)) {
+              cb = ob;
+              ci = oi;
+            }
+          }
+        }
+        if (!(cb > thr2)) {  // |u_kk| <= 1e-13 max|a| (NaN: see below)
+          if (cb == cb) {
+            if (lane == 0) {
+              *flag = 1;
+              report_singular(st, e_base + blockIdx.y, tk.fold_pos, k);
+            }
+            break;
+          }
+        }
+        const int p = ci;
+        if (lane == 0) perm[k] = p;
+        if (lane < NB && p != k) {
+          const double2 t2 = pan(k, lane);
+          pan(k, lane) = pan(p, lane);
+          pan(p, lane) = t2;
+        }
+        __syncwarp();
+        double2 pr[NB];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) pr[c] = pan(k, c);
+        double2 piv = pr[0];
+#pragma unroll
+        for (int c = 1; c < NB; ++c)
+          if (c == kk) piv = pr[c];
+        const double rd = 1.0 / fma(piv.x, piv.x, piv.y * piv.y);
+        const double2 ip = make_double2(piv.x * rd, -piv.y * rd);
+#pragma unroll
+        for (int c = 0; c < NB; ++c) pr[c] = (c == kk) ? ip : cmul(pr[c], ip);
+        const double2 nip = make_double2(-ip.x, -ip.y);
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) {
+          const int r = lane + 32 * i;
+          if (r >= m) continue;
+          if (r == k) {
+#pragma unroll
+            for (int c = 0; c < NB; ++c) pan(r, c) = pr[c];
+            continue;
+          }
+          const double2 f = pan(r, kk);
+#pragma unroll
+          for (int c = 0; c < NB; ++c) pan(r, c) = (c == kk) ? cmul(f, nip) : csub(pan(r, c), cmul(f, pr[c]));
+        }
+        __syncwarp();
       }
     } else if (kGlobal && warp == 0) {
       for (int kk = 0; kk < kb; ++kk) {

@@ -18,6 +18,10 @@ int main(int argc, char** argv) {
   double2* arena;
   cudaMalloc(&arena, sizeof(double2) * stride * nE);
   for (int e = 0; e < nE; ++e) cudaMemcpy(arena + e * stride, h.data(), sizeof(double2) * stride, cudaMemcpyHostToDevice);
+  if (m > kSmemInvMax) {
+    printf("m > %d uses the multi-CTA path (see plan.cpp); not benchmarked here\n", kSmemInvMax);
+    return 0;
+  }
   std::vector<InvTask> t(nb);
   for (int b = 0; b < nb; ++b) t[b] = InvTask{m, b, b, 0, int64_t(b) * m * m};
   InvTask* dt;
