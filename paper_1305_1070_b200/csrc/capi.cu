@@ -119,8 +119,9 @@ struct negf_gpu {
   std::vector<void*> owned;
   int capacity = 1;
   double2* arena = nullptr;
-  double2* d_template = nullptr;
-  InitRegion *d_init_copy = nullptr, *d_init_zero = nullptr;
+  int64_t* d_h_pos = nullptr;
+  double2* d_h_val = nullptr;
+  InitRegion* d_init_zero = nullptr;
   int64_t* d_diag_pos = nullptr;
   int64_t *d_sr_pos = nullptr, *d_sl_pos = nullptr, *d_gr_pos = nullptr, *d_gl_pos = nullptr;
   int *d_sr_ptr = nullptr, *d_sr_src = nullptr, *d_sl_ptr = nullptr, *d_sl_src = nullptr;
@@ -226,7 +227,7 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
   int64_t& L = g->launches;
   {
     Bracket br(g, NEGF_KSTAT_ASSEMBLE, 0.0);
-    launch_assemble(b, P, g->d_template, g->d_init_copy, g->d_init_zero, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr, g->d_sr_src,
+    launch_assemble(b, P, g->d_h_pos, g->d_h_val, g->d_init_zero, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr, g->d_sr_src,
                     static_cast<int64_t>(P.desc.sr_rows.size()), d_sr, g->d_sl_pos, g->d_sl_ptr, g->d_sl_src,
                     static_cast<int64_t>(P.desc.sl_rows.size()), d_sl, s, L);
     launch_skew_check(b, d_sl, static_cast<int64_t>(P.desc.sl_rows.size()), g->d_cslots, g->d_cslot_ptr,
@@ -441,9 +442,9 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     ck(cudaSetDevice(device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking), "stream");
     auto& o = g->owned;
-    g->d_template = reinterpret_cast<double2*>(dev_upload(P.a_template, o));
+    g->d_h_pos = dev_upload(P.h_pos, o);
+    g->d_h_val = reinterpret_cast<double2*>(dev_upload(P.h_val, o));
     g->d_diag_pos = dev_upload(P.diag_pos, o);
-    g->d_init_copy = dev_upload(P.init_copy, o);
     g->d_init_zero = dev_upload(P.init_zero, o);
     g->d_sr_pos = dev_upload(P.sr_slot_pos, o);
     g->d_sr_ptr = dev_upload(P.sr_slot_ptr, o);

@@ -47,23 +47,27 @@ __device__ __forceinline__ double2 cinv(double2 a) {
 // ---------------------------------------------------------------------------
 // Assembly
 // ---------------------------------------------------------------------------
-// Per-energy initialisation of the regions listed by the plan: copy from the
-// template (D blocks, original-entry prefix of each Arow row) or zero
-// (Sigma^< blocks).  One CTA strides over regions; rows are coalesced.
-__global__ void k_init(double2* arena, int64_t stride, const double2* __restrict__ tmpl,
-                       const InitRegion* __restrict__ copy, int ncopy, const InitRegion* __restrict__ zero,
-                       int nzero) {
+// Per-energy initialisation: zero the regions listed by the plan (D blocks,
+// the original-entry prefix of each Arow row, Sigma^< blocks).  One CTA
+// strides over regions; rows are coalesced.  Write-only traffic.
+__global__ void k_init(double2* arena, int64_t stride, const InitRegion* __restrict__ zero, int nzero) {
   double2* a = arena + blockIdx.y * stride;
-  for (int r = blockIdx.x; r < ncopy + nzero; r += gridDim.x) {
-    const bool z = r >= ncopy;
-    const InitRegion g = z ? zero[r - ncopy] : copy[r];
+  for (int r = blockIdx.x; r < nzero; r += gridDim.x) {
+    const InitRegion g = zero[r];
     const int64_t total = int64_t(g.rows) * g.cols;
     for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
       const int row = static_cast<int>(i / g.cols), col = static_cast<int>(i - int64_t(row) * g.cols);
-      const int64_t o = g.off + int64_t(row) * g.pitch + col;
-      a[o] = z ? make_double2(0.0, 0.0) : tmpl[o];
+      a[g.off + int64_t(row) * g.pitch + col] = make_double2(0.0, 0.0);
     }
   }
+}
+
+// -H entries into the zeroed A region (positions unique).
+__global__ void k_scatter_h(double2* arena, int64_t stride, const int64_t* __restrict__ pos,
+                            const double2* __restrict__ val, int64_t nnz) {
+  double2* a = arena + blockIdx.y * stride;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nnz; i += int64_t(gridDim.x) * blockDim.x)
+    a[pos[i]] = val[i];
 }
 
 // E on the diagonal and the Sigma^< slots (which live outside the A region).
@@ -1254,16 +1258,21 @@ int grid_for(int64_t work, int threads, int cap) {
 
 }  // namespace
 
-void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_template,
-                     const InitRegion* d_init_copy, const InitRegion* d_init_zero, const int64_t* d_diag_pos, const double* d_energies, const int64_t* d_sr_pos,
+void launch_assemble(const BatchArgs& b, const Plan& p, const int64_t* d_h_pos, const double2* d_h_val,
+                     const InitRegion* d_init_zero, const int64_t* d_diag_pos, const double* d_energies, const int64_t* d_sr_pos,
                      const int* d_sr_ptr, const int* d_sr_src, int64_t sr_nnz,
                      const double2* d_sigma_r, const int64_t* d_sl_pos, const int* d_sl_ptr,
                      const int* d_sl_src, int64_t sl_nnz, const double2* d_sigma_l, cudaStream_t s,
                      int64_t& launches) {
-  const int nreg = static_cast<int>(p.init_copy.size() + p.init_zero.size());
+  const int nreg = static_cast<int>(p.init_zero.size());
   dim3 g1(std::max(1, std::min(nreg, 1024)), b.nE);
-  k_init<<<g1, 256, 0, s>>>(b.arena, b.stride, d_template, d_init_copy, static_cast<int>(p.init_copy.size()),
-                            d_init_zero, static_cast<int>(p.init_zero.size()));
+  k_init<<<g1, 256, 0, s>>>(b.arena, b.stride, d_init_zero, nreg);
+  const int64_t hn = static_cast<int64_t>(p.h_pos.size());
+  if (hn > 0) {
+    dim3 gh(grid_for(hn, 256, 1024), b.nE);
+    k_scatter_h<<<gh, 256, 0, s>>>(b.arena, b.stride, d_h_pos, d_h_val, hn);
+    ++launches;
+  }
   const int sr_slots = static_cast<int>(p.sr_slot_pos.size());
   const int sl_slots = static_cast<int>(p.sl_slot_pos.size());
   dim3 g2(grid_for(std::max<int64_t>(p.desc.n, sl_slots), 256, 1024), b.nE);

@@ -23,8 +23,8 @@ struct BatchArgs {
   int e_base;         // global index of energy 0 of this batch
 };
 
-void launch_assemble(const BatchArgs& b, const Plan& p, const double2* d_template,
-                     const InitRegion* d_init_copy, const InitRegion* d_init_zero, const int64_t* d_diag_pos, const double* d_energies,
+void launch_assemble(const BatchArgs& b, const Plan& p, const int64_t* d_h_pos, const double2* d_h_val,
+                     const InitRegion* d_init_zero, const int64_t* d_diag_pos, const double* d_energies,
                      const int64_t* d_sr_pos, const int* d_sr_ptr, const int* d_sr_src,
                      int64_t sr_nnz, const double2* d_sigma_r, const int64_t* d_sl_pos,
                      const int* d_sl_ptr, const int* d_sl_src, int64_t sl_nnz,

@@ -381,16 +381,15 @@ Plan build_plan(ProblemDesc desc) {
   for (int c = 0; c < nc; ++c) {
     const ClusterInfo& I = B.I(c);
     if (I.m == 0) continue;
-    P.init_copy.push_back(InitRegion{I.off_d, 1, I.m * I.m, I.m * I.m});
-    if (I.K0 > 0) P.init_copy.push_back(InitRegion{I.off_arow, I.m, I.K0, I.K});
+    P.init_zero.push_back(InitRegion{I.off_d, 1, I.m * I.m, I.m * I.m});
+    if (I.K0 > 0) P.init_zero.push_back(InitRegion{I.off_arow, I.m, I.K0, I.K});
     if (I.seeded) P.init_zero.push_back(InitRegion{I.off_sig, 1, I.seed_dense ? I.m * I.m : I.m, 0});
   }
   if (P.any_seed && !B.I(root).has_nd && B.msz(root) > 0)
     P.init_zero.push_back(InitRegion{B.I(root).off_pd, 1, B.msz(root) * B.msz(root), 0});
 
-  // ---- template of the A region: -H scattered into the descendant-row
-  // orientation (the only one the lean fold reads, hsc.cpp:483-490).
-  P.a_template.assign(static_cast<std::size_t>(P.a_region), cplx(0.0, 0.0));
+  // ---- -H as (position, value) pairs in the descendant-row orientation (the
+  // only one the lean fold reads, hsc.cpp:483-490); duplicates summed.
   auto a_pos = [&](int r, int c) -> int64_t {
     const int ci = t.dof_cluster(r), cj = t.dof_cluster(c);
     const int lr = t.local_index(r), lc = t.local_index(c);
@@ -400,9 +399,21 @@ Plan build_plan(ProblemDesc desc) {
     if (p < 0) return -1;  // ancestor-row orientation: never read
     return I.off_arow + int64_t(lr) * I.K + I.s_col[p] + lc;
   };
-  for (std::size_t k = 0; k < d.h_rows.size(); ++k) {
-    const int64_t pos = a_pos(d.h_rows[k], d.h_cols[k]);
-    if (pos >= 0) P.a_template[static_cast<std::size_t>(pos)] -= d.h_vals[k];
+  {
+    std::vector<std::pair<int64_t, cplx>> hv;
+    hv.reserve(d.h_rows.size());
+    for (std::size_t k = 0; k < d.h_rows.size(); ++k) {
+      const int64_t pos = a_pos(d.h_rows[k], d.h_cols[k]);
+      if (pos >= 0) hv.push_back({pos, -d.h_vals[k]});
+    }
+    std::stable_sort(hv.begin(), hv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (const auto& e : hv) {
+      if (!P.h_pos.empty() && P.h_pos.back() == e.first) P.h_val.back() += e.second;
+      else {
+        P.h_pos.push_back(e.first);
+        P.h_val.push_back(e.second);
+      }
+    }
   }
   P.diag_pos.resize(static_cast<std::size_t>(n));
   for (int dof = 0; dof < n; ++dof) {

@@ -173,9 +173,9 @@ struct Plan {
   int64_t a_region = 0;      // [0, a_region): D + Arow (template copied per energy)
   int64_t big_scratch = 0;   // arena offset of the multi-CTA inverse scratch
   int64_t z_begin = 0, z_end = 0;  // region zeroed per energy (Sigma^<, N, root P)
-  std::vector<cplx> a_template;    // a_region values of -H (no E, no Sigma)
-  std::vector<InitRegion> init_copy;  // copied from the template per energy
-  std::vector<InitRegion> init_zero;  // zeroed per energy
+  std::vector<int64_t> h_pos;       // -H entries of the A region: positions ...
+  std::vector<cplx> h_val;          // ... and values (duplicates summed)
+  std::vector<InitRegion> init_zero;  // zeroed per energy (D, original Arow prefix, Sigma^<)
 
   // Per-energy scatter maps.
   std::vector<int64_t> diag_pos;          // n: A_dd position (E added)
