@@ -1037,40 +1037,49 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
     const bool a_rk = (tm.a_op == OP_N);
     const bool b_kr = (tm.b_op == OP_N || tm.b_op == OP_C);
     const int ksteps = min(KC, tm.k - ck0);
-    if (live_i > 0 && live_j > 0) {
+    // One k4-step of the 2x2 subtile block (3M products).
+    auto kstep = [&](int s) {
+      const int kk = 4 * s + t;
+      double2 a[2], b[2];
 #pragma unroll
-      for (int s = 0; s < KC / 4; ++s) {
-        if (4 * s >= ksteps) break;
-        const int kk = 4 * s + t;
-        double2 a[2], b[2];
+      for (int i = 0; i < 2; ++i) {
+        const int r = wm + 8 * i + g;
+        a[i] = a_rk ? As[r * LD_RK + kk] : As[kk * A::LDA_KR + r];
+        a[i].x *= sg;
+        a[i].y *= sg;
+      }
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int r = wm + 8 * i + g;
-          a[i] = a_rk ? As[r * LD_RK + kk] : As[kk * A::LDA_KR + r];
-          a[i].x *= sg;
-          a[i].y *= sg;
-        }
+      for (int j = 0; j < 2; ++j) {
+        const int c = wn + 8 * j + g;
+        b[j] = b_kr ? Bs[kk * A::LDB_KR + c] : Bs[c * LD_RK + kk];
+        if (conjb) b[j].y = -b[j].y;
+      }
+      double as[2], bs[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (i >= live_i) break;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          const int c = wn + 8 * j + g;
-          b[j] = b_kr ? Bs[kk * A::LDB_KR + c] : Bs[c * LD_RK + kk];
-          if (conjb) b[j].y = -b[j].y;
+          if (j >= live_j) break;
+          dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+          dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].y);
+          dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
         }
-        double as[2], bs[2];
+      }
+    };
+    if (live_i > 0 && live_j > 0) {
+      if (ksteps == KC) {  // full chunk: straight-line, loads can be hoisted
 #pragma unroll
-        for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
+        for (int s = 0; s < KC / 4; ++s) kstep(s);
+      } else {
 #pragma unroll
-        for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (i >= live_i) break;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (j >= live_j) break;
-            dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
-            dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].y);
-            dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
-          }
+        for (int s = 0; s < KC / 4; ++s) {
+          if (4 * s >= ksteps) break;
+          kstep(s);
         }
       }
     }
