@@ -49,7 +49,8 @@ enum {
   NEGF_CONFIG_ERROR = 7,         /* ConfigError (errors.hpp:21-25)          */
   NEGF_PARTITION_VIOLATION = 8,  /* PartitionViolation (errors.hpp:44-53)   */
   NEGF_RESIDUAL_TOO_LARGE = 9,   /* ResidualTooLarge (errors.hpp:67-71)     */
-  NEGF_INTERNAL = 10
+  NEGF_INTERNAL = 10,
+  NEGF_CONVERGENCE_ERROR = 11    /* ConvergenceError (errors.hpp:56-61)     */
 };
 
 typedef struct {
@@ -178,6 +179,84 @@ int negf_nccl_unique_id(char id_out[128], negf_status* st);
 int negf_gpu_nccl_init(negf_gpu* g, const char id[128], int nranks, int rank, negf_status* st);
 /* In-place sum of the unscaled density accumulators across ranks. */
 int negf_gpu_allreduce_density(negf_gpu* g, negf_status* st);
+
+/* ---- Contact self-energies on the GPU -------------
+ *
+ *   negf_lead_*                surface_self_energy  proj/src/device.cpp:195-251
+ *                              (energy-doubling decimation, fixed-point test
+ *                              ||refined - g||_F <= 1e-10, <= 200 sweeps), the
+ *                              per-energy call of attach_contacts
+ *                              device.cpp:262-304 / sigma_for_energy
+ *                              run.cpp:90-109, batched over energies
+ *   negf_lead_modes_sigma_device  analytic transverse-mode Sigma of a uniform
+ *                              hard-wall 2-D effective-mass lead (the lead model
+ *                              BASELINE.json names for configs 1/2/4/5)
+ *   negf_contacts_fill_device  lesser_self_energy device.cpp:322-366 and the
+ *                              placement of the contact / phonon
+ *                              (phonon_self_energy device.cpp:306-320) values
+ *                              into the Sigma^r / Sigma^< pattern arrays of
+ *                              negf_gpu_solve_batch_device
+ */
+typedef struct negf_lead negf_lead;
+/* One dense lead: onsite block h00 and coupling h01 (w x w complex,
+ * row-major).  criterion 0 = the reference's surface_self_energy: h01 couples
+ * a lead cell to the next one away from the device, the fixed-point test
+ * ||refined - g||_F <= 1e-10 ends the sweeps and Sigma = h01^H g h01.
+ * criterion 1 = decay test max|alpha|, max|beta| < tol (alpha_0 = h01,
+ * beta_0 = h01^T) and Sigma = h01^T (z - es)^-1 h01 (the convention of
+ * paper_1305_1070_b200/devices.py sancho_rubio, used for config 3).
+ * Errors as the reference: eta <= 0 -> NEGF_CONFIG_ERROR; w out of range ->
+ * NEGF_CONTRACT_VIOLATION. */
+int negf_lead_create(int device, int w, const double* h00, const double* h01, double eta_ev, int criterion,
+                     double tol, int max_energy_batch, negf_lead** out, negf_status* st);
+/* Sigma^r(E_k) = h01^H g_s(E_k) h01 (made exactly complex symmetric), for
+ * n_energies energies.  Host variant: energies[nE] -> sigma_out[nE][w][w].
+ * Errors report the lowest failing energy (first_energy_index + k):
+ * NEGF_SINGULAR_BLOCK from an inverse, NEGF_CONVERGENCE_ERROR after 200
+ * sweeps. */
+int negf_lead_sigma(negf_lead* l, int n_energies, const double* energies, int first_energy_index,
+                    double* sigma_out, negf_status* st);
+/* Device variant: d_energies[nE] -> d_sigma_out + k*ld_out (complex
+ * elements, ld_out >= w*w).  Synchronous on the handle's stream. */
+int negf_lead_sigma_device(negf_lead* l, int n_energies, const double* d_energies, int first_energy_index,
+                           double* d_sigma_out, int64_t ld_out, negf_status* st);
+/* Decimation sweeps each energy of the last call needed (index of the
+ * converged sweep, as the reference's loop counter), sweeps_out[nE]. */
+int negf_lead_last_sweeps(const negf_lead* l, int32_t* sweeps_out);
+int64_t negf_lead_last_launches(const negf_lead* l);
+void* negf_lead_stream(negf_lead* l);
+void negf_lead_destroy(negf_lead* l);
+
+/* Analytic lead: Sigma_ab(E) = sum_m phi_am (-t lambda_m) phi_bm with
+ * phi_ym = sqrt(2/(w+1)) sin(y m pi/(w+1)), eps_m = 4t - 2t cos(m pi/(w+1)),
+ * z = (eps_m - E - i eta)/(2t), lambda_m = z -+ sqrt(z^2 - 1) with
+ * |lambda_m| <= 1; symmetrised like surface_self_energy.  Runs on `stream`
+ * (a cudaStream_t, NULL = legacy default stream). */
+int negf_lead_modes_sigma_device(int w, double t_ev, double eta_ev, int n_energies, const double* d_energies,
+                                 double* d_sigma_out, int64_t ld_out, void* stream, negf_status* st);
+
+/* One dense contact block in the pattern arrays: its w*w entries are
+ * consecutive, row-major, starting at sr_off in Sigma^r and sl_off in
+ * Sigma^< (-1 = absent). */
+typedef struct {
+  int w;
+  const double* d_sigma;   /* device, complex, energy k at d_sigma + 2*k*ld */
+  int64_t ld;              /* complex elements between energies           */
+  int64_t sr_off, sl_off;
+  double mu_ev;            /* contact chemical potential                  */
+} negf_contact_desc;
+/* Fills, per energy k, the contact blocks of Sigma^r (copy) and Sigma^<
+ * (-f(E_k; mu) (S - S^H), device.cpp:335-342) and the phonon diagonal
+ * (Sigma^r = -i gamma_d; Sigma^< = -f(E_k; mu_ph) (s - conj s),
+ * device.cpp:356-362) with f the Fermi function of device.cpp:253-260 at
+ * kT_ev (= kBoltzmannEvPerK * temperature_k).  Phonon entries are n_phonon
+ * consecutive pattern entries from ph_sr_off / ph_sl_off (-1 = absent).
+ * Pattern entries not named here are left untouched. */
+int negf_contacts_fill_device(int n_energies, const double* d_energies, double kT_ev, int n_contacts,
+                              const negf_contact_desc* contacts, int n_phonon, const double* d_phonon_gamma,
+                              int64_t ph_sr_off, int64_t ph_sl_off, double mu_phonon_ev, double* d_sigma_r,
+                              int64_t sr_stride, double* d_sigma_lesser, int64_t sl_stride, void* stream,
+                              negf_status* st);
 
 #ifdef __cplusplus
 }

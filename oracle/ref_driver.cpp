@@ -501,11 +501,54 @@ int cmd_device(int argc, char** argv) {
   return 0;
 }
 
+// ref_driver lead in.bin out.bin : surface_self_energy (device.cpp:195-251)
+// of one dense lead at nE energies.  in: "NEGFLED1", int32 w, int32 nE,
+// f64 eta, h00[w*w], h01[w*w] (complex, row-major), f64 energies[nE].
+// out: "NEGFLEO1", int32 nE, then per energy int32 code (0 ok, 1
+// ConvergenceError, 2 SingularBlock, 3 other) and w*w complex (zeros on error).
+int cmd_lead(char** argv) {
+  std::ifstream in(argv[2], std::ios::binary);
+  char magic[8];
+  in.read(magic, 8);
+  if (std::memcmp(magic, "NEGFLED1", 8) != 0) throw std::runtime_error("bad lead input");
+  int32_t w = 0, ne = 0;
+  double eta = 0.0;
+  in.read(reinterpret_cast<char*>(&w), 4);
+  in.read(reinterpret_cast<char*>(&ne), 4);
+  in.read(reinterpret_cast<char*>(&eta), 8);
+  CMatrix h00(w, w), h01(w, w);
+  in.read(reinterpret_cast<char*>(h00.data()), sizeof(cplx) * w * w);
+  in.read(reinterpret_cast<char*>(h01.data()), sizeof(cplx) * w * w);
+  std::vector<double> es(static_cast<std::size_t>(ne));
+  in.read(reinterpret_cast<char*>(es.data()), 8 * ne);
+  if (!in) throw std::runtime_error("short lead input");
+  std::ofstream out(argv[3], std::ios::binary);
+  out.write("NEGFLEO1", 8);
+  out.write(reinterpret_cast<const char*>(&ne), 4);
+  for (double e : es) {
+    int32_t code = 0;
+    CMatrix s(w, w);
+    try {
+      s = surface_self_energy(h00, h01, e, eta);
+    } catch (const ConvergenceError&) {
+      code = 1;
+    } catch (const SingularBlock&) {
+      code = 2;
+    } catch (const Error&) {
+      code = 3;
+    }
+    out.write(reinterpret_cast<const char*>(&code), 4);
+    out.write(reinterpret_cast<const char*>(s.data()), sizeof(cplx) * w * w);
+  }
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc >= 10 && std::string(argv[1]) == "synthetic") return cmd_synthetic(argc, argv);
   if (argc >= 4 && std::string(argv[1]) == "device") return cmd_device(argc, argv);
+  if (argc >= 4 && std::string(argv[1]) == "lead") return cmd_lead(argv);
   if (argc >= 4 && std::string(argv[1]) == "cli") {
     scipy_openblas_set_num_threads64_(1);
     try {

@@ -260,3 +260,53 @@ def dump_synthetic(nx, ny, seed, fuzz, coupling, max_leaf, energies, path) -> No
 
 def dump_device(config_path: str, path: str) -> None:
     subprocess.run([REF_BIN, "device", config_path, path], check=True)
+
+
+# -- dense leads (ref_driver lead: surface_self_energy, device.cpp:195-251) ----
+def write_lead(path: str, h00: np.ndarray, h01: np.ndarray, eta: float, energies) -> None:
+    w = h00.shape[0]
+    e = np.asarray(energies, np.float64)
+    with open(path, "wb") as f:
+        f.write(b"NEGFLED1")
+        f.write(struct.pack("<iid", w, len(e), float(eta)))
+        f.write(np.ascontiguousarray(h00, np.complex128).tobytes())
+        f.write(np.ascontiguousarray(h01, np.complex128).tobytes())
+        f.write(e.tobytes())
+
+
+def read_lead(path: str):
+    """Returns (w, eta, h00, h01, energies) of a NEGFLED1 file."""
+    with open(path, "rb") as f:
+        buf = f.read()
+    assert buf[:8] == b"NEGFLED1"
+    w, ne, eta = struct.unpack_from("<iid", buf, 8)
+    pos = 24
+    h00 = np.frombuffer(buf, np.complex128, w * w, pos).reshape(w, w).copy()
+    pos += 16 * w * w
+    h01 = np.frombuffer(buf, np.complex128, w * w, pos).reshape(w, w).copy()
+    pos += 16 * w * w
+    e = np.frombuffer(buf, np.float64, ne, pos).copy()
+    return w, eta, h00, h01, e
+
+
+def read_lead_out(path: str, w: int):
+    """Returns (codes[nE], sigma[nE, w, w]) of a NEGFLEO1 file."""
+    with open(path, "rb") as f:
+        buf = f.read()
+    assert buf[:8] == b"NEGFLEO1"
+    (ne,) = struct.unpack_from("<i", buf, 8)
+    pos = 12
+    codes = np.zeros(ne, np.int32)
+    sig = np.zeros((ne, w, w), np.complex128)
+    for k in range(ne):
+        (codes[k],) = struct.unpack_from("<i", buf, pos)
+        pos += 4
+        sig[k] = np.frombuffer(buf, np.complex128, w * w, pos).reshape(w, w)
+        pos += 16 * w * w
+    return codes, sig
+
+
+def run_lead(in_path: str, out_path: str, timeout: float | None = None):
+    subprocess.run([REF_BIN, "lead", in_path, out_path], check=True, timeout=timeout)
+    w = read_lead(in_path)[0]
+    return read_lead_out(out_path, w)

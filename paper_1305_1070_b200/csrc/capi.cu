@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "capi_util.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
 #include "tree.hpp"
@@ -60,52 +61,6 @@ NcclApi& nccl() {
   api.err = reinterpret_cast<nccl_err_t>(dlsym(h, "ncclGetErrorString"));
   api.ok = api.get_id && api.init && api.allreduce && api.destroy;
   return api;
-}
-
-int set_status(negf_status* st, int code, const std::string& msg, int energy = -1, int cluster = -1,
-               int pivot = -1, int dof = -1) {
-  if (st) {
-    st->code = code;
-    st->energy_index = energy;
-    st->cluster = cluster;
-    st->pivot = pivot;
-    st->dof = dof;
-    std::snprintf(st->msg, sizeof st->msg, "%s", msg.c_str());
-  }
-  return code;
-}
-
-int ok(negf_status* st) { return set_status(st, NEGF_OK, ""); }
-
-struct CudaFail {
-  int code;
-  std::string msg;
-};
-
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    const int code = (e == cudaErrorMemoryAllocation) ? NEGF_OUT_OF_MEMORY : NEGF_CUDA_ERROR;
-    throw CudaFail{code, std::string(what) + ": " + cudaGetErrorString(e)};
-  }
-}
-
-template <class T>
-T* dev_upload(const std::vector<T>& v, std::vector<void*>& owned) {
-  if (v.empty()) return nullptr;
-  T* p = nullptr;
-  ck(cudaMalloc(&p, sizeof(T) * v.size()), "cudaMalloc");
-  owned.push_back(p);
-  ck(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice), "upload");
-  return p;
-}
-
-template <class T>
-T* dev_alloc(size_t count, std::vector<void*>& owned) {
-  if (count == 0) count = 1;
-  T* p = nullptr;
-  ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc");
-  owned.push_back(p);
-  return p;
 }
 
 constexpr double kTwoPi = 6.283185307179586476925286766559;

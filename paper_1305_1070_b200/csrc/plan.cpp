@@ -29,6 +29,11 @@ void insert_anc_order(std::vector<int>& list, const Tree& t, int j) {
   list.insert(it, j);
 }
 
+struct InvItem {
+  int m, cluster, fold_pos;
+  int64_t off;
+};
+
 struct Builder {
   Plan& P;
   const Tree& t;
@@ -146,6 +151,66 @@ struct Builder {
     }
     for (int m0 = 0; m0 < m; m0 += kArrTM[best])
       for (int n0 = 0; n0 < n; n0 += kArrTN[best]) P.gemm_tiles.push_back(GemmTile{id, m0, n0, best});
+  }
+
+  // Inverses of one group: shared-memory kernels by size class, then the
+  // multi-CTA blocked Gauss-Jordan for the large blocks (kPanel-wide panels)
+  // with its scratch from `scratch_off` on.
+  void emit_inverses(int l, int phase, const std::vector<InvItem>& items, int64_t scratch_off) {
+    auto& T = P.gemm_terms;
+    open(K_INVERSE, phase, l);
+    auto size_class = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : 3; };
+    for (int pass = 0; pass < 4; ++pass)  // grouped by kernel variant
+      for (const InvItem& it : items)
+        if (it.m > 0 && it.m <= kSmemInvMax && size_class(it.m) == pass) {
+          P.inv_tasks.push_back(InvTask{it.m, it.cluster, it.fold_pos, 0, it.off});
+          cur.cmul += double(it.m) * it.m * it.m;
+        }
+    close();
+    std::vector<BigTask> big;
+    int64_t so = scratch_off;
+    int mmax = 0;
+    for (const InvItem& it : items) {
+      const int m = it.m;
+      if (m <= kSmemInvMax) continue;
+      BigTask bt{};
+      bt.m = m;
+      bt.fold_pos = it.fold_pos;
+      bt.cluster = it.cluster;
+      bt.off = it.off;
+      bt.off_mp = so;
+      so += align8(int64_t(m) * kPanel);
+      bt.off_rs = so;
+      so += align8(int64_t(m) * kPanel);
+      bt.off_perm = so;
+      so += align8((m + 3) / 4);
+      bt.off_thr = so;
+      so += 8;
+      big.push_back(bt);
+      mmax = std::max(mmax, m);
+    }
+    if (big.empty()) return;
+    for (int k0 = 0; k0 < mmax; k0 += kPanel) {
+      open(K_PANEL, phase, l);
+      cur.k0 = k0;
+      for (const BigTask& bt : big)
+        if (bt.m > k0) {
+          P.big_tasks.push_back(bt);
+          cur.cmul += double(bt.m) * kPanel * kPanel;
+        }
+      close();
+      open(K_GEMM, phase, l);  // rank-kPanel update R += (M_p - I_p) R_p
+      for (const BigTask& bt : big) {
+        if (bt.m <= k0) continue;
+        const int tb = static_cast<int>(T.size());
+        add_term(T, kPanel, OP_N, bt.off_mp, kPanel, OP_N, bt.off_rs, bt.m, +1);
+        gemm_task(bt.m, bt.m, bt.off, bt.m, MODE_ADD, 0, 0, tb);
+      }
+      close();
+    }
+    open(K_PERM, phase, l);
+    for (const BigTask& bt : big) P.big_tasks.push_back(bt);
+    close();
   }
 };
 
@@ -504,59 +569,9 @@ Plan build_plan(ProblemDesc desc) {
   // Inverses of one level: shared-memory kernels by size class, then the
   // multi-CTA blocked Gauss-Jordan for the large blocks (kPanel-wide panels).
   auto emit_inverses = [&](int l, const std::vector<int>& xs) {
-    B.open(K_INVERSE, 0, l);
-    auto size_class = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : 3; };
-    for (int pass = 0; pass < 4; ++pass)  // grouped by kernel variant
-      for (int x : xs)
-        if (B.msz(x) > 0 && B.msz(x) <= kSmemInvMax && size_class(B.msz(x)) == pass) {
-          P.inv_tasks.push_back(InvTask{B.msz(x), x, fold_pos[x], 0, B.I(x).off_d});
-          B.cur.cmul += double(B.msz(x)) * B.msz(x) * B.msz(x);
-        }
-    B.close();
-    std::vector<BigTask> big;
-    int64_t so = P.big_scratch;
-    int mmax = 0;
-    for (int x : xs) {
-      const int m = B.msz(x);
-      if (m <= kSmemInvMax) continue;
-      BigTask bt{};
-      bt.m = m;
-      bt.fold_pos = fold_pos[x];
-      bt.cluster = x;
-      bt.off = B.I(x).off_d;
-      bt.off_mp = so;
-      so += align8(int64_t(m) * kPanel);
-      bt.off_rs = so;
-      so += align8(int64_t(m) * kPanel);
-      bt.off_perm = so;
-      so += align8((m + 3) / 4);
-      bt.off_thr = so;
-      so += 8;
-      big.push_back(bt);
-      mmax = std::max(mmax, m);
-    }
-    if (big.empty()) return;
-    for (int k0 = 0; k0 < mmax; k0 += kPanel) {
-      B.open(K_PANEL, 0, l);
-      B.cur.k0 = k0;
-      for (const BigTask& bt : big)
-        if (bt.m > k0) {
-          P.big_tasks.push_back(bt);
-          B.cur.cmul += double(bt.m) * kPanel * kPanel;
-        }
-      B.close();
-      B.open(K_GEMM, 0, l);  // rank-kPanel update R += (M_p - I_p) R_p
-      for (const BigTask& bt : big) {
-        if (bt.m <= k0) continue;
-        const int tb = static_cast<int>(T.size());
-        B.add_term(T, kPanel, OP_N, bt.off_mp, kPanel, OP_N, bt.off_rs, bt.m, +1);
-        B.gemm_task(bt.m, bt.m, bt.off, bt.m, MODE_ADD, 0, 0, tb);
-      }
-      B.close();
-    }
-    B.open(K_PERM, 0, l);
-    for (const BigTask& bt : big) P.big_tasks.push_back(bt);
-    B.close();
+    std::vector<InvItem> items;
+    for (int x : xs) items.push_back(InvItem{B.msz(x), x, fold_pos[x], B.I(x).off_d});
+    B.emit_inverses(l, 0, items, P.big_scratch);
   };
   auto gather_schur = [&](int l) {
     B.open(K_GEMM, 0, l);
@@ -845,6 +860,87 @@ Plan build_plan(ProblemDesc desc) {
     }
   }
   return P;
+}
+
+LeadPlan build_lead_plan(int w) {
+  if (w <= 0 || w > kBigMax) fail(kContractViolation, "lead: block size out of range");
+  LeadPlan L;
+  L.w = w;
+  Plan& P = L.P;
+  const int64_t w2 = align8(int64_t(w) * w);
+  for (int b = 0; b < LB_COUNT; ++b) L.off[b] = b * w2;
+  P.big_scratch = LB_COUNT * w2;
+  // scratch for two simultaneous big inverses (g and m)
+  const int64_t per = w > kSmemInvMax ? align8(int64_t(w) * kPanel) * 2 + align8((w + 3) / 4) + 8 : 0;
+  P.arena = P.big_scratch + 2 * per;
+  Builder B(P);
+  auto& T = P.gemm_terms;
+  auto mark = [&](int* r, auto&& body) {
+    r[0] = static_cast<int>(P.ops.size());
+    body();
+    r[1] = static_cast<int>(P.ops.size());
+  };
+  auto prod = [&](int c, int a, int b2, int mode, int sign, int init = -1) {
+    const int tb = static_cast<int>(T.size());
+    B.add_term(T, w, OP_N, L.off[a], w, OP_N, L.off[b2], w, sign);
+    B.gemm_task(w, w, L.off[c], w, mode, init >= 0 ? L.off[init] : 0, w, tb);
+  };
+  mark(L.inv_gm, [&] {
+    B.emit_inverses(0, 10, {InvItem{w, 0, 0, L.off[LB_G]}, InvItem{w, 0, 1, L.off[LB_M]}}, P.big_scratch);
+  });
+  for (int par = 0; par < 2; ++par) {
+    mark(L.gemm_a[par], [&] {
+      B.open(K_GEMM, 10, 0);
+      prod(LB_T1, LB_H01CT, LB_G, MODE_SET, +1);
+      prod(LB_AM, par ? LB_ALPHA1 : LB_ALPHA0, LB_M, MODE_SET, +1);
+      prod(LB_BM, par ? LB_BETA1 : LB_BETA0, LB_M, MODE_SET, +1);
+      B.close();
+    });
+  }
+  for (int par = 0; par < 2; ++par) {
+    mark(L.gemm_a2[par], [&] {
+      B.open(K_GEMM, 10, 0);
+      prod(LB_AM, par ? LB_ALPHA1 : LB_ALPHA0, LB_M, MODE_SET, +1);
+      prod(LB_BM, par ? LB_BETA1 : LB_BETA0, LB_M, MODE_SET, +1);
+      B.close();
+    });
+  }
+  mark(L.gemm_b, [&] {
+    B.open(K_GEMM, 10, 0);
+    prod(LB_RHS, LB_T1, LB_H01, MODE_INIT, -1, LB_ZH);
+    B.close();
+  });
+  mark(L.inv_rhs, [&] { B.emit_inverses(0, 10, {InvItem{w, 0, 2, L.off[LB_RHS]}}, P.big_scratch); });
+  mark(L.inv_m, [&] { B.emit_inverses(0, 10, {InvItem{w, 0, 1, L.off[LB_M]}}, P.big_scratch); });
+  mark(L.inv_fin, [&] { B.emit_inverses(0, 10, {InvItem{w, 0, 3, L.off[LB_FIN]}}, P.big_scratch); });
+  for (int par = 0; par < 2; ++par) {
+    const int al = par ? LB_ALPHA1 : LB_ALPHA0, be = par ? LB_BETA1 : LB_BETA0;
+    const int al2 = par ? LB_ALPHA0 : LB_ALPHA1, be2 = par ? LB_BETA0 : LB_BETA1;
+    mark(L.gemm_c[par], [&] {
+      B.open(K_GEMM, 10, 0);
+      prod(LB_ES, LB_AM, be, MODE_ADD, +1);
+      {
+        const int tb = static_cast<int>(T.size());
+        B.add_term(T, w, OP_N, L.off[LB_AM], w, OP_N, L.off[be], w, +1);
+        B.add_term(T, w, OP_N, L.off[LB_BM], w, OP_N, L.off[al], w, +1);
+        B.gemm_task(w, w, L.off[LB_E], w, MODE_ADD, 0, 0, tb);
+      }
+      prod(al2, LB_AM, al, MODE_SET, +1);
+      prod(be2, LB_BM, be, MODE_SET, +1);
+      B.close();
+    });
+  }
+  mark(L.fin1, [&] {
+    B.open(K_GEMM, 10, 0);
+    prod(LB_T1, LB_H01CT, LB_FIN, MODE_SET, +1);
+    B.close();
+  });
+  mark(L.fin2, [&] {
+    B.open(K_GEMM, 10, 0);
+    prod(LB_SIG, LB_T1, LB_H01, MODE_SET, +1);
+    B.close();
+  });
+  return L;
 }
 
 }  // namespace negfb

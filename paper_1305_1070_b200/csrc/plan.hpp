@@ -217,4 +217,33 @@ constexpr int kArrTN[3] = {32, 64, 16};
 
 Plan build_plan(ProblemDesc desc);
 
+// Batched energy-doubling decimation of one dense lead, the restatement of
+// surface_self_energy (device.cpp:195-251) as a grouped-kernel program over
+// per-energy arenas.  Arena blocks (w x w, row-major):
+enum LeadBlock : int {
+  LB_H00 = 0, LB_H01, LB_H01CT, LB_ZH,  // constants per energy (ZH = zI - h00)
+  LB_ES, LB_E, LB_ALPHA0, LB_ALPHA1, LB_BETA0, LB_BETA1,
+  LB_G, LB_M, LB_AM, LB_BM, LB_T1, LB_RHS, LB_FIN, LB_SIG,
+  LB_COUNT
+};
+struct LeadPlan {
+  Plan P;          // arena size + task arrays (P.ops holds every op below)
+  int w = 0;
+  int64_t off[LB_COUNT] = {};
+  // op index ranges [begin, end) in P.ops
+  int inv_gm[2] = {0, 0};      // g = (z - es)^-1, m = (z - e)^-1 (device.cpp:218, 235)
+  int gemm_a[2][2] = {};       // per parity: T1 = h01^H g; AM = alpha m; BM = beta m
+  int gemm_b[2] = {0, 0};      // rhs = (z - h00) - T1 h01 (device.cpp:220-221)
+  int inv_rhs[2] = {0, 0};     // refined = rhs^-1 (device.cpp:222)
+  int gemm_c[2][2] = {};       // per parity: es += ab; e += ab + ba; alpha', beta' (236-243)
+  int fin1[2] = {0, 0};        // T1 = h01^H refined
+  int fin2[2] = {0, 0};        // sigma = T1 h01 (device.cpp:226-227)
+  // decay-criterion variant (devices.sancho_rubio): m only per sweep, and
+  // the frozen surface block inverted once at the end (into FIN)
+  int inv_m[2] = {0, 0};
+  int gemm_a2[2][2] = {};      // per parity: AM = alpha m; BM = beta m
+  int inv_fin[2] = {0, 0};
+};
+LeadPlan build_lead_plan(int w);
+
 }  // namespace negfb

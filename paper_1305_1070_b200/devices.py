@@ -68,6 +68,7 @@ class Workload:
     nx: int
     ny: int
     description: str = ""
+    contacts: dict | None = None  # GPU self-energy recipe (GpuSelfEnergies)
 
     @property
     def n(self) -> int:
@@ -157,7 +158,12 @@ def effective_mass_device(name: str, nx: int, ny: int, a_nm: float, m_eff: float
                 sl[q, 2 * w2:] = -fermi(e, mu_ph, kT) * (s - np.conj(s))
         return sr, sl
 
-    return Workload(name, prob, energies, trapezoid_weights(energies), self_energies, nx, ny, description)
+    contacts = dict(kind="modes", w=ny, t=t, eta=eta, kT=kT,
+                    leads=[dict(sr_off=0, sl_off=0, mu=mu_l), dict(sr_off=w2, sl_off=w2, mu=mu_r)],
+                    phonon=None if gam is None else dict(gamma=gam, sr_off=2 * w2, sl_off=2 * w2, mu=mu_ph),
+                    sr_const=None if not complex_energy else (n_lesser, np.full(n, -1j * eta)))
+    return Workload(name, prob, energies, trapezoid_weights(energies), self_energies, nx, ny, description,
+                    contacts)
 
 
 def config1() -> Workload:
@@ -306,8 +312,89 @@ def config3(n_energies: int = 512, n_cells: int = 600, complex_energy: bool = Fa
             sl[q, w2:] = (-fermi(e, mu_r, kT) * (sig_r - sig_r.conj().T)).ravel()
         return sr, sl
 
+    contacts = dict(kind="sancho", w=cell, eta=eta, kT=kT, tol=1e-12, h00=h00,
+                    leads=[dict(h01=h01.T.copy(), sr_off=0, sl_off=0, mu=mu_l),
+                           dict(h01=h01, sr_off=w2, sl_off=w2, mu=mu_r)],
+                    phonon=None,
+                    sr_const=None if not complex_energy else (2 * w2, np.full(n, -1j * eta)))
     return Workload("cfg3_cnt_20_0_600", prob, energies, trapezoid_weights(energies), self_energies,
-                    n_cells * 4, k_around, "zigzag (20,0) CNT, 600 cells, onsite U[-0.05,0.05] seed 2")
+                    n_cells * 4, k_around, "zigzag (20,0) CNT, 600 cells, onsite U[-0.05,0.05] seed 2", contacts)
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
+
+
+# ---------------------------------------------------------------------------
+# Self-energies on the GPU
+# ---------------------------------------------------------------------------
+class GpuSelfEnergies:
+    """Builds a workload's Sigma^r / Sigma^< pattern values for device-resident
+    energies on the GPU: the analytic mode sum (effective-mass leads) or the
+    batched Sancho-Rubio decimation (config 3's tube), then the lesser
+    self-energies and the phonon diagonal (lesser_self_energy,
+    device.cpp:322-366) -- the device-side replacement of the per-energy host
+    ``Workload.self_energies``.  Returns torch tensors laid out like the host
+    arrays (rows = energies), ready for ``HscGpuSolver.solve_device``."""
+
+    def __init__(self, workload: Workload, device: int = 0, max_energy_batch: int = 0):
+        import torch
+
+        from . import negf as _negf
+
+        c = workload.contacts
+        if c is None:
+            raise ValueError(f"workload {workload.name} has no GPU self-energy recipe")
+        self.c = c
+        self.dev = torch.device("cuda", device)
+        self.n_sr = len(workload.problem.sr_rows)
+        self.n_sl = len(workload.problem.sl_rows)
+        self.leads = []
+        if c["kind"] == "sancho":
+            for ld in c["leads"]:
+                self.leads.append(_negf.SurfaceLead(c["h00"], ld["h01"], c["eta"], device=device,
+                                                    max_energy_batch=max_energy_batch, criterion="decay",
+                                                    tol=c["tol"]))
+        ph = c.get("phonon")
+        self.gamma = None if ph is None else torch.from_numpy(np.ascontiguousarray(ph["gamma"], np.float64)).to(
+            self.dev)
+        self.sr_const = None
+        if c.get("sr_const") is not None:
+            off, vals = c["sr_const"]
+            self.sr_const = (off, torch.from_numpy(np.ascontiguousarray(vals)).to(self.dev))
+
+    def __call__(self, energies, sigma_r=None, sigma_lesser=None):
+        import torch
+
+        from . import negf as _negf
+
+        c = self.c
+        ne = int(energies.numel())
+        w = c["w"]
+        if sigma_r is None:
+            sigma_r = torch.zeros((ne, self.n_sr), dtype=torch.complex128, device=self.dev)
+        if sigma_lesser is None:
+            sigma_lesser = torch.zeros((ne, self.n_sl), dtype=torch.complex128, device=self.dev)
+        stream = torch.cuda.current_stream(self.dev).cuda_stream
+        blocks = []
+        if c["kind"] == "modes":  # one uniform lead, the same block on both sides
+            sig = torch.empty((ne, w, w), dtype=torch.complex128, device=self.dev)
+            _negf.lead_modes_sigma_device(w, c["t"], c["eta"], energies, sig, stream=stream)
+            blocks = [sig for _ in c["leads"]]
+        else:
+            torch.cuda.current_stream(self.dev).synchronize()
+            for lead in self.leads:
+                sig = torch.empty((ne, w, w), dtype=torch.complex128, device=self.dev)
+                lead.sigma_device(energies, sig)
+                blocks.append(sig)
+        if self.sr_const is not None:
+            off, vals = self.sr_const
+            sigma_r[:, off:off + vals.numel()] = vals
+        descs = [dict(w=w, sigma=b, sr_off=ld["sr_off"], sl_off=ld["sl_off"], mu=ld["mu"])
+                 for b, ld in zip(blocks, c["leads"])]
+        ph = c.get("phonon")
+        _negf.contacts_fill_device(energies, c["kT"], descs, sigma_r, sigma_lesser,
+                                   phonon_gamma=self.gamma,
+                                   ph_sr_off=-1 if ph is None else ph["sr_off"],
+                                   ph_sl_off=-1 if ph is None else ph["sl_off"],
+                                   mu_phonon=0.0 if ph is None else ph["mu"], stream=stream)
+        return sigma_r, sigma_lesser

@@ -77,6 +77,15 @@ class ResidualTooLarge(NegfError):
         return (ResidualTooLarge, (str(self), self.energy_index, self.dof))
 
 
+class ConvergenceError(NegfError):
+    def __init__(self, msg: str, energy_index: int = -1):
+        super().__init__(msg)
+        self.energy_index = energy_index
+
+    def __reduce__(self):
+        return (ConvergenceError, (str(self), self.energy_index))
+
+
 class CudaError(NegfError):
     pass
 
@@ -181,6 +190,16 @@ def _load() -> C.CDLL:
         "negf_gpu_set_residual_check": ([vp, i32], i32),
         "negf_gpu_max_real_residual": ([vp], C.c_double),
         "negf_gpu_profile_read": ([vp, vp, i32], i32),
+        "negf_lead_create": ([i32, i32, vp, vp, C.c_double, i32, C.c_double, i32, C.POINTER(vp), st], i32),
+        "negf_lead_sigma": ([vp, i32, vp, i32, vp, st], i32),
+        "negf_lead_sigma_device": ([vp, i32, vp, i32, vp, i64, st], i32),
+        "negf_lead_last_sweeps": ([vp, vp], i32),
+        "negf_lead_last_launches": ([vp], i64),
+        "negf_lead_stream": ([vp], vp),
+        "negf_lead_destroy": ([vp], None),
+        "negf_lead_modes_sigma_device": ([i32, C.c_double, C.c_double, i32, vp, vp, i64, vp, st], i32),
+        "negf_contacts_fill_device": ([i32, vp, C.c_double, i32, vp, i32, vp, i64, i64, C.c_double, vp, i64, vp,
+                                       i64, vp, st], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -196,7 +215,9 @@ ABI_SYMBOLS = (
     "negf_gpu_check negf_gpu_density negf_gpu_stream negf_gpu_density_device "
     "negf_gpu_last_launches negf_gpu_destroy negf_nccl_unique_id negf_gpu_nccl_init "
     "negf_gpu_allreduce_density negf_gpu_profile negf_gpu_profile_read negf_gpu_set_residual_check "
-    "negf_gpu_max_real_residual"
+    "negf_gpu_max_real_residual negf_lead_create negf_lead_sigma negf_lead_sigma_device negf_lead_last_sweeps "
+    "negf_lead_last_launches negf_lead_stream negf_lead_destroy negf_lead_modes_sigma_device "
+    "negf_contacts_fill_device"
 ).split()
 
 KSTAT_NAMES = ("gemm", "inverse", "diag", "scale", "assemble", "output")
@@ -226,6 +247,8 @@ def _raise(st: _Status) -> None:
         raise PartitionViolation(msg)
     if code == 9:
         raise ResidualTooLarge(msg, st.energy_index, st.dof)
+    if code == 11:
+        raise ConvergenceError(msg, st.energy_index)
     if code == 4:
         raise CudaError(msg)
     raise NegfError(msg)
@@ -560,3 +583,114 @@ def trapezoid_weights(energies) -> np.ndarray:
     w[1:-1] = 0.5 * (e[2:] - e[:-2])
     w[-1] = 0.5 * (e[-1] - e[-2])
     return w
+
+
+# ---------------------------------------------------------------------------
+# contact self-energies on the GPU (include/negf_gpu.h)
+# ---------------------------------------------------------------------------
+class _ContactDesc(C.Structure):
+    _fields_ = [
+        ("w", C.c_int),
+        ("d_sigma", C.c_void_p),
+        ("ld", C.c_int64),
+        ("sr_off", C.c_int64),
+        ("sl_off", C.c_int64),
+        ("mu_ev", C.c_double),
+    ]
+
+
+class SurfaceLead:
+    """surface_self_energy (device.cpp:195-251) on the GPU, batched over
+    energies: one dense semi-infinite lead with onsite block ``h00`` and the
+    coupling ``h01`` from a lead cell to the next one away from the device
+    (attach_contacts, device.cpp:284-303, builds these from the device's
+    boundary layers).  ``criterion="decay"`` switches to the Sancho-Rubio
+    convention of ``devices.sancho_rubio`` (config 3's lead)."""
+
+    CRITERIA = {"fixed-point": 0, "decay": 1}
+
+    def __init__(self, h00: np.ndarray, h01: np.ndarray, eta: float, device: int = 0,
+                 max_energy_batch: int = 0, criterion: str = "fixed-point", tol: float = 1e-12):
+        h00 = np.ascontiguousarray(h00, np.complex128)
+        h01 = np.ascontiguousarray(h01, np.complex128)
+        w = h00.shape[0]
+        if h00.shape != (w, w):
+            raise ContractViolation("surface_self_energy: h00 must be square")
+        if h01.shape != (w, w):
+            raise ContractViolation("surface_self_energy: h01 must match h00's shape")
+        self.w = w
+        self._h = C.c_void_p()
+        st = _Status()
+        if criterion not in self.CRITERIA:
+            raise ContractViolation(f"unknown lead criterion {criterion!r}")
+        _lib.negf_lead_create(int(device), w, _ptr(h00), _ptr(h01), float(eta), self.CRITERIA[criterion],
+                              float(tol), int(max_energy_batch), C.byref(self._h), C.byref(st))
+        _raise(st)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.negf_lead_destroy(self._h)
+            self._h = None
+
+    def sigma(self, energies, first_energy_index: int = 0) -> np.ndarray:
+        """Host energies -> Sigma^r blocks (nE, w, w)."""
+        e = np.ascontiguousarray(np.atleast_1d(energies), np.float64)
+        out = np.empty((len(e), self.w, self.w), np.complex128)
+        st = _Status()
+        _lib.negf_lead_sigma(self._h, len(e), _ptr(e), int(first_energy_index), _ptr(out), C.byref(st))
+        _raise(st)
+        return out
+
+    def sigma_device(self, energies, out, ld: int | None = None, first_energy_index: int = 0) -> None:
+        """torch CUDA tensors: energies (nE,) float64 -> out (complex128, energy k
+        at element k*ld)."""
+        ld = self.w * self.w if ld is None else int(ld)
+        st = _Status()
+        _lib.negf_lead_sigma_device(self._h, int(energies.numel()), energies.data_ptr(), int(first_energy_index),
+                                    out.data_ptr(), ld, C.byref(st))
+        _raise(st)
+
+    def last_sweeps(self, n: int) -> np.ndarray:
+        """Converging sweep index per energy of the last call."""
+        out = np.zeros(n, np.int32)
+        _lib.negf_lead_last_sweeps(self._h, _ptr(out))
+        return out
+
+    @property
+    def last_launches(self) -> int:
+        return int(_lib.negf_lead_last_launches(self._h))
+
+
+def lead_modes_sigma_device(w: int, t: float, eta: float, energies, out, ld: int | None = None,
+                            stream: int = 0) -> None:
+    """Analytic transverse-mode Sigma^r of a uniform hard-wall 2-D lead
+    (devices.analytic_lead_sigma) for torch CUDA energies -> out."""
+    ld = w * w if ld is None else int(ld)
+    st = _Status()
+    _lib.negf_lead_modes_sigma_device(int(w), float(t), float(eta), int(energies.numel()), energies.data_ptr(),
+                                      out.data_ptr(), ld, C.c_void_p(stream or None), C.byref(st))
+    _raise(st)
+
+
+def contacts_fill_device(energies, kT: float, contacts, sigma_r, sigma_lesser, phonon_gamma=None,
+                         ph_sr_off: int = -1, ph_sl_off: int = -1, mu_phonon: float = 0.0, stream: int = 0) -> None:
+    """lesser_self_energy (device.cpp:322-366) + pattern placement on the GPU.
+
+    ``contacts``: sequence of dicts {w, sigma (torch complex tensor), ld,
+    sr_off, sl_off, mu}; ``sigma_r``/``sigma_lesser``: (nE, nnz) complex128
+    torch tensors (rows = energies)."""
+    descs = (_ContactDesc * max(1, len(contacts)))()
+    for k, c in enumerate(contacts):
+        descs[k] = _ContactDesc(int(c["w"]), c["sigma"].data_ptr(), int(c.get("ld", c["w"] * c["w"])),
+                                int(c.get("sr_off", -1)), int(c.get("sl_off", -1)), float(c["mu"]))
+    n_ph = 0 if phonon_gamma is None else int(phonon_gamma.numel())
+    st = _Status()
+    _lib.negf_contacts_fill_device(int(energies.numel()), energies.data_ptr(), float(kT), len(contacts), descs, n_ph,
+                                   None if phonon_gamma is None else phonon_gamma.data_ptr(), int(ph_sr_off),
+                                   int(ph_sl_off), float(mu_phonon),
+                                   None if sigma_r is None else sigma_r.data_ptr(),
+                                   0 if sigma_r is None else int(sigma_r.shape[-1]),
+                                   None if sigma_lesser is None else sigma_lesser.data_ptr(),
+                                   0 if sigma_lesser is None else int(sigma_lesser.shape[-1]),
+                                   C.c_void_p(stream or None), C.byref(st))
+    _raise(st)

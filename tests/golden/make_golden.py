@@ -98,5 +98,43 @@ def main() -> None:
             shutil.copy(src, os.path.join(HERE, f"cli_{sub}_{fn}"))
 
 
+# Dense leads through the reference's surface_self_energy (device.cpp:195-251,
+# ref_driver lead): (name, h00/h01 builder, eta, energies).  cnt80 is the
+# config-3 (20,0) tube cell (E = 3.0 does not converge: ConvergenceError);
+# em100 the config-2 2-D effective-mass lead; em120 exceeds the 112-wide
+# shared-memory inverse (multi-CTA inverse path).
+def _em_lead(w: int, t: float):
+    import numpy as np
+    h00 = np.diag(np.full(w, 4.0 * t)) - t * (np.eye(w, k=1) + np.eye(w, k=-1))
+    return h00.astype(np.complex128), (-t * np.eye(w)).astype(np.complex128)
+
+
+def _cnt_lead():
+    import numpy as np
+    from paper_1305_1070_b200 import devices
+    h00, h01 = devices._cnt_cell(20, -2.7)
+    return h00.astype(np.complex128), h01.astype(np.complex128)
+
+
+T_EM = 0.0380998 / (0.067 * 0.5 * 0.5)
+LEADS = [
+    ("lead_cnt80", _cnt_lead, 1e-6, [-0.9, -0.3, 0.05, 0.4, 0.95, 3.0]),
+    ("lead_em100", lambda: _em_lead(100, T_EM), 1e-6, [0.0, 0.13, 0.4]),
+    ("lead_em120", lambda: _em_lead(120, T_EM), 1e-6, [0.05, 0.3]),
+]
+
+
+def make_leads() -> None:
+    for name, build, eta, energies in LEADS:
+        h00, h01 = build()
+        path = os.path.join(HERE, name + ".bin")
+        refio.write_lead(path, h00, h01, eta, energies)
+        refio.run_lead(path, os.path.join(HERE, name + ".out"))
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["leads"]:
+        make_leads()
+    else:
+        main()
+        make_leads()

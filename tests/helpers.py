@@ -13,7 +13,24 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def golden_names():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.bin")))
+    """Problem fixtures (NEGFPRB1); lead_*.bin are lead fixtures (NEGFLED1)."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.bin"))
+                  if not os.path.basename(p).startswith("lead_"))
+
+
+def lead_names():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "lead_*.bin")))
+
+
+def dense_block(rp, rows, cols) -> np.ndarray:
+    """dense_block (device.cpp:27-43) of the problem's H over dof lists."""
+    ri = {d: k for k, d in enumerate(rows)}
+    ci = {d: k for k, d in enumerate(cols)}
+    m = np.zeros((len(rows), len(cols)), np.complex128)
+    for r, c, v in zip(rp.h_rows, rp.h_cols, rp.h_vals):
+        if r in ri and c in ci:
+            m[ri[r], ci[c]] += v
+    return m
 
 
 def load_golden(name: str):
