@@ -258,6 +258,45 @@ int negf_contacts_fill_device(int n_energies, const double* d_energies, double k
                               int64_t sr_stride, double* d_sigma_lesser, int64_t sl_stride, void* stream,
                               negf_status* st);
 
+/* ---- Output path -----------------------------------
+ *
+ *   negf_format_double     format_double   proj/src/run.cpp:276-281
+ *                          (std::to_chars, general, 17 significant digits)
+ *   negf_write_solve_csv   cmd_solve's artefacts run.cpp:284-326:
+ *                          density.csv, ldos.csv (ldos observables.cpp:50-55),
+ *                          line_density.csv (line_density_y
+ *                          observables.cpp:96-110); dof j = y*nx + x
+ *   negf_shard_writer_*    (new) binary per-shard diag G^r / G^< writer,
+ *                          replacing ldos.csv's per-energy x dof text for
+ *                          large runs
+ */
+/* Writes v into buf (NUL-terminated); returns its length or -1. */
+int negf_format_double(double v, char* buf, int len);
+/* density[nx*ny] already scaled (density_scale, run.cpp:55-56); gr_diag
+ * (nE x nx*ny complex) or NULL to skip ldos.csv.  Creates out_dir. */
+int negf_write_solve_csv(const char* out_dir, int nx, int ny, int n_energies, const double* energies,
+                         const double* density, const double* gr_diag, negf_status* st);
+
+/* Shard file: 64-byte header "NEGFSHD1", int32 version, n_dofs, rank, world,
+ * what (1 = G^r, 2 = G^<, 3 = both), int32 0, int64 record count; then one
+ * record per energy: int32 energy_index, int32 0, f64 energy, [n c128 diag
+ * G^r], [n c128 diag G^<].  Records are written by a background thread in
+ * append order. */
+typedef struct negf_shard_writer negf_shard_writer;
+int negf_shard_writer_open(const char* path, int n_dofs, int rank, int world, int what,
+                           negf_shard_writer** out, negf_status* st);
+/* Host diagonals (nE x n complex each; the array `what` excludes may be NULL). */
+int negf_shard_writer_append(negf_shard_writer* w, int n_energies, int first_energy_index,
+                             const double* energies, const double* gr, const double* gless, negf_status* st);
+/* Device diagonals: one strided D2H copy per array on `stream` into pinned
+ * staging (two slots, reused when written), file write off the caller's
+ * thread.  The device buffers may be reused once the stream passes. */
+int negf_shard_writer_append_device(negf_shard_writer* w, int n_energies, int first_energy_index,
+                                    const double* energies, const double* d_gr, const double* d_gless,
+                                    void* stream, negf_status* st);
+/* Drains the queue, patches the record count, closes the file. */
+int negf_shard_writer_close(negf_shard_writer* w, negf_status* st);
+
 #ifdef __cplusplus
 }
 #endif

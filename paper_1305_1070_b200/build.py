@@ -12,7 +12,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnegf_b200.so")
 OBJDIR = os.path.join(ROOT, "build", "negf_b200")
-SOURCES = ["tree.cpp", "plan.cpp", "kernels.cu", "capi.cu", "lead.cu"]
+SOURCES = ["tree.cpp", "plan.cpp", "kernels.cu", "capi.cu", "lead.cu", "output.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", f"-I{os.path.join(ROOT, 'include')}"]

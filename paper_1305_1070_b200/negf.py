@@ -200,6 +200,12 @@ def _load() -> C.CDLL:
         "negf_lead_modes_sigma_device": ([i32, C.c_double, C.c_double, i32, vp, vp, i64, vp, st], i32),
         "negf_contacts_fill_device": ([i32, vp, C.c_double, i32, vp, i32, vp, i64, i64, C.c_double, vp, i64, vp,
                                        i64, vp, st], i32),
+        "negf_format_double": ([C.c_double, C.c_char_p, i32], i32),
+        "negf_write_solve_csv": ([C.c_char_p, i32, i32, i32, vp, vp, vp, st], i32),
+        "negf_shard_writer_open": ([C.c_char_p, i32, i32, i32, i32, C.POINTER(vp), st], i32),
+        "negf_shard_writer_append": ([vp, i32, i32, vp, vp, vp, st], i32),
+        "negf_shard_writer_append_device": ([vp, i32, i32, vp, vp, vp, vp, st], i32),
+        "negf_shard_writer_close": ([vp, st], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -217,7 +223,8 @@ ABI_SYMBOLS = (
     "negf_gpu_allreduce_density negf_gpu_profile negf_gpu_profile_read negf_gpu_set_residual_check "
     "negf_gpu_max_real_residual negf_lead_create negf_lead_sigma negf_lead_sigma_device negf_lead_last_sweeps "
     "negf_lead_last_launches negf_lead_stream negf_lead_destroy negf_lead_modes_sigma_device "
-    "negf_contacts_fill_device"
+    "negf_contacts_fill_device negf_format_double negf_write_solve_csv negf_shard_writer_open "
+    "negf_shard_writer_append negf_shard_writer_append_device negf_shard_writer_close"
 ).split()
 
 KSTAT_NAMES = ("gemm", "inverse", "diag", "scale", "assemble", "output")
@@ -694,3 +701,102 @@ def contacts_fill_device(energies, kT: float, contacts, sigma_r, sigma_lesser, p
                                    0 if sigma_lesser is None else int(sigma_lesser.shape[-1]),
                                    C.c_void_p(stream or None), C.byref(st))
     _raise(st)
+
+
+# ---------------------------------------------------------------------------
+# output path (include/negf_gpu.h)
+# ---------------------------------------------------------------------------
+def format_double(v: float) -> str:
+    """format_double (run.cpp:276-281): general format, 17 significant digits."""
+    buf = C.create_string_buffer(64)
+    n = _lib.negf_format_double(float(v), buf, 64)
+    return buf.value[:n].decode()
+
+
+def write_solve_csv(out_dir: str, nx: int, ny: int, energies, density, gr_diag=None) -> None:
+    """cmd_solve's density.csv / ldos.csv / line_density.csv (run.cpp:284-326);
+    ``density`` already scaled (density_scale), dof j = y*nx + x."""
+    e = np.ascontiguousarray(energies, np.float64)
+    d = np.ascontiguousarray(density, np.float64)
+    g = None if gr_diag is None else np.ascontiguousarray(gr_diag, np.complex128)
+    st = _Status()
+    _lib.negf_write_solve_csv(out_dir.encode(), int(nx), int(ny), len(e), _ptr(e), _ptr(d), _ptr(g), C.byref(st))
+    _raise(st)
+
+
+class ShardWriter:
+    """Binary per-shard writer of per-energy diag G^r / G^< (negf_shard_writer_*)."""
+
+    def __init__(self, path: str, n_dofs: int, rank: int = 0, world: int = 1, gr: bool = True, gless: bool = True):
+        self.n = n_dofs
+        self.what = (1 if gr else 0) | (2 if gless else 0)
+        self._h = C.c_void_p()
+        st = _Status()
+        _lib.negf_shard_writer_open(path.encode(), int(n_dofs), int(rank), int(world), self.what,
+                                    C.byref(self._h), C.byref(st))
+        _raise(st)
+
+    def append(self, energies, first_energy_index: int, gr=None, gless=None) -> None:
+        e = np.ascontiguousarray(energies, np.float64)
+        g1 = None if gr is None else np.ascontiguousarray(gr, np.complex128)
+        g2 = None if gless is None else np.ascontiguousarray(gless, np.complex128)
+        st = _Status()
+        _lib.negf_shard_writer_append(self._h, len(e), int(first_energy_index), _ptr(e), _ptr(g1), _ptr(g2),
+                                      C.byref(st))
+        _raise(st)
+
+    def append_device(self, energies, first_energy_index: int, gr=None, gless=None, stream: int = 0) -> None:
+        """``gr``/``gless``: torch CUDA complex128 tensors (nE, n); host energies."""
+        e = np.ascontiguousarray(energies, np.float64)
+        st = _Status()
+        _lib.negf_shard_writer_append_device(self._h, len(e), int(first_energy_index), _ptr(e),
+                                             None if gr is None else gr.data_ptr(),
+                                             None if gless is None else gless.data_ptr(),
+                                             C.c_void_p(stream or None), C.byref(st))
+        _raise(st)
+
+    def close(self) -> None:
+        if self._h:
+            st = _Status()
+            _lib.negf_shard_writer_close(self._h, C.byref(st))
+            self._h = None
+            _raise(st)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            try:
+                self.close()
+            except NegfError:
+                pass
+
+
+def read_shard(path: str) -> dict:
+    """Reads a NEGFSHD1 shard: energy_index[k], energy[k], gr[k, n], gless[k, n]."""
+    import struct
+
+    with open(path, "rb") as f:
+        buf = f.read()
+    if buf[:8] != b"NEGFSHD1":
+        raise ContractViolation(f"{path}: not a shard file")
+    ver, n, rank, world, what, _ = struct.unpack_from("<6i", buf, 8)
+    (count,) = struct.unpack_from("<q", buf, 32)
+    rec = 16 + (16 * n if what & 1 else 0) + (16 * n if what & 2 else 0)
+    if len(buf) != 64 + rec * count:
+        raise ContractViolation(f"{path}: truncated shard ({len(buf)} bytes for {count} records)")
+    raw = np.frombuffer(buf, np.uint8, rec * count, 64).reshape(count, rec)
+    out = {"n_dofs": n, "rank": rank, "world": world,
+           "energy_index": raw[:, :4].copy().view(np.int32).ravel(),
+           "energies": raw[:, 8:16].copy().view(np.float64).ravel()}
+    at = 16
+    if what & 1:
+        out["gr"] = raw[:, at:at + 16 * n].copy().view(np.complex128)
+        at += 16 * n
+    if what & 2:
+        out["gless"] = raw[:, at:at + 16 * n].copy().view(np.complex128)
+    return out
