@@ -119,6 +119,18 @@ int negf_plan_gemm_tasks(const negf_plan* p, int32_t* m, int32_t* n, int64_t* k_
                          int32_t* level);
 void negf_plan_destroy(negf_plan* p);
 
+/* Layered RGF plan: rgf_gr + rgf_gless
+ * (proj/src/rgf.cpp:181-380) on layered_from_coo's layer map
+ * (rgf.cpp:69-150; n_layers lists of dofs, layer_ptr[n_layers+1]) of the same
+ * problem, as a plan the negf_gpu_* device calls solve exactly like an HSC
+ * plan (diag G^r, diag G^<, density).  Every coupling is handled as a dense
+ * block.  Errors: NEGF_CONTRACT_VIOLATION for a layer map that is not a
+ * disjoint cover, a non-transposed lower coupling or a Sigma^< that is not
+ * layer-block-diagonal; NEGF_PARTITION_VIOLATION for entries coupling
+ * non-adjacent layers.  negf_plan_tree / negf_plan_fill do not apply. */
+int negf_rgf_plan_create(const negf_problem* p, int n_layers, const int32_t* layer_ptr,
+                         const int32_t* layer_dofs, negf_plan** out, negf_status* st);
+
 /* Device side: allocates the per-energy arenas for up to max_energy_batch
  * energies (0 = as many as fit in 85% of free HBM) on `device`. */
 int negf_gpu_create(const negf_plan* plan, int device, int max_energy_batch, negf_gpu** out,

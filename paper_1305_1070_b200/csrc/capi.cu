@@ -90,6 +90,8 @@ struct negf_gpu {
   ScaleTask* d_scale = nullptr;
   InvTask* d_inv = nullptr;
   BigTask* d_big = nullptr;
+  SkewTask* d_skew_tasks = nullptr;
+  CombineTask* d_comb_tasks = nullptr;
   // per-batch staging
   double *d_energies = nullptr, *d_weights = nullptr;
   double2 *d_sigma_r = nullptr, *d_sigma_l = nullptr, *d_gr = nullptr, *d_gl = nullptr;
@@ -189,8 +191,9 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
                       g->d_sl_ptr, g->d_sl_src, g->d_sl_partner, static_cast<int>(P.seeded_ids.size()), g->d_seeded,
                       g->d_skew, g->d_status, s, L);
   }
-  static const int kind_stat[6] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
-                                   NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE};
+  static const int kind_stat[8] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
+                                   NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE,
+                                   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE};
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
     const Op& op = P.ops[oi];
     Bracket br(g, kind_stat[op.kind], op.cmul * nE, static_cast<int>(oi));
@@ -209,6 +212,12 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         break;
       case K_PERM:
         launch_bigperm(b, g->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, s, L);
+        break;
+      case K_SKEW:
+        launch_skew(b, g->d_skew_tasks, P.skew_tasks.data(), op.begin, op.count, s, L);
+        break;
+      case K_COMBINE:
+        launch_combine(b, g->d_comb_tasks, P.comb_tasks.data(), op.begin, op.count, s, L);
         break;
       default:
         launch_scale(b, g->d_scale, op.begin, op.count, s, L);
@@ -240,6 +249,14 @@ int collect(negf_gpu* g, negf_status* st) {
   if (es >= 0 && (en < 0 || es <= en)) {
     const int fold_pos = static_cast<int>((h.singular_key >> 20) & 0xFFFFF);
     const int pivot = static_cast<int>(h.singular_key & 0xFFFFF);
+    if (!g->plan->rgf_layers.empty()) {  // RGF: fold_pos is the layer
+      const int sz = static_cast<int>(g->plan->rgf_layers[static_cast<size_t>(fold_pos)].size());
+      return set_status(st, NEGF_SINGULAR_BLOCK,
+                        "energy point " + std::to_string(es) + ": inverse: singular pivot " + std::to_string(pivot) +
+                            " in " + std::to_string(sz) + "x" + std::to_string(sz) + " block of layer " +
+                            std::to_string(fold_pos),
+                        static_cast<int>(es), fold_pos, pivot);
+    }
     const Tree& t = g->plan->tree;
     const int cluster = fold_pos < static_cast<int>(t.fold_order().size()) ? t.fold_order()[fold_pos] : t.root();
     return set_status(st, NEGF_SINGULAR_BLOCK,
@@ -271,38 +288,65 @@ int collect(negf_gpu* g, negf_status* st) {
 
 extern "C" {
 
+}  // extern "C"
+
+namespace {
+
+ProblemDesc desc_from_c(const negf_problem* p) {
+  ProblemDesc d;
+  d.n = p->n_dofs;
+  d.h_rows.assign(p->h_rows, p->h_rows + p->h_nnz);
+  d.h_cols.assign(p->h_cols, p->h_cols + p->h_nnz);
+  d.h_vals.resize(static_cast<size_t>(p->h_nnz));
+  for (int64_t k = 0; k < p->h_nnz; ++k) d.h_vals[k] = cplx(p->h_vals[2 * k], p->h_vals[2 * k + 1]);
+  if (p->sr_nnz) {
+    d.sr_rows.assign(p->sr_rows, p->sr_rows + p->sr_nnz);
+    d.sr_cols.assign(p->sr_cols, p->sr_cols + p->sr_nnz);
+  }
+  if (p->sl_nnz) {
+    d.sl_rows.assign(p->sl_rows, p->sl_rows + p->sl_nnz);
+    d.sl_cols.assign(p->sl_cols, p->sl_cols + p->sl_nnz);
+  }
+  if (p->coords) {
+    d.coords.resize(static_cast<size_t>(p->n_dofs));
+    for (int i = 0; i < p->n_dofs; ++i) d.coords[i] = {p->coords[2 * i], p->coords[2 * i + 1]};
+  }
+  for (int gi = 0; gi < p->n_groups; ++gi)
+    d.atomic_groups.emplace_back(p->group_dofs + p->group_ptr[gi], p->group_dofs + p->group_ptr[gi + 1]);
+  d.max_leaf = p->max_leaf;
+  if (p->n_tree_clusters > 0) {
+    d.explicit_tree = true;
+    d.tree_parent.assign(p->tree_parent, p->tree_parent + p->n_tree_clusters);
+    for (int c = 0; c < p->n_tree_clusters; ++c)
+      d.tree_dofs.emplace_back(p->tree_dofs + p->tree_ptr[c], p->tree_dofs + p->tree_ptr[c + 1]);
+  }
+  return d;
+}
+
+}  // namespace
+
+extern "C" {
+
 int negf_plan_create(const negf_problem* p, negf_plan** out, negf_status* st) {
   if (!p || !out) return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
   try {
-    ProblemDesc d;
-    d.n = p->n_dofs;
-    d.h_rows.assign(p->h_rows, p->h_rows + p->h_nnz);
-    d.h_cols.assign(p->h_cols, p->h_cols + p->h_nnz);
-    d.h_vals.resize(static_cast<size_t>(p->h_nnz));
-    for (int64_t k = 0; k < p->h_nnz; ++k) d.h_vals[k] = cplx(p->h_vals[2 * k], p->h_vals[2 * k + 1]);
-    if (p->sr_nnz) {
-      d.sr_rows.assign(p->sr_rows, p->sr_rows + p->sr_nnz);
-      d.sr_cols.assign(p->sr_cols, p->sr_cols + p->sr_nnz);
-    }
-    if (p->sl_nnz) {
-      d.sl_rows.assign(p->sl_rows, p->sl_rows + p->sl_nnz);
-      d.sl_cols.assign(p->sl_cols, p->sl_cols + p->sl_nnz);
-    }
-    if (p->coords) {
-      d.coords.resize(static_cast<size_t>(p->n_dofs));
-      for (int i = 0; i < p->n_dofs; ++i) d.coords[i] = {p->coords[2 * i], p->coords[2 * i + 1]};
-    }
-    for (int gi = 0; gi < p->n_groups; ++gi)
-      d.atomic_groups.emplace_back(p->group_dofs + p->group_ptr[gi], p->group_dofs + p->group_ptr[gi + 1]);
-    d.max_leaf = p->max_leaf;
-    if (p->n_tree_clusters > 0) {
-      d.explicit_tree = true;
-      d.tree_parent.assign(p->tree_parent, p->tree_parent + p->n_tree_clusters);
-      for (int c = 0; c < p->n_tree_clusters; ++c)
-        d.tree_dofs.emplace_back(p->tree_dofs + p->tree_ptr[c], p->tree_dofs + p->tree_ptr[c + 1]);
-    }
-    auto* h = new negf_plan{build_plan(std::move(d))};
-    *out = h;
+    *out = new negf_plan{build_plan(desc_from_c(p))};
+    return ok(st);
+  } catch (const Failure& f) {
+    return set_status(st, f.code, f.what());
+  } catch (const std::exception& e) {
+    return set_status(st, NEGF_INTERNAL, e.what());
+  }
+}
+
+int negf_rgf_plan_create(const negf_problem* p, int n_layers, const int32_t* layer_ptr, const int32_t* layer_dofs,
+                         negf_plan** out, negf_status* st) {
+  if (!p || !out || n_layers < 0 || (n_layers > 0 && (!layer_ptr || !layer_dofs)))
+    return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
+  try {
+    std::vector<std::vector<int>> layers;
+    for (int l = 0; l < n_layers; ++l) layers.emplace_back(layer_dofs + layer_ptr[l], layer_dofs + layer_ptr[l + 1]);
+    *out = new negf_plan{build_rgf_plan(desc_from_c(p), std::move(layers))};
     return ok(st);
   } catch (const Failure& f) {
     return set_status(st, f.code, f.what());
@@ -315,9 +359,10 @@ int negf_plan_info_get(const negf_plan* h, negf_plan_info* info) {
   if (!h || !info) return NEGF_CONTRACT_VIOLATION;
   const Plan& P = h->plan;
   info->n_dofs = P.desc.n;
-  info->n_clusters = P.tree.num_clusters();
-  info->levels = P.tree.levels();
-  info->root = P.tree.root();
+  const bool rgf = !P.rgf_layers.empty();
+  info->n_clusters = rgf ? static_cast<int>(P.rgf_layers.size()) : P.tree.num_clusters();
+  info->levels = rgf ? 0 : P.tree.levels();
+  info->root = rgf ? -1 : P.tree.root();
   info->max_block = P.max_block;
   info->arena_bytes_per_energy = P.arena * 16;
   info->ref_fold_mul = P.ref_fold.multiply_ops;
@@ -335,6 +380,7 @@ int negf_plan_info_get(const negf_plan* h, negf_plan_info* info) {
 
 int negf_plan_tree(const negf_plan* h, int32_t* parent, int32_t* level, int32_t* dof_ptr, int32_t* dofs,
                    int32_t* fold_order) {
+  if (h && !h->plan.rgf_layers.empty()) return NEGF_CONTRACT_VIOLATION;
   if (!h) return NEGF_CONTRACT_VIOLATION;
   const Tree& t = h->plan.tree;
   int32_t off = 0;
@@ -352,6 +398,7 @@ int negf_plan_tree(const negf_plan* h, int32_t* parent, int32_t* level, int32_t*
 }
 
 int negf_plan_fill(const negf_plan* h, int32_t* ptr, int32_t* ids) {
+  if (h && !h->plan.rgf_layers.empty()) return NEGF_CONTRACT_VIOLATION;
   if (!h) return NEGF_CONTRACT_VIOLATION;
   int32_t off = 0;
   const auto& ci = h->plan.ci;
@@ -422,6 +469,8 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     g->d_scale = dev_upload(P.scale_tasks, o);
     g->d_inv = dev_upload(P.inv_tasks, o);
     g->d_big = dev_upload(P.big_tasks, o);
+    g->d_skew_tasks = dev_upload(P.skew_tasks, o);
+    g->d_comb_tasks = dev_upload(P.comb_tasks, o);
     const int n = P.desc.n;
     const size_t sr = P.desc.sr_rows.size(), sl = P.desc.sl_rows.size();
     const size_t per_energy = size_t(P.arena) * 16 + (sr + sl) * 16 + size_t(n) * 32 + 16 +

@@ -1303,6 +1303,60 @@ void launch_assemble(const BatchArgs& b, const Plan& p, const int64_t* d_h_pos, 
   }
 }
 
+// RGF elementwise steps.  skew_half (dense.cpp:136-170): upper triangle of
+// the product, the diagonal's imaginary part, lower = -conj(upper).
+__global__ void k_skew(double2* arena, int64_t stride, const SkewTask* __restrict__ tasks, int begin) {
+  const SkewTask tk = tasks[begin + blockIdx.x];
+  double2* a = arena + blockIdx.z * stride;
+  const int n = tk.n;
+  const int64_t nn = int64_t(n) * n;
+  for (int64_t idx = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; idx < nn; idx += int64_t(gridDim.y) * blockDim.x) {
+    const int i = static_cast<int>(idx / n), j = static_cast<int>(idx - int64_t(i) * n);
+    double2 v;
+    if (i < j) v = a[tk.src + idx];
+    else if (i == j) v = make_double2(0.0, a[tk.src + idx].y);
+    else {
+      const double2 u = a[tk.src + int64_t(j) * n + i];
+      v = make_double2(-u.x, u.y);
+    }
+    a[tk.dst + idx] = v;
+  }
+}
+
+// out = gl + term + x - x^H (rgf.cpp:373-377, in that order).
+__global__ void k_combine(double2* arena, int64_t stride, const CombineTask* __restrict__ tasks, int begin) {
+  const CombineTask tk = tasks[begin + blockIdx.x];
+  double2* a = arena + blockIdx.z * stride;
+  const int n = tk.n;
+  const int64_t nn = int64_t(n) * n;
+  for (int64_t idx = int64_t(blockIdx.y) * blockDim.x + threadIdx.x; idx < nn; idx += int64_t(gridDim.y) * blockDim.x) {
+    const int i = static_cast<int>(idx / n), j = static_cast<int>(idx - int64_t(i) * n);
+    const double2 g = a[tk.gl + idx], t = a[tk.term + idx], x = a[tk.x + idx];
+    const double2 xh = a[tk.x + int64_t(j) * n + i];  // (x^H)_ij = conj(x_ji)
+    double2 v = cadd(cadd(g, t), x);
+    v = make_double2(v.x - xh.x, v.y + xh.y);
+    a[tk.out + idx] = v;
+  }
+}
+
+void launch_skew(const BatchArgs& b, const SkewTask* d_tasks, const SkewTask* h_tasks, int begin, int count,
+                 cudaStream_t s, int64_t& launches) {
+  int nmax = 0;
+  for (int i = 0; i < count; ++i) nmax = std::max(nmax, h_tasks[begin + i].n);
+  const int gy = std::max(1, std::min(64, (nmax * nmax + 255) / 256));
+  k_skew<<<dim3(count, gy, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, begin);
+  ++launches;
+}
+
+void launch_combine(const BatchArgs& b, const CombineTask* d_tasks, const CombineTask* h_tasks, int begin, int count,
+                    cudaStream_t s, int64_t& launches) {
+  int nmax = 0;
+  for (int i = 0; i < count; ++i) nmax = std::max(nmax, h_tasks[begin + i].n);
+  const int gy = std::max(1, std::min(64, (nmax * nmax + 255) / 256));
+  k_combine<<<dim3(count, gy, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, begin);
+  ++launches;
+}
+
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
                     DevStatus* st, cudaStream_t s, int64_t& launches) {
   // Tasks of a level are pre-sorted by size class (see plan.cpp), so each

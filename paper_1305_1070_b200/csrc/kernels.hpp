@@ -46,6 +46,10 @@ void launch_skew_check(const BatchArgs& b, const double2* d_sigma_l, int64_t sl_
                        const int* d_cslot_ptr, const int* d_sl_ptr, const int* d_sl_src, const int* d_sl_partner,
                        int n_seeded, const int* d_seeded_ids, double* d_acc, DevStatus* st, cudaStream_t s,
                        int64_t& launches);
+void launch_skew(const BatchArgs& b, const SkewTask* d_tasks, const SkewTask* h_tasks, int begin, int count,
+                 cudaStream_t s, int64_t& launches);
+void launch_combine(const BatchArgs& b, const CombineTask* d_tasks, const CombineTask* h_tasks, int begin, int count,
+                    cudaStream_t s, int64_t& launches);
 void launch_output(const BatchArgs& b, int n, const int64_t* d_gr_pos, const int64_t* d_gl_pos,
                    const double* d_weights, double2* d_gr, double2* d_gl, double* d_density,
                    DevStatus* st, cudaStream_t s, int64_t& launches);

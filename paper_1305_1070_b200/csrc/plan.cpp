@@ -943,4 +943,296 @@ LeadPlan build_lead_plan(int w) {
   return L;
 }
 
+Plan build_rgf_plan(ProblemDesc desc, std::vector<std::vector<int>> layers) {
+  struct {
+    int max_layer = 0;
+  } R;
+  Plan P;
+  P.desc = std::move(desc);
+  const ProblemDesc& d = P.desc;
+  const int n = d.n;
+  if (n <= 0) fail(kContractViolation, "problem: no dofs");
+  if (layers.empty()) fail(kContractViolation, "layer map is empty");
+  // layered_from_coo (rgf.cpp:69-150): sorted layers, disjoint cover.
+  const int L = static_cast<int>(layers.size());
+  std::vector<int> layer_of(static_cast<size_t>(n), -1), local_of(static_cast<size_t>(n), -1);
+  for (int l = 0; l < L; ++l) {
+    auto& dofs = layers[static_cast<size_t>(l)];
+    std::sort(dofs.begin(), dofs.end());
+    for (size_t k = 0; k < dofs.size(); ++k) {
+      const int x = dofs[k];
+      if (x < 0 || x >= n || layer_of[static_cast<size_t>(x)] != -1)
+        fail(kContractViolation, "layer map is not a disjoint cover");
+      layer_of[static_cast<size_t>(x)] = l;
+      local_of[static_cast<size_t>(x)] = static_cast<int>(k);
+    }
+  }
+  for (int x = 0; x < n; ++x)
+    if (layer_of[static_cast<size_t>(x)] == -1) fail(kContractViolation, "layer map does not cover every dof");
+  std::vector<int> nl(static_cast<size_t>(L));
+  for (int l = 0; l < L; ++l) {
+    nl[static_cast<size_t>(l)] = static_cast<int>(layers[static_cast<size_t>(l)].size());
+    if (nl[static_cast<size_t>(l)] == 0) fail(kContractViolation, "layer map has an empty layer");
+    R.max_layer = std::max(R.max_layer, nl[static_cast<size_t>(l)]);
+  }
+  if (R.max_layer > kBigMax) fail(kContractViolation, "layer larger than the inverse kernels support");
+  // Entries coupling non-adjacent layers (H and Sigma^r are A's pattern).
+  {
+    std::vector<std::pair<int, int>> viol;
+    auto scan = [&](const std::vector<int>& rows, const std::vector<int>& cols) {
+      for (size_t k = 0; k < rows.size(); ++k) {
+        const int lr = layer_of[static_cast<size_t>(rows[k])], lc = layer_of[static_cast<size_t>(cols[k])];
+        if (std::abs(lr - lc) > 1) viol.push_back({std::min(rows[k], cols[k]), std::max(rows[k], cols[k])});
+      }
+    };
+    scan(d.h_rows, d.h_cols);
+    scan(d.sr_rows, d.sr_cols);
+    if (!viol.empty()) {
+      std::sort(viol.begin(), viol.end());
+      viol.erase(std::unique(viol.begin(), viol.end()), viol.end());
+      fail(kPartitionViolation, std::to_string(viol.size()) + " entr(ies) couple non-adjacent layers");
+    }
+    // lower coupling == transpose of the upper one (rgf.cpp:137-147), on H
+    std::map<std::pair<int, int>, cplx> inter;
+    for (size_t k = 0; k < d.h_rows.size(); ++k)
+      if (layer_of[static_cast<size_t>(d.h_rows[k])] != layer_of[static_cast<size_t>(d.h_cols[k])])
+        inter[{d.h_rows[k], d.h_cols[k]}] += d.h_vals[k];
+    for (const auto& kv : inter) {
+      auto it = inter.find({kv.first.second, kv.first.first});
+      const cplx mirror = it == inter.end() ? cplx(0.0, 0.0) : it->second;
+      if (mirror != kv.second) {
+        const int l = std::min(layer_of[static_cast<size_t>(kv.first.first)], layer_of[static_cast<size_t>(kv.first.second)]);
+        fail(kContractViolation, "lower coupling " + std::to_string(l) + " is not the transpose of the upper coupling");
+      }
+    }
+    for (size_t k = 0; k < d.sl_rows.size(); ++k)
+      if (layer_of[static_cast<size_t>(d.sl_rows[k])] != layer_of[static_cast<size_t>(d.sl_cols[k])])
+        fail(kContractViolation, "sigma_lesser is not block diagonal on the layer map");
+  }
+  // ---- arena
+  int64_t cur = 0;
+  auto take = [&](int64_t count) {
+    const int64_t o = cur;
+    cur += align8(std::max<int64_t>(count, 1));
+    return o;
+  };
+  std::vector<int64_t> og(L), osl(L), ogl(L), ob(L, -1), ogb(L, -1), oxc(L, -1), ogrd(L), oout(L);
+  for (int l = 0; l < L; ++l) {
+    const int64_t a = nl[l], b = l + 1 < L ? nl[l + 1] : 0;
+    og[l] = take(a * a);
+    osl[l] = take(a * a);
+    ogl[l] = take(a * a);
+    if (l + 1 < L) {
+      ob[l] = take(a * b);
+      ogb[l] = take(a * b);
+      oxc[l] = take(a * a);
+      ogrd[l] = take(a * a);
+      oout[l] = take(a * a);
+    }
+  }
+  ogrd[L - 1] = og[L - 1];
+  oout[L - 1] = ogl[L - 1];
+  const int64_t nm2 = int64_t(R.max_layer) * R.max_layer;
+  const int64_t oT = take(nm2), oM = take(nm2), oPP = take(nm2), oTERM = take(nm2), oX = take(nm2);
+  P.big_scratch = cur;
+  if (R.max_layer > kSmemInvMax) take(align8(int64_t(R.max_layer) * kPanel) * 2 + align8((R.max_layer + 3) / 4) + 8);
+  P.arena = cur;
+  P.a_region = 0;
+  for (int l = 0; l < L; ++l) {
+    P.init_zero.push_back(InitRegion{og[l], 1, nl[l] * nl[l], 0});
+    P.init_zero.push_back(InitRegion{osl[l], 1, nl[l] * nl[l], 0});
+    if (l + 1 < L) P.init_zero.push_back(InitRegion{ob[l], 1, nl[l] * nl[l + 1], 0});
+  }
+  // ---- assembly maps (same kernels as the HSC path)
+  auto a_pos = [&](int r, int c) -> int64_t {
+    const int lr = layer_of[static_cast<size_t>(r)], lc = layer_of[static_cast<size_t>(c)];
+    const int ir = local_of[static_cast<size_t>(r)], ic = local_of[static_cast<size_t>(c)];
+    if (lr == lc) return og[lr] + int64_t(ir) * nl[lr] + ic;
+    if (lc == lr + 1) return ob[lr] + int64_t(ir) * nl[lc] + ic;
+    return -1;  // lower coupling: the transpose of the upper one
+  };
+  {
+    std::vector<std::pair<int64_t, cplx>> hv;
+    for (size_t k = 0; k < d.h_rows.size(); ++k) {
+      const int64_t pos = a_pos(d.h_rows[k], d.h_cols[k]);
+      if (pos >= 0) hv.push_back({pos, -d.h_vals[k]});
+    }
+    std::stable_sort(hv.begin(), hv.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (const auto& e : hv) {
+      if (!P.h_pos.empty() && P.h_pos.back() == e.first) P.h_val.back() += e.second;
+      else {
+        P.h_pos.push_back(e.first);
+        P.h_val.push_back(e.second);
+      }
+    }
+  }
+  P.diag_pos.resize(static_cast<size_t>(n));
+  for (int x = 0; x < n; ++x) {
+    const int l = layer_of[static_cast<size_t>(x)];
+    P.diag_pos[static_cast<size_t>(x)] = og[l] + int64_t(local_of[static_cast<size_t>(x)]) * (nl[l] + 1);
+  }
+  {
+    std::map<int64_t, std::vector<int>> by_pos;
+    for (size_t k = 0; k < d.sr_rows.size(); ++k) {
+      const int64_t pos = a_pos(d.sr_rows[k], d.sr_cols[k]);
+      if (pos >= 0) by_pos[pos].push_back(static_cast<int>(k));
+    }
+    P.sr_slot_ptr.push_back(0);
+    for (const auto& kv : by_pos) {
+      P.sr_slot_pos.push_back(kv.first);
+      for (int s : kv.second) P.sr_slot_src.push_back(s);
+      P.sr_slot_ptr.push_back(static_cast<int>(P.sr_slot_src.size()));
+    }
+  }
+  {
+    std::map<std::pair<int, int>, std::vector<int>> by_rc;
+    for (size_t k = 0; k < d.sl_rows.size(); ++k) by_rc[{d.sl_rows[k], d.sl_cols[k]}].push_back(static_cast<int>(k));
+    std::map<std::pair<int, int>, int> slot_of;
+    P.sl_slot_ptr.push_back(0);
+    for (const auto& kv : by_rc) {
+      const int r = kv.first.first, c = kv.first.second;
+      const int l = layer_of[static_cast<size_t>(r)];
+      slot_of[kv.first] = static_cast<int>(P.sl_slot_pos.size());
+      P.sl_slot_pos.push_back(osl[l] + int64_t(local_of[static_cast<size_t>(r)]) * nl[l] + local_of[static_cast<size_t>(c)]);
+      P.sl_cluster.push_back(l);
+      for (int s : kv.second) P.sl_slot_src.push_back(s);
+      P.sl_slot_ptr.push_back(static_cast<int>(P.sl_slot_src.size()));
+    }
+    for (const auto& kv : by_rc) {
+      auto it = slot_of.find({kv.first.second, kv.first.first});
+      P.sl_partner.push_back(it == slot_of.end() ? -1 : it->second);
+    }
+    std::vector<int> lidx(static_cast<size_t>(L), -1);
+    for (int l : P.sl_cluster)
+      if (lidx[l] < 0) lidx[l] = 0;
+    for (int l = 0; l < L; ++l)
+      if (lidx[l] == 0) {
+        lidx[l] = static_cast<int>(P.seeded_ids.size());
+        P.seeded_ids.push_back(l);
+      }
+    for (int l : P.sl_cluster) P.sl_cidx.push_back(lidx[l]);
+    P.cslot_ptr.assign(P.seeded_ids.size() + 1, 0);
+    for (int c : P.sl_cidx) ++P.cslot_ptr[c + 1];
+    for (size_t q = 1; q < P.cslot_ptr.size(); ++q) P.cslot_ptr[q] += P.cslot_ptr[q - 1];
+    P.cslots.assign(P.sl_cidx.size(), 0);
+    std::vector<int> fillp(P.cslot_ptr.begin(), P.cslot_ptr.end() - 1);
+    for (size_t s2 = 0; s2 < P.sl_cidx.size(); ++s2) P.cslots[fillp[P.sl_cidx[s2]]++] = static_cast<int>(s2);
+  }
+  P.out_gr_pos.resize(static_cast<size_t>(n));
+  P.out_gl_pos.resize(static_cast<size_t>(n));
+  for (int x = 0; x < n; ++x) {
+    const int l = layer_of[static_cast<size_t>(x)];
+    const int64_t dd = int64_t(local_of[static_cast<size_t>(x)]) * (nl[l] + 1);
+    P.out_gr_pos[static_cast<size_t>(x)] = ogrd[l] + dd;
+    P.out_gl_pos[static_cast<size_t>(x)] = oout[l] + dd;
+  }
+  // ---- schedule
+  Builder B(P);
+  auto& T = P.gemm_terms;
+  auto term = [&](int k, int aop, int64_t a, int lda, int bop, int64_t b, int ldb, int sign) {
+    B.add_term(T, k, aop, a, lda, bop, b, ldb, sign);
+  };
+  auto skew = [&](int sz, int64_t src, int64_t dst) {
+    Op op{};
+    op.kind = K_SKEW;
+    op.phase = 11;
+    op.begin = static_cast<int>(P.skew_tasks.size());
+    op.count = 1;
+    P.skew_tasks.push_back(SkewTask{sz, 0, src, dst});
+    P.ops.push_back(op);
+  };
+  // rgf_gr forward sweep (rgf.cpp:198-225), dense couplings
+  for (int l = 0; l < L; ++l) {
+    if (l > 0) {
+      const int a = nl[l - 1], b = nl[l];
+      B.open(K_GEMM, 10, l);  // GB_{l-1} = g_{l-1} B_{l-1}
+      int tb = static_cast<int>(T.size());
+      term(a, OP_N, og[l - 1], a, OP_N, ob[l - 1], b, +1);
+      B.gemm_task(a, b, ogb[l - 1], b, MODE_SET, 0, 0, tb);
+      B.close();
+      B.open(K_GEMM, 10, l);  // m = D_l - GB^T B
+      tb = static_cast<int>(T.size());
+      term(a, OP_T, ogb[l - 1], b, OP_N, ob[l - 1], b, -1);
+      B.gemm_task(b, b, og[l], b, MODE_ADD, 0, 0, tb);
+      B.close();
+    }
+    B.emit_inverses(l, 10, {InvItem{nl[l], l, l, og[l]}}, P.big_scratch);
+  }
+  // backward sweep (rgf.cpp:227-282)
+  for (int l = L - 2; l >= 0; --l) {
+    const int a = nl[l], b = nl[l + 1];
+    B.open(K_GEMM, 10, l);  // goff = -G_{l+1,l+1} GB_l^T   (b x a)
+    int tb = static_cast<int>(T.size());
+    term(b, OP_N, ogrd[l + 1], b, OP_T, ogb[l], b, -1);
+    B.gemm_task(b, a, oT, a, MODE_SET, 0, 0, tb);
+    B.close();
+    B.open(K_GEMM, 10, l);
+    tb = static_cast<int>(T.size());  // G_ll = g_l - GB_l goff
+    term(b, OP_N, ogb[l], b, OP_N, oT, a, -1);
+    B.gemm_task(a, a, ogrd[l], a, MODE_INIT, og[l], a, tb);
+    tb = static_cast<int>(T.size());  // xcoef_l = -goff^T B_l^T
+    term(b, OP_T, oT, a, OP_T, ob[l], b, -1);
+    B.gemm_task(a, a, oxc[l], a, MODE_SET, 0, 0, tb);
+    B.close();
+  }
+  P.rgf_gr_ops = static_cast<int>(P.ops.size());
+  // rgf_gless forward sweep (rgf.cpp:310-345)
+  for (int l = 0; l < L; ++l) {
+    const int b = nl[l];
+    if (l > 0) {
+      const int a = nl[l - 1];
+      B.open(K_GEMM, 11, l);  // t = B^T g<_{l-1}   (b x a)
+      int tb = static_cast<int>(T.size());
+      term(a, OP_T, ob[l - 1], b, OP_N, ogl[l - 1], a, +1);
+      B.gemm_task(b, a, oT, a, MODE_SET, 0, 0, tb);
+      B.close();
+      B.open(K_GEMM, 11, l);  // S_l += t conj(B)
+      tb = static_cast<int>(T.size());
+      term(a, OP_N, oT, a, OP_C, ob[l - 1], b, +1);
+      B.gemm_task(b, b, osl[l], b, MODE_ADD, 0, 0, tb);
+      B.close();
+    }
+    B.open(K_GEMM, 11, l);  // m = g_l S_l
+    int tb = static_cast<int>(T.size());
+    term(b, OP_N, og[l], b, OP_N, osl[l], b, +1);
+    B.gemm_task(b, b, oM, b, MODE_SET, 0, 0, tb);
+    B.close();
+    B.open(K_GEMM, 11, l);  // m g_l^H
+    tb = static_cast<int>(T.size());
+    term(b, OP_N, oM, b, OP_H, og[l], b, +1);
+    B.gemm_task(b, b, oPP, b, MODE_SET, 0, 0, tb);
+    B.close();
+    skew(b, oPP, ogl[l]);
+  }
+  // backward sweep (rgf.cpp:347-378)
+  for (int l = L - 2; l >= 0; --l) {
+    const int a = nl[l], b = nl[l + 1];
+    B.open(K_GEMM, 11, l);
+    int tb = static_cast<int>(T.size());  // m = W G<_{l+1}, W = GB_l
+    term(b, OP_N, ogb[l], b, OP_N, oout[l + 1], b, +1);
+    B.gemm_task(a, b, oM, b, MODE_SET, 0, 0, tb);
+    tb = static_cast<int>(T.size());  // x = xcoef_l g<_l
+    term(a, OP_N, oxc[l], a, OP_N, ogl[l], a, +1);
+    B.gemm_task(a, a, oX, a, MODE_SET, 0, 0, tb);
+    B.close();
+    B.open(K_GEMM, 11, l);  // m W^H
+    tb = static_cast<int>(T.size());
+    term(b, OP_N, oM, b, OP_H, ogb[l], b, +1);
+    B.gemm_task(a, a, oPP, a, MODE_SET, 0, 0, tb);
+    B.close();
+    skew(a, oPP, oTERM);
+    Op op{};
+    op.kind = K_COMBINE;
+    op.phase = 11;
+    op.begin = static_cast<int>(P.comb_tasks.size());
+    op.count = 1;
+    P.comb_tasks.push_back(CombineTask{a, 0, ogl[l], oTERM, oX, oout[l]});
+    P.ops.push_back(op);
+  }
+  P.max_block = R.max_layer;
+  for (int l = 0; l < L; ++l) P.exec_inv_cmul += double(nl[l]) * nl[l] * nl[l];
+  P.rgf_layers = std::move(layers);
+  return P;
+}
+
 }  // namespace negfb

@@ -124,7 +124,8 @@ struct BigTask {
   int64_t off_thr;   // (threshold, failed flag)
 };
 
-enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL = 4, K_PERM = 5 };
+enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL = 4, K_PERM = 5, K_SKEW = 6,
+                    K_COMBINE = 7 };
 
 struct Op {
   int kind;
@@ -134,6 +135,16 @@ struct Op {
   int level;
   int k0;            // K_PANEL: first column of the panel
   double cmul;       // executed complex multiply-adds per energy
+};
+
+// Elementwise steps of the RGF path (K_SKEW / K_COMBINE ops).
+struct SkewTask {      // dst = skew_half(src): upper triangle of src, Im of
+  int n, pad;          // the diagonal, lower = -conj(upper) (dense.cpp:136-170)
+  int64_t src, dst;
+};
+struct CombineTask {   // out = gl + term + x - x^H (rgf.cpp:373-377)
+  int n, pad;
+  int64_t gl, term, x, out;
 };
 
 struct Ledger {
@@ -202,7 +213,11 @@ struct Plan {
   std::vector<ScaleTask> scale_tasks;
   std::vector<InvTask> inv_tasks;
   std::vector<BigTask> big_tasks;
+  std::vector<SkewTask> skew_tasks;      // RGF path only
+  std::vector<CombineTask> comb_tasks;   // RGF path only
   std::vector<Op> ops;
+  std::vector<std::vector<int>> rgf_layers;  // non-empty: an RGF plan (no tree)
+  int rgf_gr_ops = 0;                        // ops [0, rgf_gr_ops) = rgf_gr
 
   Ledger ref_fold, ref_gless;   // reference ledger per energy (hsc_fold / hsc_gless)
   double exec_cmul = 0.0;       // executed complex MACs per energy (incl. inversions m^3)
@@ -245,5 +260,12 @@ struct LeadPlan {
   int inv_fin[2] = {0, 0};
 };
 LeadPlan build_lead_plan(int w);
+
+// Layered recursive Green's function (rgf_gr / rgf_gless, rgf.cpp:181-380)
+// as one replayable op list over per-energy arenas (Plan::rgf_layers set):
+// the second, independent GPU path (chain partitions == RGF,
+// test_hsc.cpp:648-678) and the paper's comparison baseline.  Every coupling
+// is treated as dense.
+Plan build_rgf_plan(ProblemDesc desc, std::vector<std::vector<int>> layers);
 
 }  // namespace negfb

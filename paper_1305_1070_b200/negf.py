@@ -173,6 +173,7 @@ def _load() -> C.CDLL:
         "negf_plan_fill": ([vp, vp, vp], i32),
         "negf_plan_gemm_tasks": ([vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_destroy": ([vp], None),
+        "negf_rgf_plan_create": ([C.POINTER(_Problem), i32, vp, vp, C.POINTER(vp), st], i32),
         "negf_gpu_create": ([vp, i32, i32, C.POINTER(vp), st], i32),
         "negf_gpu_batch_capacity": ([vp], i32),
         "negf_gpu_solve_batch": ([vp, i32, vp, vp, vp, vp, i32, vp, vp, st], i32),
@@ -216,7 +217,7 @@ def _load() -> C.CDLL:
 
 _lib = _load()
 ABI_SYMBOLS = (
-    "negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_gemm_tasks negf_plan_destroy "
+    "negf_rgf_plan_create negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_gemm_tasks negf_plan_destroy "
     "negf_gpu_create negf_gpu_batch_capacity negf_gpu_solve_batch negf_gpu_solve_batch_device "
     "negf_gpu_check negf_gpu_density negf_gpu_stream negf_gpu_density_device "
     "negf_gpu_last_launches negf_gpu_destroy negf_nccl_unique_id negf_gpu_nccl_init "
@@ -451,6 +452,37 @@ class HscPlan:
         ids = np.zeros(max(int(ptr[-1]), 1), np.int32)
         _lib.negf_plan_fill(self._h, _ptr(ptr), _ptr(ids))
         return [ids[ptr[c] : ptr[c + 1]].tolist() for c in range(nc)]
+
+
+class RgfPlan(HscPlan):
+    """Layered recursive Green's function plan (rgf_gr + rgf_gless,
+    rgf.cpp:181-380) over the problem's layers (or ``layers``): the
+    independent second GPU path and the paper's comparison baseline.  Solved
+    by the same ``HscGpuSolver``; errors as layered_from_coo (rgf.cpp:69-150):
+    ContractViolation for a bad layer map, PartitionViolation for entries
+    coupling non-adjacent layers."""
+
+    def __init__(self, problem: Problem, layers=None):
+        self.problem = problem
+        layers = problem.layers if layers is None else layers
+        if layers is None or len(layers) == 0:
+            raise ContractViolation("layer map is empty")
+        ptr = np.zeros(len(layers) + 1, np.int32)
+        ptr[1:] = np.cumsum([len(x) for x in layers])
+        dofs = np.ascontiguousarray(np.concatenate([np.asarray(x, np.int32) for x in layers]), np.int32)
+        p, keep = problem.c_struct()
+        h = C.c_void_p()
+        st = _Status()
+        _lib.negf_rgf_plan_create(C.byref(p), len(layers), _ptr(ptr), _ptr(dofs), C.byref(h), C.byref(st))
+        del keep
+        _raise(st)
+        self._h = h
+
+    def tree(self):
+        raise ContractViolation("an RGF plan has layers, not a separator tree")
+
+    def fill_sets(self):
+        raise ContractViolation("an RGF plan has layers, not fill sets")
 
 
 def nested_dissection(n: int, edges: np.ndarray, atomic_groups=(), max_leaf: int = 64, coords=None) -> SeparatorTree:

@@ -132,9 +132,23 @@ def make_leads() -> None:
         refio.run_lead(path, os.path.join(HERE, name + ".out"))
 
 
+def make_rgf() -> None:
+    """The reference's layered RGF (rgf_gr + rgf_gless, rgf.cpp:181-380) on
+    every problem fixture's own layer map."""
+    import glob
+    for p in sorted(glob.glob(os.path.join(HERE, "*.bin"))):
+        name = os.path.basename(p)[:-4]
+        if name.startswith("lead_"):
+            continue
+        refio.run_reference(p, os.path.join(HERE, name + ".rgf.out"), solver="rgf")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["leads"]:
         make_leads()
+    elif sys.argv[1:] == ["rgf"]:
+        make_rgf()
     else:
         main()
         make_leads()
+        make_rgf()
