@@ -328,6 +328,31 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
     e2g_value = world * per_rank / (float(ms_e2g.item()) / 1e3)
     solver.check()
 
+    # ---- the paper's comparison baseline on the same GPU: layered RGF
+    # (rgf_gr + rgf_gless), same inputs, device-resident.
+    rgf = None
+    if not args.no_rgf:
+        rplan = negf.RgfPlan(w.problem)
+        rs = negf.HscGpuSolver(rplan, device=local_rank, max_energy_batch=min(per_rank, 128))
+        rs.set_residual_check(False)
+        rstream = torch.cuda.ExternalStream(rs.stream_ptr, device=dev)
+        rs.solve_device(E, Wt, SR, SL, first_energy_index=int(my[0]))
+        torch.cuda.synchronize(dev)
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(rstream)
+        rs.solve_device(E, Wt, SR, SL, first_energy_index=int(my[0]), sync=False)
+        r1.record(rstream)
+        torch.cuda.synchronize(dev)
+        rs.check()
+        rms = r0.elapsed_time(r1)
+        rinfo = rplan.info()
+        rgf = {"value": per_rank / (rms / 1e3), "unit": UNIT, "ms_per_step": rms,
+               "exec_gflop_per_energy": rinfo.exec_cmul * 8 / 1e9,
+               "fp64_tflops": rinfo.exec_cmul * 8 * per_rank / (rms / 1e3) / 1e12,
+               "note": "layered RGF on the same GPU and inputs (one timed step, rank-local)"}
+        del rs, rplan
+
     if rank != 0:
         return
     g = kstats["gemm"]
@@ -387,6 +412,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
                           "d2h_bytes_per_step": d2h,
                           "note": "energies/weights in; contact self-energies built on the GPU "
                                   "(analytic lead modes + lesser fill) inside the timed region"},
+        "rgf_gpu": rgf,
         "gpu_launches": launches_timed,
         "clocks": clk,
     }
@@ -403,6 +429,7 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--energies", type=int, default=256, help="energy points per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rgf", action="store_true", help="skip the GPU RGF comparison line")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
