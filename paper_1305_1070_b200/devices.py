@@ -398,3 +398,142 @@ class GpuSelfEnergies:
                                    ph_sl_off=-1 if ph is None else ph["sl_off"],
                                    mu_phonon=0.0 if ph is None else ph["mu"], stream=stream)
         return sigma_r, sigma_lesser
+
+
+# ---------------------------------------------------------------------------
+# make_synthetic_system (synthetic.cpp:10-150): the reference's benchmark
+# system (cmd_bench, run.cpp:361-419)
+# ---------------------------------------------------------------------------
+def synthetic_system(nx: int, ny: int, seed: int, fuzz: bool = False, coupling_t: float = 1.0,
+                     max_leaf: int = 64, args_right_to_left: bool = True) -> dict:
+    """Restatement of make_synthetic_system: dof = j*nx + i (layer j = row of
+    the grid), coords (i, j), draws from mt19937_64(seed) in the reference's
+    order.  ``args_right_to_left``: the evaluation order of the two draws
+    inside one ``cplx(re, im)`` constructor call (unspecified in C++; GCC
+    evaluates right to left) -- pinned against the reference's own dumps in
+    tests/test_ledger_bench.py.  Returns H (COO, coo_normalize order), the
+    contact blocks, the Sigma^< COO, layers, coords and a ``Problem``."""
+    if nx < 1 or ny < 1:
+        raise ValueError("synthetic grid dimensions must be positive")
+    if coupling_t == 0.0:
+        raise ValueError("synthetic coupling strength must be nonzero")
+    rng = MT19937_64(seed)
+    u = lambda: float(rng.uniform01(1)[0])  # noqa: E731
+
+    def pair(f_re, f_im):
+        if args_right_to_left:
+            im = f_im()
+            re = f_re()
+        else:
+            re = f_re()
+            im = f_im()
+        return complex(re, im)
+
+    n = nx * ny
+    t = coupling_t
+    h = {}
+
+    def add(r, c, v):
+        h[(r, c)] = h.get((r, c), 0j) + v
+
+    layers = [list(range(j * nx, (j + 1) * nx)) for j in range(ny)]
+    coords = np.array([[d % nx, d // nx] for d in range(n)], np.float64)
+    for d in range(n):
+        re = 6.0 + u()
+        im = -0.2 * u() if fuzz else 0.0
+        add(d, d, complex(re, im))
+    for j in range(ny):
+        for i in range(nx - 1):
+            d = j * nx + i
+            v = pair(lambda: -(0.5 + u()), lambda: 0.3 * (u() - 0.5)) if fuzz else complex(-t, 0.0)
+            add(d, d + 1, v)
+            add(d + 1, d, v)
+    for j in range(ny - 1):
+        if not fuzz:
+            for i in range(nx):
+                d = j * nx + i
+                add(d, d + nx, complex(-t, 0.0))
+                add(d + nx, d, complex(-t, 0.0))
+            continue
+        kind = j % 3
+        if kind == 0:
+            v = complex(-(0.5 + u()), 0.0)
+            for i in range(nx):
+                d = j * nx + i
+                add(d, d + nx, v)
+                add(d + nx, d, v)
+        else:
+            for i in range(nx):
+                v = pair(lambda: -(0.5 + u()), lambda: 0.2 * (u() - 0.5))
+                d = j * nx + i
+                add(d, d + nx, v)
+                add(d + nx, d, v)
+            if kind == 2 and nx >= 2:
+                v = pair(lambda: -0.3 * u(), lambda: 0.1 * (u() - 0.5))
+                d = j * nx
+                add(d, d + nx + 1, v)
+                add(d + nx + 1, d, v)
+                w = pair(lambda: -0.3 * u(), lambda: 0.1 * (u() - 0.5))
+                add(d + 1, d + nx, w)
+                add(d + nx, d + 1, w)
+    keys = sorted(h)
+    h_rows = np.array([k[0] for k in keys], np.int32)
+    h_cols = np.array([k[1] for k in keys], np.int32)
+    h_vals = np.array([h[k] for k in keys], np.complex128)
+
+    def draw_contact(m):
+        r = np.zeros((m, m), np.complex128)
+        for a in range(m):
+            for b in range(m):
+                r[a, b] = pair(lambda: 0.2 * (u() - 0.5), lambda: 0.2 * (u() - 0.5))
+        s = r + r.T
+        for a in range(m):
+            s[a, a] -= complex(0.0, 0.5 + 0.25 * u())
+        return s
+
+    sig_l = draw_contact(nx)
+    sig_r = draw_contact(nx) if ny > 1 else None
+    less = {}
+
+    def add_lesser(dofs):
+        m = len(dofs)
+        x = np.zeros((m, m), np.complex128)
+        for a in range(m):
+            for b in range(m):
+                x[a, b] = pair(lambda: 0.3 * (u() - 0.5), lambda: 0.3 * (u() - 0.5))
+        for a in range(m):
+            for b in range(m):
+                v = x[a, b] - np.conj(x[b, a])
+                if v != 0:
+                    less[(dofs[a], dofs[b])] = less.get((dofs[a], dofs[b]), 0j) + v
+
+    add_lesser(layers[0])
+    if ny > 1:
+        add_lesser(layers[-1])
+    if fuzz:
+        for j in range(1, ny - 1):
+            for d in layers[j]:
+                less[(d, d)] = less.get((d, d), 0j) + complex(0.0, 0.1 + 0.2 * u())
+    lk = sorted(less)
+    sl_rows = np.array([k[0] for k in lk], np.int32)
+    sl_cols = np.array([k[1] for k in lk], np.int32)
+    sl_vals = np.array([less[k] for k in lk], np.complex128)
+    # Sigma^r pattern: the dense contact blocks (assemble_system adds them whole)
+    w = nx
+    L = np.array(layers[0])
+    sr_rows = [np.repeat(L, w)]
+    sr_cols = [np.tile(L, w)]
+    sr_vals = [sig_l.ravel()]
+    if sig_r is not None:
+        R = np.array(layers[-1])
+        sr_rows.append(np.repeat(R, w))
+        sr_cols.append(np.tile(R, w))
+        sr_vals.append(sig_r.ravel())
+    groups = [layers[0]] + ([layers[-1]] if ny > 1 else [])
+    prob = Problem(n=n, h_rows=h_rows, h_cols=h_cols, h_vals=h_vals,
+                   sr_rows=np.concatenate(sr_rows).astype(np.int32), sr_cols=np.concatenate(sr_cols).astype(np.int32),
+                   sl_rows=sl_rows, sl_cols=sl_cols, coords=coords, atomic_groups=groups, max_leaf=max_leaf,
+                   layers=layers)
+    return dict(problem=prob, h_rows=h_rows, h_cols=h_cols, h_vals=h_vals, sig_l=sig_l, sig_r=sig_r,
+                sl_rows=sl_rows, sl_cols=sl_cols, sl_vals=sl_vals, sr_vals=np.concatenate(sr_vals),
+                layers=layers, coords=coords)
