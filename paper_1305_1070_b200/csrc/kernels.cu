@@ -1116,18 +1116,11 @@ __global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride, in
                                               const GemmTask* __restrict__ tasks,
                                               const GemmTerm* __restrict__ terms,
                                               const GemmTile* __restrict__ tiles, int tile_begin,
-                                              int64_t items, int eg) {
+                                              int64_t items) {
   extern __shared__ double2 gsm[];
-  // Items are (energy group, tile, energy in group), energy fastest within
-  // a group of eg energies.
-  const int64_t ntiles = items / nE;
   for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
-    const int64_t grp = w / (ntiles * eg);
-    const int e0 = static_cast<int>(grp * eg);
-    const int ge = min(eg, nE - e0);
-    const int64_t rem = w - grp * ntiles * eg;
-    const int64_t ti = rem / ge;
-    const int e = e0 + static_cast<int>(rem - ti * ge);
+    const int64_t ti = w / nE;
+    const int e = static_cast<int>(w - ti * nE);
     const GemmTile tl = tiles[tile_begin + ti];
     const GemmTask tk = tasks[tl.task];
     gemm_item<WR, WC>(arena + e * stride, tk, terms, tl, gsm);
@@ -1420,15 +1413,9 @@ static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const G
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm<WR, WC>, 128, smem);
     slots = std::max(1, sms * std::max(1, per_sm));
   }
-  static int eg_env = -1;
-  if (eg_env < 0) {
-    const char* v = getenv("NEGF_GEMM_EG");
-    eg_env = v ? std::max(1, atoi(v)) : 0;
-  }
-  const int eg = eg_env > 0 ? std::min(eg_env, b.nE) : b.nE;
   const int64_t items = int64_t(tile_count) * b.nE;
   const int grid = static_cast<int>(std::min<int64_t>(items, slots));
-  k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items, eg);
+  k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
 }
 
 void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0,

@@ -24,7 +24,7 @@ from typing import Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnegf_b200.so")
+LIB_PATH = os.environ.get("NEGF_LIB") or os.path.join(_HERE, "libnegf_b200.so")  # NEGF_LIB: variant builds
 
 
 # ---------------------------------------------------------------------------
