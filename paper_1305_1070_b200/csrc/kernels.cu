@@ -979,6 +979,13 @@ __device__ __forceinline__ void load_chunk(double2* st, const double2* base, con
   }
 }
 
+constexpr int kTermCache = 48;  // term descriptors staged in shared memory per item
+
+// Sign flip on the integer pipe (keeps the FP64 pipes free).
+__device__ __forceinline__ double flip_sign(double v, int mask) {
+  return __hiloint2double(__double2hiint(v) ^ mask, __double2loint(v));
+}
+
 template <int WR, int WC>
 __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, const GemmTerm* __restrict__ terms,
                                           const GemmTile& tl, double2* smem) {
@@ -1032,8 +1039,9 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
     const GemmTerm tm = terms[ct];
     const double2* As = smem + stage * A::STAGE;
     const double2* Bs = As + A::OPA;
-    const double sg = static_cast<double>(tm.sign);
-    const bool conjb = (tm.b_op == OP_C || tm.b_op == OP_H);
+    // Sign of the term and conj(B) as sign-bit masks (integer pipe).
+    const int negA = tm.sign < 0 ? int(0x80000000) : 0;
+    const int conjB = (tm.b_op == OP_C || tm.b_op == OP_H) ? int(0x80000000) : 0;
     const bool a_rk = (tm.a_op == OP_N);
     const bool b_kr = (tm.b_op == OP_N || tm.b_op == OP_C);
     const int ksteps = min(KC, tm.k - ck0);
@@ -1045,14 +1053,14 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
       for (int i = 0; i < 2; ++i) {
         const int r = wm + 8 * i + g;
         a[i] = a_rk ? As[r * LD_RK + kk] : As[kk * A::LDA_KR + r];
-        a[i].x *= sg;
-        a[i].y *= sg;
+        a[i].x = flip_sign(a[i].x, negA);
+        a[i].y = flip_sign(a[i].y, negA);
       }
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int c = wn + 8 * j + g;
         b[j] = b_kr ? Bs[kk * A::LDB_KR + c] : Bs[c * LD_RK + kk];
-        if (conjb) b[j].y = -b[j].y;
+        b[j].y = flip_sign(b[j].y, conjB);
       }
       double as[2], bs[2];
 #pragma unroll
@@ -1123,7 +1131,19 @@ __global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride, in
     const int e = static_cast<int>(w - ti * nE);
     const GemmTile tl = tiles[tile_begin + ti];
     const GemmTask tk = tasks[tl.task];
-    gemm_item<WR, WC>(arena + e * stride, tk, terms, tl, gsm);
+    // Stage the task's term descriptors in shared memory (read every chunk).
+    GemmTerm* tsm = reinterpret_cast<GemmTerm*>(gsm + 2 * Arr<WR, WC>::STAGE);
+    const GemmTerm* tp = terms;
+    if (tk.term_count <= kTermCache) {
+      const int2* src = reinterpret_cast<const int2*>(terms + tk.term_begin);
+      int2* dst = reinterpret_cast<int2*>(tsm);
+      constexpr int W = sizeof(GemmTerm) / 8;
+      static_assert(sizeof(GemmTerm) % 8 == 0, "term copy granule");
+      for (int q = threadIdx.x; q < tk.term_count * W; q += blockDim.x) dst[q] = src[q];
+      __syncthreads();
+      tp = tsm - tk.term_begin;
+    }
+    gemm_item<WR, WC>(arena + e * stride, tk, tp, tl, gsm);
     __syncthreads();
   }
 }
@@ -1403,7 +1423,7 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
 template <int WR, int WC>
 static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                             const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
-  constexpr size_t smem = sizeof(double2) * 2 * Arr<WR, WC>::STAGE;
+  constexpr size_t smem = sizeof(double2) * 2 * Arr<WR, WC>::STAGE + sizeof(GemmTerm) * kTermCache;
   static int slots = 0;
   if (!slots) {
     int dev = 0, sms = 0, per_sm = 0;
