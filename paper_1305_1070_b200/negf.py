@@ -413,7 +413,7 @@ class HscPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:  # None during interpreter teardown
             _lib.negf_plan_destroy(h)
             self._h = None
 
@@ -512,7 +512,7 @@ class HscGpuSolver:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:
             _lib.negf_gpu_destroy(h)
             self._h = None
 
@@ -667,7 +667,7 @@ class SurfaceLead:
         _raise(st)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.negf_lead_destroy(self._h)
             self._h = None
 
