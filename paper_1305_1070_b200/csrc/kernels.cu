@@ -122,99 +122,7 @@ __device__ void report_singular(DevStatus* st, int e_global, int fold_pos, int p
   atomicMin(&st->singular_key, key);
 }
 
-// Block-wide reduction helpers (blockDim.x multiple of 32, <= 1024).
-__device__ double block_max(double v, double* red) {
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    v = (l < (blockDim.x >> 5)) ? red[l] : 0.0;
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (l == 0) red[0] = v;
-  }
-  __syncthreads();
-  const double r = red[0];
-  __syncthreads();
-  return r;
-}
 
-// Matrix view: element (r, c) at base[r * ld + c]; base in smem or global.
-template <bool kShared>
-__device__ void gauss_jordan(double2* a, int m, int* perm, double2* colk, double* red, int* flag,
-                             DevStatus* st, int e_global, int fold_pos) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  double mx = 0.0;
-  for (int i = tid; i < m * m; i += nt) mx = fmax(mx, cabs2(a[i]));
-  const double thresh = 1e-13 * block_max(mx, red);
-  for (int k = 0; k < m; ++k) {
-    // Pivot: largest |a_rk| over r >= k, lowest row on ties (warp 0).
-    if (tid < 32) {
-      double best = -1.0;
-      int bi = k;
-      for (int r = k + tid; r < m; r += 32) {
-        const double v = cabs2(a[r * m + k]);
-        if (v > best) {
-          best = v;
-          bi = r;
-        }
-      }
-      for (int o = 16; o; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      if (tid == 0) {
-        perm[k] = bi;
-        // Same pivot magnitudes as LU with partial pivoting (the rows below
-        // k hold the Schur complement); NaN never trips the test, as in
-        // the reference's `mag <= threshold`.
-        if (best <= thresh) {
-          *flag = 1;
-          report_singular(st, e_global, fold_pos, k);
-        }
-      }
-    }
-    __syncthreads();
-    if (*flag) return;
-    const int p = perm[k];
-    if (p != k)
-      for (int c = tid; c < m; c += nt) {
-        const double2 t = a[k * m + c];
-        a[k * m + c] = a[p * m + c];
-        a[p * m + c] = t;
-      }
-    __syncthreads();
-    for (int r = tid; r < m; r += nt) colk[r] = a[r * m + k];
-    __syncthreads();
-    const double2 ip = cinv(colk[k]);
-    for (int c = tid; c < m; c += nt) a[k * m + c] = (c == k) ? ip : cmul(a[k * m + c], ip);
-    __syncthreads();
-    for (int i = tid; i < m * m; i += nt) {
-      const int r = i / m, c = i - r * m;
-      if (r == k) continue;
-      const double2 f = colk[r];
-      if (c == k) a[i] = make_double2(-(f.x * ip.x - f.y * ip.y), -(f.x * ip.y + f.y * ip.x));
-      else a[i] = csub(a[i], cmul(f, a[k * m + c]));
-    }
-    __syncthreads();
-  }
-  // Undo the row interchanges as column interchanges, last first.
-  for (int k = m - 1; k >= 0; --k) {
-    const int p = perm[k];
-    if (p != k)
-      for (int r = tid; r < m; r += nt) {
-        const double2 t = a[r * m + k];
-        a[r * m + k] = a[r * m + p];
-        a[r * m + p] = t;
-      }
-    __syncthreads();
-  }
-}
 
 // Register-resident Gauss-Jordan for m <= TR*R (one CTA per (block, energy)).
 // Thread (tr, tc) of a TR x TC grid owns rows tr + TR*i and columns
@@ -872,42 +780,6 @@ __global__ void __launch_bounds__(128) k_bigperm(double2* arena, int64_t stride,
     for (int c = lane; c < m; c += 32) A[int64_t(r) * m + pos_of[c]] = buf[c];
     __syncwarp();
   }
-}
-
-__global__ void __launch_bounds__(512) k_inverse_smem(double2* arena, int64_t stride,
-                                                      const InvTask* __restrict__ tasks, int e_base,
-                                                      DevStatus* st) {
-  extern __shared__ double2 sm[];
-  const InvTask tk = tasks[blockIdx.x];
-  const int m = tk.m;
-  double2* g = arena + blockIdx.y * stride + tk.off;
-  double* red = reinterpret_cast<double*>(sm);
-  double2* colk = sm + 16;
-  double2* a = colk + m;
-  int* perm = reinterpret_cast<int*>(a + m * m);
-  int* flag = perm + m;
-  if (threadIdx.x == 0) *flag = 0;
-  for (int i = threadIdx.x; i < m * m; i += blockDim.x) a[i] = g[i];
-  __syncthreads();
-  gauss_jordan<true>(a, m, perm, colk, red, flag, st, e_base + blockIdx.y, tk.fold_pos);
-  __syncthreads();
-  for (int i = threadIdx.x; i < m * m; i += blockDim.x) g[i] = a[i];
-}
-
-__global__ void __launch_bounds__(1024) k_inverse_global(double2* arena, int64_t stride,
-                                                         const InvTask* __restrict__ tasks,
-                                                         int e_base, DevStatus* st) {
-  extern __shared__ double2 sm[];
-  const InvTask tk = tasks[blockIdx.x];
-  const int m = tk.m;
-  double2* a = arena + blockIdx.y * stride + tk.off;
-  double* red = reinterpret_cast<double*>(sm);
-  double2* colk = sm + 16;
-  int* perm = reinterpret_cast<int*>(colk + m);
-  int* flag = perm + m;
-  if (threadIdx.x == 0) *flag = 0;
-  __syncthreads();
-  gauss_jordan<false>(a, m, perm, colk, red, flag, st, e_base + blockIdx.y, tk.fold_pos);
 }
 
 // ---------------------------------------------------------------------------
