@@ -290,8 +290,12 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
     SR_d, SL_d = torch.empty_like(SR), torch.empty_like(SL)
     gr_d = torch.empty((per_rank, w.n), dtype=torch.complex128, device=dev)
     gl_d = torch.empty_like(gr_d)
-    e_t, w_t = torch.from_numpy(e_h), torch.from_numpy(w_h)
-    gr_t, gl_t = torch.from_numpy(gr_p), torch.from_numpy(gl_p)
+    # torch-owned pinned buffers (a tensor made from a numpy view of pinned
+    # memory is not flagged pinned, and its copies would be synchronous)
+    e_t = torch.from_numpy(e_h.copy()).pin_memory()
+    w_t = torch.from_numpy(w_h.copy()).pin_memory()
+    gr_t = torch.empty((per_rank, w.n), dtype=torch.complex128).pin_memory()
+    gl_t = torch.empty((per_rank, w.n), dtype=torch.complex128).pin_memory()
 
     s2 = torch.cuda.Stream(dev)  # torch-owned: host<->device copies + self-energies
 
@@ -373,7 +377,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
             if refio.ref_available():
                 cores = host_cores()
                 with tempfile.TemporaryDirectory() as tmp:
-                    r = run_reference_sample(w, 2 * cores, cores, tmp)
+                    r = run_reference_sample(w, 6 * cores, cores, tmp)
                 cpu = {"value": r["energies"] / r["wall_s"], "unit": UNIT, "cores": cores, "kind": "reference",
                        "sample": f"{r['energies']} evenly spaced energy points of config 2 on {cores} threads "
                                  f"(reference hsc_fold+hsc_gless, oracle/_ref), {r['wall_s']:.1f} s"}

@@ -243,7 +243,9 @@ void negf_lead_destroy(negf_lead* l);
  * phi_ym = sqrt(2/(w+1)) sin(y m pi/(w+1)), eps_m = 4t - 2t cos(m pi/(w+1)),
  * z = (eps_m - E - i eta)/(2t), lambda_m = z -+ sqrt(z^2 - 1) with
  * |lambda_m| <= 1; symmetrised like surface_self_energy.  Runs on `stream`
- * (a cudaStream_t, NULL = legacy default stream). */
+ * (a cudaStream_t, NULL = legacy default stream) without host sync; it uses
+ * a per-thread scratch buffer, so calls from one host thread on different
+ * streams must not overlap. */
 int negf_lead_modes_sigma_device(int w, double t_ev, double eta_ev, int n_energies, const double* d_energies,
                                  double* d_sigma_out, int64_t ld_out, void* stream, negf_status* st);
 

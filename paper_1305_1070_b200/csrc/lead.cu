@@ -600,17 +600,37 @@ int negf_lead_modes_sigma_device(int w, double t_ev, double eta_ev, int n_energi
   if (n_energies == 0) return ok(st);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   try {
-    double* phi = nullptr;
-    double2* sig = nullptr;
-    ck(cudaMallocAsync(&phi, sizeof(double) * w * w, s), "phi");
-    ck(cudaMallocAsync(&sig, sizeof(double2) * int64_t(w) * n_energies, s), "sigma_m");
-    k_modes_phi<<<(w * w + 255) / 256, 256, 0, s>>>(w, phi);
-    k_modes_lambda<<<dim3((w + 127) / 128, n_energies), 128, 0, s>>>(w, t_ev, eta_ev, d_energies, sig);
+    // Grow-only scratch (mode functions per width, lambda_m per energy): no
+    // per-call allocation, so the call stays asynchronous on `stream`.
+    struct Scratch {
+      int device = -1, w = 0;
+      double* phi = nullptr;
+      double2* sig = nullptr;
+      size_t sig_cap = 0;
+    };
+    static thread_local Scratch sc;
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    if (sc.device != dev) sc = Scratch{dev};
+    if (sc.w != w) {
+      if (sc.phi) ck(cudaFree(sc.phi), "cudaFree");
+      sc.phi = nullptr;
+      ck(cudaMalloc(&sc.phi, sizeof(double) * w * w), "phi");
+      sc.w = w;
+      k_modes_phi<<<(w * w + 255) / 256, 256, 0, s>>>(w, sc.phi);
+      ck(cudaStreamSynchronize(s), "phi");  // later calls may use other streams
+    }
+    const size_t need = size_t(w) * n_energies;
+    if (sc.sig_cap < need) {
+      if (sc.sig) ck(cudaFree(sc.sig), "cudaFree");
+      sc.sig = nullptr;
+      ck(cudaMalloc(&sc.sig, sizeof(double2) * need), "sigma_m");
+      sc.sig_cap = need;
+    }
+    k_modes_lambda<<<dim3((w + 127) / 128, n_energies), 128, 0, s>>>(w, t_ev, eta_ev, d_energies, sc.sig);
     const int nb = (w + 31) / 32;
-    k_modes_sigma<<<dim3(nb, nb, n_energies), dim3(32, 32), 0, s>>>(w, phi, sig,
+    k_modes_sigma<<<dim3(nb, nb, n_energies), dim3(32, 32), 0, s>>>(w, sc.phi, sc.sig,
                                                                     reinterpret_cast<double2*>(d_sigma_out), ld_out);
-    ck(cudaFreeAsync(phi, s), "phi free");
-    ck(cudaFreeAsync(sig, s), "sigma_m free");
     ck(cudaGetLastError(), "modes launch");
   } catch (const CudaFail& f) {
     return set_status(st, f.code, f.msg);
