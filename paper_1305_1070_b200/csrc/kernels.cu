@@ -1250,9 +1250,11 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
   int i = 0;
   while (i < count) {
     const int c = cls(h_tasks[i].m);
+    const int g8 = (h_tasks[i].m + 7) & ~7;
     int j = i;
     int mmax = 0;
-    while (j < count && cls(h_tasks[j].m) == c) {
+    // one launch per variant; the shared-memory variants per padded size
+    while (j < count && cls(h_tasks[j].m) == c && (c < 2 || ((h_tasks[j].m + 7) & ~7) == g8)) {
       mmax = std::max(mmax, h_tasks[j].m);
       ++j;
     }
