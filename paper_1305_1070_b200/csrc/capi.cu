@@ -45,11 +45,8 @@ struct NcclId {
 };
 typedef int (*nccl_init_by_value_t)(void**, int, NcclId, int);
 
-NcclApi& nccl() {
-  static NcclApi api;
-  static bool tried = false;
-  if (tried) return api;
-  tried = true;
+NcclApi load_nccl() {
+  NcclApi api;
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
   if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
@@ -60,6 +57,11 @@ NcclApi& nccl() {
   api.destroy = reinterpret_cast<nccl_destroy_t>(dlsym(h, "ncclCommDestroy"));
   api.err = reinterpret_cast<nccl_err_t>(dlsym(h, "ncclGetErrorString"));
   api.ok = api.get_id && api.init && api.allreduce && api.destroy;
+  return api;
+}
+
+NcclApi& nccl() {
+  static NcclApi api = load_nccl();  // thread-safe one-time resolution
   return api;
 }
 

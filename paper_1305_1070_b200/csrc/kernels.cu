@@ -18,9 +18,19 @@
 #include "kernels.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 
 namespace negfb {
+
+// Per-device one-time setup (function attributes are per device): true the
+// first time a call site runs on the current device.
+inline bool first_on_device(std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  return (done.fetch_or(bit) & bit) == 0;
+}
 
 namespace {
 
@@ -1267,11 +1277,10 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
       case 2:
       case 3: {
         const size_t smem = size_t(m8) * (m8 + 2) * 16 + tail;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr)) {
           cudaFuncSetAttribute(k_inverse_blocked<false, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
           cudaFuncSetAttribute(k_inverse_blocked<false, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-          attr = true;
         }
         if (mmax <= 64)
           k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
@@ -1281,11 +1290,9 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
       }
       default: {
         const size_t smem = tail + size_t(8) * m8 * 16;
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};
+        if (first_on_device(attr))
           cudaFuncSetAttribute(k_inverse_blocked<true, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-          attr = true;
-        }
         k_inverse_blocked<true, 1, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
       }
     }
@@ -1298,10 +1305,12 @@ template <int WR, int WC>
 static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                             const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
   constexpr size_t smem = sizeof(double2) * 2 * Arr<WR, WC>::STAGE + sizeof(GemmTerm) * kTermCache;
-  static int slots = 0;
+  static int slots_of[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& slots = slots_of[dev & 63];
   if (!slots) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaFuncSetAttribute(k_gemm<WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm<WR, WC>, 128, smem);
@@ -1318,11 +1327,8 @@ void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* 
   int mmax = 0;
   for (int i = 0; i < count; ++i) mmax = std::max(mmax, h_tasks[i].m);
   const size_t smem = size_t(mmax) * kPanel * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_bigpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) cudaFuncSetAttribute(k_bigpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   k_bigpanel<<<dim3(count, b.nE), 256, smem, s>>>(b.arena, b.stride, d_tasks, k0, b.e_base, st);
   ++launches;
 }
@@ -1333,11 +1339,8 @@ void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h
   int mmax = 0;
   for (int i = 0; i < count; ++i) mmax = std::max(mmax, h_tasks[i].m);
   const size_t smem = size_t(4) * mmax * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_bigperm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) cudaFuncSetAttribute(k_bigperm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   k_bigperm<<<dim3(count, b.nE), 128, smem, s>>>(b.arena, b.stride, d_tasks);
   ++launches;
 }
