@@ -1264,7 +1264,7 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
     int j = i;
     int mmax = 0;
     // one launch per variant; the shared-memory variants per padded size
-    while (j < count && cls(h_tasks[j].m) == c && (c < 2 || ((h_tasks[j].m + 7) & ~7) == g8)) {
+    while (j < count && cls(h_tasks[j].m) == c && (c < 1 || ((h_tasks[j].m + 7) & ~7) == g8)) {
       mmax = std::max(mmax, h_tasks[j].m);
       ++j;
     }
@@ -1273,7 +1273,14 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
     const size_t tail = size_t(8) * (m8 + 2) * 16 + size_t(2 * m8 + 2) * 4 + 64;
     switch (c) {
       case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st); break;
-      case 1: k_inverse_reg<8, 4><<<grid, 64, 0, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st); break;
+      case 1: {  // 17..32: the blocked kernel beats the register one ~1.8x (tools/inv_bench.cu)
+        const size_t smem = size_t(m8) * (m8 + 2) * 16 + tail;
+        static std::atomic<unsigned long long> attr1{0};
+        if (first_on_device(attr1))
+          cudaFuncSetAttribute(k_inverse_blocked<false, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        k_inverse_blocked<false, 1, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+        break;
+      }
       case 2:
       case 3: {
         const size_t smem = size_t(m8) * (m8 + 2) * 16 + tail;

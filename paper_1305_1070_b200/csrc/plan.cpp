@@ -160,14 +160,14 @@ struct Builder {
     auto& T = P.gemm_terms;
     open(K_INVERSE, phase, l);
     auto size_class = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : 3; };
-    // Grouped by kernel variant; the shared-memory variants (m > 32) also by
+    // Grouped by kernel variant; the shared-memory variants (m > 16) also by
     // padded size m8 (largest first), so each launch sizes its shared memory
     // for its own blocks and small blocks get more CTAs per SM.
     std::vector<InvItem> order(items.begin(), items.end());
     std::stable_sort(order.begin(), order.end(), [&](const InvItem& a, const InvItem& b) {
       const int ca = size_class(a.m), cb = size_class(b.m);
       if (ca != cb) return ca < cb;
-      if (ca >= 2) return ((a.m + 7) & ~7) > ((b.m + 7) & ~7);
+      if (ca >= 1) return ((a.m + 7) & ~7) > ((b.m + 7) & ~7);
       return false;
     });
     for (const InvItem& it : order)
