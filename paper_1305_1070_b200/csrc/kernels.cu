@@ -1287,12 +1287,12 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
         static std::atomic<unsigned long long> attr{0};
         if (first_on_device(attr)) {
           cudaFuncSetAttribute(k_inverse_blocked<false, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-          cudaFuncSetAttribute(k_inverse_blocked<false, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+          cudaFuncSetAttribute(k_inverse_blocked<false, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         }
         if (mmax <= 64)
           k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
         else
-          k_inverse_blocked<false, 4, 4><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+          k_inverse_blocked<false, 4, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
         break;
       }
       default: {
