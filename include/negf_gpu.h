@@ -189,8 +189,12 @@ void negf_gpu_destroy(negf_gpu* g);
  * torch.distributed broadcast of the 128-byte id). */
 int negf_nccl_unique_id(char id_out[128], negf_status* st);
 int negf_gpu_nccl_init(negf_gpu* g, const char id[128], int nranks, int rank, negf_status* st);
-/* In-place sum of the unscaled density accumulators across ranks. */
+/* In-place sum of the unscaled density accumulators across ranks.  Default
+ * (ordered): ncclAllGather of the partials + a device sum in
+ * rank order, bit-reproducible for any rank count and NCCL algorithm;
+ * negf_gpu_set_ordered_reduce(g, 0) selects a plain ncclAllReduce. */
 int negf_gpu_allreduce_density(negf_gpu* g, negf_status* st);
+int negf_gpu_set_ordered_reduce(negf_gpu* g, int ordered);
 
 /* ---- Contact self-energies on the GPU -------------
  *

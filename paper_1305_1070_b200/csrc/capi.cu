@@ -30,6 +30,7 @@ namespace {
 // framework (torch) already loaded.
 typedef int (*nccl_get_id_t)(void*);
 typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_allgather_t)(const void*, void*, size_t, int, void*, cudaStream_t);
 typedef int (*nccl_destroy_t)(void*);
 typedef const char* (*nccl_err_t)(int);
 struct NcclApi {
@@ -37,6 +38,7 @@ struct NcclApi {
   nccl_get_id_t get_id = nullptr;
   void* init = nullptr;
   nccl_allreduce_t allreduce = nullptr;
+  nccl_allgather_t allgather = nullptr;
   nccl_destroy_t destroy = nullptr;
   nccl_err_t err = nullptr;
 };
@@ -54,6 +56,7 @@ NcclApi load_nccl() {
   api.get_id = reinterpret_cast<nccl_get_id_t>(dlsym(h, "ncclGetUniqueId"));
   api.init = dlsym(h, "ncclCommInitRank");
   api.allreduce = reinterpret_cast<nccl_allreduce_t>(dlsym(h, "ncclAllReduce"));
+  api.allgather = reinterpret_cast<nccl_allgather_t>(dlsym(h, "ncclAllGather"));
   api.destroy = reinterpret_cast<nccl_destroy_t>(dlsym(h, "ncclCommDestroy"));
   api.err = reinterpret_cast<nccl_err_t>(dlsym(h, "ncclGetErrorString"));
   api.ok = api.get_id && api.init && api.allreduce && api.destroy;
@@ -101,8 +104,11 @@ struct negf_gpu {
   double* d_skew = nullptr;
   DevStatus* d_status = nullptr;
   void* comm = nullptr;
+  int nranks = 1;
+  double* d_gather = nullptr;  // nranks x n partial densities (ordered reduction)
   int64_t launches = 0;
   int residual_mode = 1;
+  int ordered_reduce = 1;
   double max_resid = 0.0;
   // profiling
   bool profiling = false;
@@ -665,7 +671,19 @@ int negf_gpu_nccl_init(negf_gpu* g, const char id[128], int nranks, int rank, ne
   std::memcpy(nid.internal, id, 128);
   const int r = reinterpret_cast<nccl_init_by_value_t>(api.init)(&g->comm, nranks, nid, rank);
   if (r != 0) return set_status(st, NEGF_NCCL_ERROR, api.err ? api.err(r) : "ncclCommInitRank failed");
+  g->nranks = nranks;
+  try {
+    g->d_gather = dev_alloc<double>(size_t(nranks) * g->plan->desc.n, g->owned);
+  } catch (const CudaFail& f) {
+    return set_status(st, f.code, f.msg);
+  }
   return ok(st);
+}
+
+int negf_gpu_set_ordered_reduce(negf_gpu* g, int ordered) {
+  if (!g) return NEGF_CONTRACT_VIOLATION;
+  g->ordered_reduce = ordered != 0;
+  return NEGF_OK;
 }
 
 int negf_gpu_allreduce_density(negf_gpu* g, negf_status* st) {
@@ -673,6 +691,17 @@ int negf_gpu_allreduce_density(negf_gpu* g, negf_status* st) {
   if (!g || !g->comm) return set_status(st, NEGF_CONTRACT_VIOLATION, "no NCCL communicator");
   cudaSetDevice(g->device);
   const int n = g->plan->desc.n;
+  if (g->ordered_reduce && api.allgather) {
+    // Deterministic for any rank count and NCCL algorithm: gather the
+    // partials, then sum them in rank order on the device.
+    const int r = api.allgather(g->d_density, g->d_gather, size_t(n), 8, g->comm, g->stream);
+    if (r != 0) return set_status(st, NEGF_NCCL_ERROR, api.err ? api.err(r) : "ncclAllGather failed");
+    int64_t L = 0;
+    launch_ordered_sum(g->d_gather, g->nranks, n, g->d_density, g->stream, L);
+    if (cudaStreamSynchronize(g->stream) != cudaSuccess)
+      return set_status(st, NEGF_CUDA_ERROR, "sync after allgather failed");
+    return ok(st);
+  }
   // ncclFloat64 = 8, ncclSum = 0 (nccl.h)
   const int r = api.allreduce(g->d_density, g->d_density, size_t(n), 8, 0, g->comm, g->stream);
   if (r != 0) return set_status(st, NEGF_NCCL_ERROR, api.err ? api.err(r) : "ncclAllReduce failed");

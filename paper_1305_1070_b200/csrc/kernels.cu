@@ -1234,6 +1234,20 @@ __global__ void k_combine(double2* arena, int64_t stride, const CombineTask* __r
   }
 }
 
+// out[j] = sum over ranks r = 0, 1, ... of parts[r * n + j], in rank order.
+__global__ void k_ordered_sum(const double* __restrict__ parts, int nranks, int n, double* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    double s = parts[j];
+    for (int r = 1; r < nranks; ++r) s += parts[int64_t(r) * n + j];
+    out[j] = s;
+  }
+}
+
+void launch_ordered_sum(const double* parts, int nranks, int n, double* out, cudaStream_t s, int64_t& launches) {
+  k_ordered_sum<<<std::max(1, std::min(1024, (n + 255) / 256)), 256, 0, s>>>(parts, nranks, n, out);
+  ++launches;
+}
+
 void launch_skew(const BatchArgs& b, const SkewTask* d_tasks, const SkewTask* h_tasks, int begin, int count,
                  cudaStream_t s, int64_t& launches) {
   int nmax = 0;

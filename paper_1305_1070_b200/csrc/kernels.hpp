@@ -50,6 +50,7 @@ void launch_skew(const BatchArgs& b, const SkewTask* d_tasks, const SkewTask* h_
                  cudaStream_t s, int64_t& launches);
 void launch_combine(const BatchArgs& b, const CombineTask* d_tasks, const CombineTask* h_tasks, int begin, int count,
                     cudaStream_t s, int64_t& launches);
+void launch_ordered_sum(const double* parts, int nranks, int n, double* out, cudaStream_t s, int64_t& launches);
 void launch_output(const BatchArgs& b, int n, const int64_t* d_gr_pos, const int64_t* d_gl_pos,
                    const double* d_weights, double2* d_gr, double2* d_gl, double* d_density,
                    DevStatus* st, cudaStream_t s, int64_t& launches);

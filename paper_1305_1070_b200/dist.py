@@ -88,15 +88,27 @@ def sweep(solver, energies, weights, self_energies, group=None, batch: int | Non
         if nccl:
             solver.allreduce_density()          # ncclAllReduce inside the C ABI
             dens = solver.density()
-        else:
-            import torch
-
-            part = torch.from_numpy(solver.density() * (2.0 * np.pi))
-            dist.all_reduce(part, group=group)
-            dens = part.numpy() / (2.0 * np.pi)
+        else:  # same semantics as the C ABI's ordered reduction
+            dens = ordered_sum(solver.density() * (2.0 * np.pi), group) / (2.0 * np.pi)
     else:
         dens = solver.density()
     return SweepResult(idx, np.concatenate(grs) if grs else None, np.concatenate(gls) if gls else None, dens)
+
+
+def ordered_sum(part: np.ndarray, group=None) -> np.ndarray:
+    """All-gather the per-rank partials and sum them in rank order: the same
+    result for any NCCL/gloo algorithm, bit-reproducible run to run (SURVEY
+    §8(e)); the C ABI does the same on the device (negf_gpu_allreduce_density)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(part, np.float64))
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, t, group=group)
+    out = parts[0].clone()
+    for p in parts[1:]:
+        out += p
+    return out.numpy()
 
 
 def init_nccl(solver, group=None) -> None:

@@ -187,6 +187,7 @@ def _load() -> C.CDLL:
         "negf_nccl_unique_id": ([vp, st], i32),
         "negf_gpu_nccl_init": ([vp, vp, i32, i32, st], i32),
         "negf_gpu_allreduce_density": ([vp, st], i32),
+        "negf_gpu_set_ordered_reduce": ([vp, i32], i32),
         "negf_gpu_profile": ([vp, i32], i32),
         "negf_gpu_set_residual_check": ([vp, i32], i32),
         "negf_gpu_max_real_residual": ([vp], C.c_double),
@@ -221,7 +222,7 @@ ABI_SYMBOLS = (
     "negf_gpu_create negf_gpu_batch_capacity negf_gpu_solve_batch negf_gpu_solve_batch_device "
     "negf_gpu_check negf_gpu_density negf_gpu_stream negf_gpu_density_device "
     "negf_gpu_last_launches negf_gpu_destroy negf_nccl_unique_id negf_gpu_nccl_init "
-    "negf_gpu_allreduce_density negf_gpu_profile negf_gpu_profile_read negf_gpu_set_residual_check "
+    "negf_gpu_allreduce_density negf_gpu_set_ordered_reduce negf_gpu_profile negf_gpu_profile_read negf_gpu_set_residual_check "
     "negf_gpu_max_real_residual negf_lead_create negf_lead_sigma negf_lead_sigma_device negf_lead_last_sweeps "
     "negf_lead_last_launches negf_lead_stream negf_lead_destroy negf_lead_modes_sigma_device "
     "negf_contacts_fill_device negf_format_double negf_write_solve_csv negf_shard_writer_open "
@@ -594,7 +595,11 @@ class HscGpuSolver:
         _lib.negf_gpu_nccl_init(self._h, buf, int(nranks), int(rank), C.byref(st))
         _raise(st)
 
-    def allreduce_density(self) -> None:
+    def allreduce_density(self, ordered: bool = True) -> None:
+        """Sum the density partials over the NCCL communicator's ranks;
+        ``ordered`` (default): all-gather + rank-ordered sum, bit-reproducible
+        for any rank count."""
+        _lib.negf_gpu_set_ordered_reduce(self._h, int(bool(ordered)))
         st = _Status()
         _lib.negf_gpu_allreduce_density(self._h, C.byref(st))
         _raise(st)

@@ -110,3 +110,23 @@ def test_lowest_failing_energy_wins_across_ranks():
     out = _run(2, fail_at={5, 2})  # rank 0 owns 0..3, rank 1 owns 4..6
     assert [o[1] for o in out] == ["err", "err"]
     assert all(o[2] == 2 for o in out)
+
+
+def test_density_reduction_is_rank_ordered_and_bitwise_reproducible():
+    """The density partials are summed in rank order (all-gather + ordered
+    sum, the same rule as the C ABI's ncclAllGather path): every rank holds
+    bit-identical results equal to p0 + p1 + p2 computed in that order."""
+    E, W, se = _grid()
+    world = 3
+    parts = []
+    for r in range(world):
+        s = OracleSolver("syn_24x20_s5_fuzz")
+        idx = pdist.shard(len(E), world, r)
+        sr, sl = se(idx)
+        s.solve(E[idx], W[idx], sr, sl, first_energy_index=int(idx[0]))
+        parts.append(s.density() * (2.0 * np.pi))
+    expect = ((parts[0] + parts[1]) + parts[2]) / (2.0 * np.pi)
+    out = _run(world)
+    assert [o[1] for o in out] == ["ok"] * world
+    for o in out:
+        assert np.array_equal(o[3], expect)
