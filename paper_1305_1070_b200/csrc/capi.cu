@@ -582,9 +582,9 @@ int negf_gpu_solve_batch_device(negf_gpu* g, int nE, const double* d_E, const do
                 d_gr ? reinterpret_cast<double2*>(d_gr) + size_t(n) * e0 : nullptr,
                 d_gless ? reinterpret_cast<double2*>(d_gless) + size_t(n) * e0 : nullptr);
     }
+    if (!sync) return ok(st);  // profile events are read later (profile_read): no host sync here
     flush_profile(g);
-    if (sync) return collect(g, st);
-    return ok(st);
+    return collect(g, st);
   } catch (const CudaFail& f) {
     return set_status(st, f.code, f.msg);
   }
