@@ -48,7 +48,24 @@ def build(verbose: bool = False) -> str:
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)
+    build_example(verbose)
     return LIB
+
+
+EXAMPLE_SRC = os.path.join(ROOT, "examples", "negf_solve.cpp")
+EXAMPLE_BIN = os.path.join(ROOT, "examples", "negf_solve")
+
+
+def build_example(verbose: bool = False) -> str:
+    """The C++ host program on the C ABI alone (examples/negf_solve.cpp)."""
+    if os.path.exists(EXAMPLE_SRC) and _newer(EXAMPLE_BIN, [EXAMPLE_SRC, LIB, os.path.join(ROOT, "include", "negf_gpu.h")]):
+        cmd = [os.environ.get("CXX", "g++"), "-std=c++17", "-O2", "-Wall", f"-I{os.path.join(ROOT, 'include')}",
+               EXAMPLE_SRC, f"-L{HERE}", "-lnegf_b200", "-Wl,-rpath,$ORIGIN/../paper_1305_1070_b200",
+               "-o", EXAMPLE_BIN]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+    return EXAMPLE_BIN
 
 
 if __name__ == "__main__":
