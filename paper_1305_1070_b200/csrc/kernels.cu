@@ -978,7 +978,9 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
   }
   cp_async_wait<0>();
 
-  // Epilogue: lane owns C[r][c], C[r][c+1] of each 8x8 subtile.
+  // Epilogue: lane owns C[r][c], C[r][c+1] of each 8x8 subtile.  Fused
+  // diagonal (GemmTask::dmode): row sums of Psi[r][c] op(C[r][c]).
+  double2 rs[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int r = tl.m0 + wm + 8 * i + g;
@@ -993,7 +995,31 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         double2* dst = base + tk.c_off + int64_t(r) * tk.ldc + c;
         if (tk.mode == MODE_ADD) v = cadd(*dst, v);
         else if (tk.mode == MODE_INIT) v = cadd(base[tk.init_off + int64_t(r) * tk.ld_init + c], v);
-        *dst = v;
+        if (!tk.nostore) *dst = v;
+        if (tk.dmode) {
+          const double2 psi = base[tk.dpsi_off + int64_t(r) * tk.dpsi_ld + c];
+          if (tk.dmode == 2) v.y = -v.y;
+          rs[i] = cadd(rs[i], cmul(psi, v));
+        }
+      }
+    }
+  }
+  if (tk.dmode) {  // task-uniform: reduce over the 4 lanes of a row, one partial per (row, 16-column group)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      rs[i].x += __shfl_xor_sync(0xffffffffu, rs[i].x, 1);
+      rs[i].y += __shfl_xor_sync(0xffffffffu, rs[i].y, 1);
+      rs[i].x += __shfl_xor_sync(0xffffffffu, rs[i].x, 2);
+      rs[i].y += __shfl_xor_sync(0xffffffffu, rs[i].y, 2);
+    }
+    const int c0 = tl.n0 + wn;
+    if (t == 0 && c0 < tk.n) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = tl.m0 + wm + 8 * i + g;
+        if (r >= tk.m) continue;
+        const double2 s = tk.dmode == 2 ? make_double2(-rs[i].x, -rs[i].y) : rs[i];
+        base[tk.dpart_off + int64_t(r) * tk.dpart_ld + c0 / 16] = s;
       }
     }
   }
@@ -1041,6 +1067,8 @@ __global__ void k_diag(double2* arena, int64_t stride, const DiagTask* __restric
   double2* base = arena + blockIdx.y * stride;
   for (int a = threadIdx.x; a < tk.m; a += blockDim.x) {
     double2 acc = tk.has_init ? base[tk.init_off + int64_t(a) * tk.init_stride] : make_double2(0.0, 0.0);
+    for (int q = 0; q < tk.part_np; ++q)  // fused row-task partials, in order
+      acc = cadd(acc, base[tk.part_off + int64_t(a) * tk.part_np + q]);
     for (int q = tk.term_begin; q < tk.term_begin + tk.term_count; ++q) {
       const GemmTerm tm = terms[q];
       double2 s = make_double2(0.0, 0.0);

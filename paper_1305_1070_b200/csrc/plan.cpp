@@ -118,13 +118,18 @@ struct Builder {
     }
   }
 
+  // Fused-diagonal settings for the next gemm_task (see GemmTask::dmode).
+  GemmTask pend_diag{};
+
   void gemm_task(int m, int n, int64_t c_off, int ldc, int mode, int64_t init_off, int ld_init,
                  int term_begin) {
+    const GemmTask pd = pend_diag;
+    pend_diag = GemmTask{};
     if (m <= 0 || n <= 0) {
       P.gemm_terms.resize(static_cast<std::size_t>(term_begin));
       return;
     }
-    GemmTask tk;
+    GemmTask tk = pd;
     tk.m = m;
     tk.n = n;
     tk.ldc = ldc;
@@ -431,9 +436,21 @@ Plan build_plan(ProblemDesc desc) {
     if (ci.K) ci.off_psi = take(int64_t(ci.m) * ci.K);
     if (c == root) ci.off_gd = ci.off_d;  // G_rr = (A_rr folded)^-1 (hsc.cpp:148-150)
     else ci.off_gd = take(ci.full_g ? int64_t(ci.m) * ci.m : int64_t(ci.m));
-    if (ci.WG) ci.off_grow = take(int64_t(ci.m) * ci.WG);
+    // Rows of never-referenced clusters feed only their diagonal (fused into
+    // the row tasks' epilogue, GemmTask::dmode): never stored, no storage.
+    const bool g_fused = !ci.full_g && c != root, p_fused = !ci.full_p && c != root;
+    if (ci.WG) ci.off_grow = g_fused ? 0 : take(int64_t(ci.m) * ci.WG);
     if (P.any_seed && c != root) ci.off_pd = take(ci.full_p ? int64_t(ci.m) * ci.m : int64_t(ci.m));
-    if (P.any_seed && ci.WP) ci.off_prow = take(int64_t(ci.m) * ci.WP);
+    if (P.any_seed && ci.WP) ci.off_prow = p_fused ? 0 : take(int64_t(ci.m) * ci.WP);
+    // fused-diagonal partials: one per row and 16-column group of each row task
+    if (!ci.full_g && c != root && ci.m > 0) {
+      for (int j : ci.gcols) ci.gpart_np += (B.msz(j) + 15) / 16;
+      if (ci.gpart_np) ci.off_gpart = take(int64_t(ci.m) * ci.gpart_np);
+    }
+    if (P.any_seed && !ci.full_p && c != root && ci.m > 0) {
+      for (int j : ci.pcols) ci.ppart_np += (B.msz(j) + 15) / 16;
+      if (ci.ppart_np) ci.off_ppart = take(int64_t(ci.m) * ci.ppart_np);
+    }
   }
   // Scratch of the multi-CTA inverse, reused level after level.
   {
@@ -642,6 +659,18 @@ Plan build_plan(ProblemDesc desc) {
             B.add_term(T, B.msz(k), OP_N, a, X.K, OP_T,
                        B.I(j).off_grow + B.col_of(B.I(j).gcols, B.I(j).gcol_off, k), B.I(j).WG, +1);
         }
+        if (!X.full_g && X.off_gpart >= 0) {  // rows feed only diag(G_xx): fused, not stored
+          int gb = 0;
+          for (std::size_t q = 0; q < jj; ++q) gb += (B.msz(X.gcols[q]) + 15) / 16;
+          const int kk = find_pos(X.S, j);
+          if (kk < 0) fail(kInternal, "plan: diagonal-only row outside the fill set");
+          B.pend_diag.dmode = 1;
+          B.pend_diag.nostore = 1;
+          B.pend_diag.dpsi_off = X.off_psi + X.s_col[static_cast<std::size_t>(kk)];
+          B.pend_diag.dpsi_ld = X.K;
+          B.pend_diag.dpart_off = X.off_gpart + gb;
+          B.pend_diag.dpart_ld = X.gpart_np;
+        }
         B.gemm_task(X.m, B.msz(j), X.off_grow + X.gcol_off[jj], X.WG, MODE_SET, 0, 0, tb);
       }
     }
@@ -668,10 +697,9 @@ Plan build_plan(ProblemDesc desc) {
       dt.out_off = X.off_gd;
       dt.init_off = X.off_d;
       dt.term_begin = static_cast<int>(P.diag_terms.size());
-      for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
-        B.add_term(P.diag_terms, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_T,
-                   X.off_grow + B.col_of(X.gcols, X.gcol_off, X.S[kk]), X.WG, +1);
-        B.cur.cmul += double(X.m) * B.msz(X.S[kk]);
+      if (X.off_gpart >= 0) {  // sum of the fused row-task partials
+        dt.part_off = X.off_gpart;
+        dt.part_np = X.gpart_np;
       }
       dt.term_count = static_cast<int>(P.diag_terms.size()) - dt.term_begin;
       P.diag_tasks.push_back(dt);
@@ -773,6 +801,18 @@ Plan build_plan(ProblemDesc desc) {
               B.add_term(T, B.msz(k), OP_N, a, X.K, OP_H,
                          B.I(j).off_prow + B.col_of(B.I(j).pcols, B.I(j).pcol_off, k), B.I(j).WP, -1);
           }
+          if (!X.full_p && X.off_ppart >= 0) {  // rows feed only diag(P_xx): fused, not stored
+            int gb = 0;
+            for (std::size_t q = 0; q < jj; ++q) gb += (B.msz(X.pcols[q]) + 15) / 16;
+            const int kk = find_pos(X.S, j);
+            if (kk < 0) fail(kInternal, "plan: diagonal-only row outside the fill set");
+            B.pend_diag.dmode = 2;
+            B.pend_diag.nostore = 1;
+            B.pend_diag.dpsi_off = X.off_psi + X.s_col[static_cast<std::size_t>(kk)];
+            B.pend_diag.dpsi_ld = X.K;
+            B.pend_diag.dpart_off = X.off_ppart + gb;
+            B.pend_diag.dpart_ld = X.ppart_np;
+          }
           B.gemm_task(X.m, B.msz(j), X.off_prow + X.pcol_off[jj], X.WP, MODE_SET, 0, 0, tb);
         }
       }
@@ -803,10 +843,9 @@ Plan build_plan(ProblemDesc desc) {
           B.add_term(P.diag_terms, X.m, OP_N, X.off_d, X.m, OP_N, X.off_nd, X.m, +1);
           B.cur.cmul += double(X.m) * X.m;
         }
-        for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
-          B.add_term(P.diag_terms, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_H,
-                     X.off_prow + B.col_of(X.pcols, X.pcol_off, X.S[kk]), X.WP, -1);
-          B.cur.cmul += double(X.m) * B.msz(X.S[kk]);
+        if (X.off_ppart >= 0) {  // sum of the fused row-task partials
+          dt.part_off = X.off_ppart;
+          dt.part_np = X.ppart_np;
         }
         dt.term_count = static_cast<int>(P.diag_terms.size()) - dt.term_begin;
         P.diag_tasks.push_back(dt);

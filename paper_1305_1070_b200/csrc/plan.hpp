@@ -60,6 +60,14 @@ struct GemmTask {
   int64_t init_off;
   int ld_init;
   int term_begin, term_count;
+  // Fused diagonal (rows of never-referenced clusters, whose G / P rows feed
+  // only diag(G_xx) / diag(P_xx)): the epilogue forms, per output row r and
+  // 16-column warp group, sum_c Psi[r][c] * op(C[r][c]) (dmode 1: +C, 2:
+  // -conj(C)) into partials[dpart_off + r * dpart_ld + group]; nostore skips
+  // writing C itself.
+  int dmode, nostore;
+  int dpsi_ld, dpart_ld;
+  int64_t dpsi_off, dpart_off;
 };
 
 struct GemmTerm {
@@ -85,9 +93,10 @@ struct DiagTask {
   int init_stride;   // m+1 when init is a full m x m block, 1 for a vector
   int has_init;
   int term_begin, term_count;
-  int pad;
+  int part_np;       // fused-epilogue partials per row (0: none), summed in order
   int64_t out_off;   // vector of m
   int64_t init_off;
+  int64_t part_off;
 };
 
 // dst[a][b] = sig[a] * conj(src[a][b]), a < m, b < n (diagonal Sigma^< seed).
@@ -166,6 +175,8 @@ struct ClusterInfo {
   int WG = 0, WN = 0, WP = 0;
   int64_t off_d = -1, off_arow = -1, off_psi = -1, off_sig = -1;
   int64_t off_gd = -1, off_grow = -1, off_nd = -1, off_nrow = -1, off_pd = -1, off_prow = -1;
+  int64_t off_gpart = -1, off_ppart = -1;  // fused-diagonal partials (m x NP)
+  int gpart_np = 0, ppart_np = 0;
 };
 
 // Region [off, off + rows*pitch) with `cols` leading elements per row.
