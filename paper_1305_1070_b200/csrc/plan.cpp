@@ -436,12 +436,7 @@ Plan build_plan(ProblemDesc desc) {
     if (ci.K) ci.off_psi = take(int64_t(ci.m) * ci.K);
     if (c == root) ci.off_gd = ci.off_d;  // G_rr = (A_rr folded)^-1 (hsc.cpp:148-150)
     else ci.off_gd = take(ci.full_g ? int64_t(ci.m) * ci.m : int64_t(ci.m));
-    // Rows of never-referenced clusters feed only their diagonal (fused into
-    // the row tasks' epilogue, GemmTask::dmode): never stored, no storage.
-    const bool g_fused = !ci.full_g && c != root, p_fused = !ci.full_p && c != root;
-    if (ci.WG) ci.off_grow = g_fused ? 0 : take(int64_t(ci.m) * ci.WG);
     if (P.any_seed && c != root) ci.off_pd = take(ci.full_p ? int64_t(ci.m) * ci.m : int64_t(ci.m));
-    if (P.any_seed && ci.WP) ci.off_prow = p_fused ? 0 : take(int64_t(ci.m) * ci.WP);
     // fused-diagonal partials: one per row and 16-column group of each row task
     if (!ci.full_g && c != root && ci.m > 0) {
       for (int j : ci.gcols) ci.gpart_np += (B.msz(j) + 15) / 16;
@@ -452,7 +447,32 @@ Plan build_plan(ProblemDesc desc) {
       if (ci.ppart_np) ci.off_ppart = take(int64_t(ci.m) * ci.ppart_np);
     }
   }
-  // Scratch of the multi-CTA inverse, reused level after level.
+  // Row storage, by liveness.  The multi-CTA inverse scratch lives only in
+  // the fold, G rows from the G^r sweep to the seeds (hsc.cpp:229-237), P rows
+  // from the P sweep on -- so all three share one region.  Rows of
+  // never-referenced clusters feed only their diagonal (fused into the row
+  // tasks' epilogue, GemmTask::dmode): never stored, no storage.
+  const int64_t rows_begin = cur;
+  for (int c = 0; c < nc; ++c) {
+    ClusterInfo& ci = B.I(c);
+    const bool g_fused = !ci.full_g && c != root;
+    if (ci.WG) ci.off_grow = g_fused ? 0 : take(int64_t(ci.m) * ci.WG);
+  }
+  {
+    int64_t pc = rows_begin;
+    for (int c = 0; c < nc; ++c) {
+      ClusterInfo& ci = B.I(c);
+      const bool p_fused = !ci.full_p && c != root;
+      if (P.any_seed && ci.WP && !p_fused) {
+        ci.off_prow = pc;
+        pc = align8(pc + int64_t(ci.m) * ci.WP);
+      } else if (P.any_seed && ci.WP) {
+        ci.off_prow = 0;
+      }
+    }
+    cur = std::max(cur, pc);
+  }
+  // Scratch of the multi-CTA inverse (fold only), reused level after level.
   {
     std::vector<int64_t> need(static_cast<std::size_t>(t.levels()) + 1, 0);
     for (int c = 0; c < nc; ++c) {
@@ -463,7 +483,8 @@ Plan build_plan(ProblemDesc desc) {
                                      std::to_string(kBigMax));
       need[B.lev(c)] += align8(m * kPanel) * 2 + align8((m + 3) / 4) + 8;
     }
-    P.big_scratch = take(*std::max_element(need.begin(), need.end()));
+    P.big_scratch = rows_begin;
+    cur = std::max(cur, align8(rows_begin + *std::max_element(need.begin(), need.end())));
   }
   P.arena = std::max<int64_t>(cur, 8);
   // Per-energy initialisation: D blocks and the original-entry prefix of each
