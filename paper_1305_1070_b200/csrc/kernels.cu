@@ -996,6 +996,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         if (tk.mode == MODE_ADD) v = cadd(*dst, v);
         else if (tk.mode == MODE_INIT) v = cadd(base[tk.init_off + int64_t(r) * tk.ld_init + c], v);
         if (!tk.nostore) *dst = v;
+        if (tk.c2_off >= 0) base[tk.c2_off + int64_t(r) * tk.ldc + c] = make_double2(2.0 * v.x, 2.0 * v.y);
         if (tk.dmode) {
           const double2 psi = base[tk.dpsi_off + int64_t(r) * tk.dpsi_ld + c];
           if (tk.dmode == 2) v.y = -v.y;

@@ -118,13 +118,18 @@ struct Builder {
     }
   }
 
-  // Fused-diagonal settings for the next gemm_task (see GemmTask::dmode).
-  GemmTask pend_diag{};
+  // Fused-diagonal / second-output settings for the next gemm_task.
+  static GemmTask no_extra() {
+    GemmTask t{};
+    t.c2_off = -1;
+    return t;
+  }
+  GemmTask pend_diag = no_extra();
 
   void gemm_task(int m, int n, int64_t c_off, int ldc, int mode, int64_t init_off, int ld_init,
                  int term_begin) {
     const GemmTask pd = pend_diag;
-    pend_diag = GemmTask{};
+    pend_diag = no_extra();
     if (m <= 0 || n <= 0) {
       P.gemm_terms.resize(static_cast<std::size_t>(term_begin));
       return;
@@ -434,6 +439,10 @@ Plan build_plan(ProblemDesc desc) {
   for (int c = 0; c < nc; ++c) {
     ClusterInfo& ci = B.I(c);
     if (ci.K) ci.off_psi = take(int64_t(ci.m) * ci.K);
+    // 2 Psi for never-referenced, unseeded clusters: diag(G_xx) = diag(inv) +
+    // diag(Psi G_SS Psi^T) with G_SS complex symmetric, so each off-diagonal
+    // block pair enters once, doubled (see the G-row loop)
+    if (ci.K && !ci.full_g && c != root) ci.off_psi2 = take(int64_t(ci.m) * ci.K);
     if (c == root) ci.off_gd = ci.off_d;  // G_rr = (A_rr folded)^-1 (hsc.cpp:148-150)
     else ci.off_gd = take(ci.full_g ? int64_t(ci.m) * ci.m : int64_t(ci.m));
     if (P.any_seed && c != root) ci.off_pd = take(ci.full_p ? int64_t(ci.m) * ci.m : int64_t(ci.m));
@@ -650,6 +659,7 @@ Plan build_plan(ProblemDesc desc) {
       if (!I.K) continue;
       const int tb = static_cast<int>(T.size());
       B.add_term(T, I.m, OP_N, I.off_d, I.m, OP_N, I.off_arow, I.K, -1);
+      if (I.off_psi2 >= 0) B.pend_diag.c2_off = I.off_psi2;
       B.gemm_task(I.m, I.K, I.off_psi, I.K, MODE_SET, 0, 0, tb);
     }
     B.close();
@@ -666,12 +676,17 @@ Plan build_plan(ProblemDesc desc) {
     B.open(K_GEMM, 1, l);
     for (int x : xs) {
       const ClusterInfo& X = B.I(x);
+      const bool sym = !X.full_g && X.off_gpart >= 0 && X.off_psi2 >= 0;
       for (std::size_t jj = 0; jj < X.gcols.size(); ++jj) {
         const int j = X.gcols[jj];
         const int tb = static_cast<int>(T.size());
+        const int jpos = find_pos(X.S, j);
         for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
           const int k = X.S[kk];
-          const int64_t a = X.off_psi + X.s_col[kk];
+          // symmetric form: block pair (k, j) once, in the task of the later
+          // one, from 2 Psi_k; the diagonal block from Psi_j
+          if (sym && static_cast<int>(kk) > jpos) continue;
+          const int64_t a = (sym && static_cast<int>(kk) < jpos ? X.off_psi2 : X.off_psi) + X.s_col[kk];
           if (k == j) B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N, B.I(j).off_gd, B.msz(j), +1);
           else if (B.lev(k) < B.lev(j))
             B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N,

@@ -68,6 +68,9 @@ struct GemmTask {
   int dmode, nostore;
   int dpsi_ld, dpart_ld;
   int64_t dpsi_off, dpart_off;
+  // Second output 2*C at c2_off (same ldc) when >= 0: the doubled Psi of
+  // clusters whose symmetric diagonal quadratic form uses each block pair once.
+  int64_t c2_off;
 };
 
 struct GemmTerm {
@@ -176,6 +179,7 @@ struct ClusterInfo {
   int64_t off_d = -1, off_arow = -1, off_psi = -1, off_sig = -1;
   int64_t off_gd = -1, off_grow = -1, off_nd = -1, off_nrow = -1, off_pd = -1, off_prow = -1;
   int64_t off_gpart = -1, off_ppart = -1;  // fused-diagonal partials (m x NP)
+  int64_t off_psi2 = -1;                   // 2 Psi (symmetric fused G diagonal)
   int gpart_np = 0, ppart_np = 0;
 };
 
