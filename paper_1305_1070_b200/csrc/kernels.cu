@@ -297,7 +297,8 @@ __device__ __forceinline__ double2 crcp(double2 a) {
 }
 
 template <bool kGlobal, int RPL, int NB>
-__global__ void __launch_bounds__(INV_THREADS, 4) k_inverse_blocked(double2* arena, int64_t stride,
+// blocks <= 32 wide need few registers and little shared memory: 6 CTAs/SM
+__global__ void __launch_bounds__(INV_THREADS, RPL == 1 ? 6 : 4) k_inverse_blocked(double2* arena, int64_t stride,
                                                                  const InvTask* __restrict__ tasks, int e_base,
                                                                  DevStatus* st) {
   extern __shared__ double2 sm[];
