@@ -135,3 +135,41 @@ def test_gpu_rgf_errors(cuda_ok):
         bad[:, 0] += 1.0  # Hermitian part on a diagonal entry
         with pytest.raises(negf.NonSkewHermitianInput):
             s.solve(E, rp.weights, sr, bad)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["syn_24x20_s5_fuzz", "superlattice_6x20_dense", "syn_5x6_s24"])
+def test_gpu_chain_partition_equals_rgf(name, cuda_ok):
+    """test_hsc.cpp:648-678 on the GPU: the HSC path on a chain partition (one
+    cluster per layer, each layer's parent the next one) equals the layered
+    RGF path to 1e-10."""
+    rp, prob, _, _ = load_golden(name)
+    L = [list(map(int, x)) for x in rp.layers]
+    chain = negf.Problem(n=prob.n, h_rows=prob.h_rows, h_cols=prob.h_cols, h_vals=prob.h_vals,
+                         sr_rows=prob.sr_rows, sr_cols=prob.sr_cols, sl_rows=prob.sl_rows, sl_cols=prob.sl_cols,
+                         tree_parent=list(range(1, len(L))) + [-1], tree_dofs=L, layers=prob.layers)
+    sr, sl = rp.values(np.arange(len(rp.energies)))
+    g1, l1 = negf.HscGpuSolver(negf.HscPlan(chain)).solve(rp.energies, rp.weights, sr, sl)
+    g2, l2 = negf.HscGpuSolver(negf.RgfPlan(prob)).solve(rp.energies, rp.weights, sr, sl)
+    for k in range(len(rp.energies)):
+        assert rel_err(g1[k], g2[k]) < TOL
+        assert rel_err(l1[k], l2[k]) < TOL
+
+
+@pytest.mark.gpu
+def test_gpu_reruns_are_bitwise_identical(cuda_ok):
+    """Byte-identical reruns (test_cli.cpp:396-411): no atomics on the data
+    path, ordered accumulation -- two solves agree bit for bit, and so do two
+    solver instances."""
+    wl = devices.config1()
+    sr, sl = wl.self_energies([0])
+    a = negf.HscGpuSolver(negf.HscPlan(wl.problem))
+    r1 = a.solve(wl.energies, wl.weights, sr, sl)
+    d1 = a.density(reset=True)
+    r2 = a.solve(wl.energies, wl.weights, sr, sl)
+    d2 = a.density()
+    b = negf.HscGpuSolver(negf.HscPlan(wl.problem))
+    r3 = b.solve(wl.energies, wl.weights, sr, sl)
+    for x, y in ((r1, r2), (r1, r3)):
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+    assert np.array_equal(d1, d2)
