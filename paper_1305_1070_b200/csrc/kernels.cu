@@ -622,6 +622,224 @@ __global__ void __launch_bounds__(INV_THREADS, RPL == 1 ? 6 : 4) k_inverse_block
   }
 }
 
+// Look-ahead variant of the shared-memory blocked Gauss-Jordan (8-column
+// panels): while warps 1..3 apply panel p's rank-8 update to the bulk of the
+// block, warp 0 first updates the 8 columns of panel p+1 and factors them, so
+// the serial panel chain overlaps the update instead of following it.  Same
+// pivots, same singular rule, same arithmetic per element as
+// k_inverse_blocked<false, RPL, 8>.
+template <int RPL>
+__global__ void __launch_bounds__(INV_THREADS, RPL == 1 ? 6 : 4) k_inverse_la(double2* arena, int64_t stride,
+                                                                           const InvTask* __restrict__ tasks,
+                                                                           int e_base, DevStatus* st) {
+  constexpr int NB = 8;
+  extern __shared__ double2 sm[];
+  const InvTask tk = tasks[blockIdx.x];
+  const int m = tk.m;
+  const int m8 = (m + 7) & ~7;
+  const int ld = m8 + 2;  // smem row pitch: 2 mod 8 -> conflict-free fragments
+  double2* g = arena + int64_t(blockIdx.y) * stride + tk.off;
+  double2* A = sm;
+  double2* Rs = sm + int64_t(m8) * ld;
+  int* perm = reinterpret_cast<int*>(Rs + 8 * (m8 + 2));
+  int* pos_of = perm + m8;
+  double* red = reinterpret_cast<double*>(pos_of + m8 + (m8 & 1));
+  int* flag = reinterpret_cast<int*>(red + INV_THREADS / 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  double mx = 0.0;
+  for (int i = tid; i < m8 * m8; i += INV_THREADS) {
+    const int r = i / m8, c = i - r * m8;
+    const double2 v = (r < m && c < m) ? g[int64_t(r) * m + c] : make_double2(0.0, 0.0);
+    A[r * ld + c] = v;
+    mx = fmax(mx, cabs2(v));
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  if (tid == 0) *flag = 0;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < INV_THREADS / 32; ++w) mx = fmax(mx, red[w]);
+  const double thresh = 1e-13 * mx;
+  auto at = [&](int r, int c) -> double2& { return A[int64_t(r) * ld + c]; };
+
+  // Panel factorisation of columns k0..k0+7 (all rows) on warp 0.
+  auto factor = [&](int k0) {
+    const int kb = min(NB, m - k0);
+    auto pan = [&](int r, int c) -> double2& { return at(r, k0 + c); };
+    const double thr2 = thresh * thresh;
+    for (int kk = 0; kk < kb; ++kk) {
+      const int k = k0 + kk;
+      double best = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        if (r >= k && r < m) {
+          const double v = cnorm(pan(r, kk));
+          if (v > best) {
+            best = v;
+            bi = r;
+          }
+        }
+      }
+      const unsigned key = best >= 0.0 ? __float_as_uint(__double2float_ru(best)) : 0u;
+      const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+      const unsigned tied = __ballot_sync(0xffffffffu, key == kmax);
+      double cb;
+      int ci;
+      if (__popc(tied) == 1) {
+        const int src = __ffs(tied) - 1;
+        cb = __shfl_sync(0xffffffffu, best, src);
+        ci = __shfl_sync(0xffffffffu, bi, src);
+      } else {
+        cb = (key == kmax) ? best : -1.0;
+        ci = (key == kmax) ? bi : 0x7fffffff;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, cb, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, ci, o);
+          if (ob > cb || (ob == cb && oi < ci)) {
+            cb = ob;
+            ci = oi;
+          }
+        }
+      }
+      if (!(cb > thr2)) {  // |u_kk| <= 1e-13 max|a|
+        if (cb == cb) {
+          if (lane == 0) {
+            *flag = 1;
+            report_singular(st, e_base + blockIdx.y, tk.fold_pos, k);
+          }
+          return;
+        }
+      }
+      const int p = ci;
+      if (lane == 0) perm[k] = p;
+      if (lane < NB && p != k) {
+        const double2 t2 = pan(k, lane);
+        pan(k, lane) = pan(p, lane);
+        pan(p, lane) = t2;
+      }
+      __syncwarp();
+      double2 pr[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) pr[c] = pan(k, c);
+      double2 piv = pr[0];
+#pragma unroll
+      for (int c = 1; c < NB; ++c)
+        if (c == kk) piv = pr[c];
+      const double rd = 1.0 / fma(piv.x, piv.x, piv.y * piv.y);
+      const double2 ip = make_double2(piv.x * rd, -piv.y * rd);
+#pragma unroll
+      for (int c = 0; c < NB; ++c) pr[c] = (c == kk) ? ip : cmul(pr[c], ip);
+      const double2 nip = make_double2(-ip.x, -ip.y);
+#pragma unroll
+      for (int i = 0; i < RPL; ++i) {
+        const int r = lane + 32 * i;
+        if (r >= m) continue;
+        if (r == k) {
+#pragma unroll
+          for (int c = 0; c < NB; ++c) pan(r, c) = pr[c];
+          continue;
+        }
+        const double2 f = pan(r, kk);
+#pragma unroll
+        for (int c = 0; c < NB; ++c) pan(r, c) = (c == kk) ? cmul(f, nip) : csub(pan(r, c), cmul(f, pr[c]));
+      }
+      __syncwarp();
+    }
+  };
+
+  // Rank-8 update from panel k0 of the subtiles in column range [sc_lo, sc_hi)
+  // (panel k0's own columns keep M_p), by warps w0 .. w0+nw-1.
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int nsub = m8 / 8;
+  auto update = [&](int k0, int sc_lo, int sc_hi, int skip_sc, int w0, int nw) {
+    const int ncol = sc_hi - sc_lo;
+    for (int s = warp - w0; s < nsub * ncol; s += nw) {
+      const int sr = s / ncol, sc = sc_lo + (s - sr * ncol);
+      if (sc * 8 == k0 || sc == skip_sc) continue;
+      const int r = sr * 8 + g8, c = sc * 8 + 2 * t4;
+      const double2 v0 = at(r, c), v1 = at(r, c + 1);
+      double cr0 = v0.x, ci0 = v0.y, cr1 = v1.x, ci1 = v1.y;
+#pragma unroll
+      for (int q = 0; q < NB / 4; ++q) {
+        const double2 a = at(r, k0 + 4 * q + t4);
+        const double2 b = Rs[(4 * q + t4) * (m8 + 2) + sc * 8 + g8];
+        dmma(cr0, cr1, a.x, b.x);
+        dmma(cr0, cr1, -a.y, b.y);
+        dmma(ci0, ci1, a.x, b.y);
+        dmma(ci0, ci1, a.y, b.x);
+      }
+      at(r, c) = make_double2(cr0, ci0);
+      at(r, c + 1) = make_double2(cr1, ci1);
+    }
+  };
+
+  if (warp == 0) factor(0);
+  __syncthreads();
+  if (*flag) return;
+  for (int k0 = 0; k0 < m; k0 += NB) {
+    const int kb = min(NB, m - k0);
+    // row interchanges of panel k0 on the other columns; stage its pivot rows
+    for (int c = tid; c < m8; c += INV_THREADS) {
+      if (c >= k0 && c < k0 + NB) {
+#pragma unroll
+        for (int kk = 0; kk < NB; ++kk) Rs[kk * (m8 + 2) + c] = make_double2(0.0, 0.0);
+        continue;
+      }
+      for (int kk = 0; kk < kb; ++kk) {
+        const int k = k0 + kk, p = perm[k];
+        if (p != k) {
+          const double2 t2 = at(k, c);
+          at(k, c) = at(p, c);
+          at(p, c) = t2;
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < NB; ++kk) Rs[kk * (m8 + 2) + c] = (kk < kb) ? at(k0 + kk, c) : make_double2(0.0, 0.0);
+    }
+    if (tid < kb) at(k0 + tid, k0 + tid).x -= 1.0;  // M_p - I_p
+    __syncthreads();
+    const int k1 = k0 + NB;
+    if (k1 < m) {
+      if (warp == 0) {  // look-ahead: next panel's columns, then its factorisation
+        update(k0, k1 / 8, k1 / 8 + 1, -1, 0, 1);
+        __syncwarp();
+        factor(k1);
+      } else {
+        update(k0, 0, nsub, k1 / 8, 1, INV_THREADS / 32 - 1);
+      }
+    } else {
+      update(k0, 0, nsub, -1, 0, INV_THREADS / 32);
+    }
+    __syncthreads();
+    if (tid < kb) at(k0 + tid, k0 + tid).x += 1.0;
+    __syncthreads();
+    if (*flag) return;
+  }
+  // Undo the row interchanges as column interchanges (last first).
+  if (tid == 0) {
+    int* cur_at = pos_of;
+    for (int c = 0; c < m; ++c) cur_at[c] = c;
+    for (int k = m - 1; k >= 0; --k) {
+      const int p = perm[k];
+      const int t2 = cur_at[k];
+      cur_at[k] = cur_at[p];
+      cur_at[p] = t2;
+    }
+    int* inv_pos = reinterpret_cast<int*>(Rs);
+    for (int q = 0; q < m; ++q) inv_pos[cur_at[q]] = q;
+    for (int q = 0; q < m; ++q) pos_of[q] = inv_pos[q];
+  }
+  __syncthreads();
+  for (int i = tid; i < m * m; i += INV_THREADS) {
+    const int r = i / m, c = i - r * m;
+    g[int64_t(r) * m + pos_of[c]] = at(r, c);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Multi-CTA blocked Gauss-Jordan for large blocks (m > kSmemInvMax).
 // Per kPanel-column panel: k_bigpanel (one CTA per block and energy) factors
@@ -1333,10 +1551,15 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
           cudaFuncSetAttribute(k_inverse_blocked<false, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
           cudaFuncSetAttribute(k_inverse_blocked<false, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         }
+        // 65..112: the look-ahead variant (panel p+1 overlaps update p) is
+        // 15-20 % faster there; at <= 64 other CTAs already hide the panel
+        static std::atomic<unsigned long long> attr_la{0};
+        if (first_on_device(attr_la))
+          cudaFuncSetAttribute(k_inverse_la<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (mmax <= 64)
           k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
         else
-          k_inverse_blocked<false, 4, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+          k_inverse_la<4><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
         break;
       }
       default: {
