@@ -36,6 +36,7 @@ int main(int argc, char** argv) {
       terms.push_back(g);
     }
     GemmTask tk{};
+    tk.c2_off = -1;
     tk.m = M;
     tk.n = N;
     tk.ldc = N;
