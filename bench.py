@@ -196,9 +196,10 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
     info = plan.info()
     plan_s = time.perf_counter() - t0
     solver = negf.HscGpuSolver(plan, device=local_rank, max_energy_batch=per_rank)
-    # The reference's own solver leaves |Re G^<_jj| / |G^<_jj| up to ~2e-7 on
-    # this eta = 1e-6 workload (its electron_density guard of 1e-8 would stop
-    # the reference run too); record the residual instead of raising.
+    # The reference's own solver leaves |Re G^<_jj| / |G^<_jj| up to ~5e-7 on
+    # this eta = 1e-6 workload, and 0.53 at the breakdown energy (index 199,
+    # DESIGN.md §4) -- its electron_density guard of 1e-8 would stop the
+    # reference run too; record the residual instead of raising.
     solver.set_residual_check(False)
     if solver.capacity < per_rank:
         log(f"[bench] batch capacity {solver.capacity} < {per_rank}: solving in chunks")
@@ -334,10 +335,16 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
 
     # ---- the paper's comparison baseline on the same GPU: layered RGF
     # (rgf_gr + rgf_gless), same inputs, device-resident.
+    max_resid = solver.max_real_residual
     rgf = None
     if not args.no_rgf:
+        # the HSC arenas are no longer needed: give the RGF a full batch
+        del gen, SR_d, SL_d, gr_d, gl_d
+        del solver
+        torch.cuda.synchronize(dev)
+        torch.cuda.empty_cache()
         rplan = negf.RgfPlan(w.problem)
-        rs = negf.HscGpuSolver(rplan, device=local_rank, max_energy_batch=min(per_rank, 128))
+        rs = negf.HscGpuSolver(rplan, device=local_rank, max_energy_batch=per_rank)
         rs.set_residual_check(False)
         rstream = torch.cuda.ExternalStream(rs.stream_ptr, device=dev)
         rs.solve_device(E, Wt, SR, SL, first_energy_index=int(my[0]))
@@ -398,7 +405,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
                    "exec_gflop_per_energy": info.exec_flops / 1e9,
                    "ref_ledger_gflop_per_energy": info.ref_ledger_flops / 1e9,
                    "plan_seconds": plan_s,
-                   "max_real_residual": solver.max_real_residual,
+                   "max_real_residual": max_resid,
                    "fp64_tflops_step": step_tflops,
                    "fp64_peak_frac_step": step_tflops / FP64_PEAK_TFLOPS},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
