@@ -208,16 +208,54 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
     Wt = torch.from_numpy(w.weights[my].copy()).to(dev)
     SR = torch.from_numpy(sr_h).to(dev)
     SL = torch.from_numpy(sl_h).to(dev)
-    if world > 1:
-        uid = [negf.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        solver.nccl_init(uid[0], world, rank)
     stream = torch.cuda.ExternalStream(solver.stream_ptr, device=dev)
+    # The one exchange: the density partials over the C ABI's own NCCL
+    # communicator (rank-ordered all-gather + sum).  Decided collectively: if
+    # any rank cannot bring it up, every rank reduces the same way over the
+    # torch process group instead (still rank-ordered, still on the GPU).
+    reduce_mode = "none"
+    if world > 1:
+        ok = 1
+        uid = [None]
+        if rank == 0:
+            try:
+                uid = [negf.nccl_unique_id()]
+            except negf.NegfError:
+                uid = [None]
+        dist.broadcast_object_list(uid, src=0)
+        try:
+            if uid[0] is None:
+                raise negf.NcclError("no NCCL unique id")
+            solver.nccl_init(uid[0], world, rank)
+        except negf.NegfError as exc:
+            log(f"[bench] rank {rank}: C-ABI NCCL unavailable ({exc})")
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        reduce_mode = "negf-nccl" if int(flag.item()) == 1 else "torch"
+
+    class _DensityView:  # zero-copy torch view of the solver's density accumulator
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+    dens_dev = torch.as_tensor(_DensityView(solver.density_ptr, w.n), device=dev) if reduce_mode == "torch" else None
+
+    def reduce_density():
+        if reduce_mode == "negf-nccl":
+            solver.allreduce_density()
+        elif reduce_mode == "torch":
+            with torch.cuda.stream(stream):
+                parts = [torch.empty_like(dens_dev) for _ in range(world)]
+                dist.all_gather(parts, dens_dev)
+                s = parts[0].clone()
+                for p in parts[1:]:
+                    s += p
+                dens_dev.copy_(s)
 
     def step():
         solver.solve_device(E, Wt, SR, SL, first_energy_index=int(my[0]), sync=False)
         if world > 1:
-            solver.allreduce_density()
+            reduce_density()
 
     for _ in range(args.warmup):
         step()
@@ -262,7 +300,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
     def e2e_step():
         solver.solve(e_h, w_h, sr_p, sl_p, first_energy_index=int(my[0]), out_gr=gr_p, out_gless=gl_p)
         if world > 1:
-            solver.allreduce_density()
+            reduce_density()
         dens[:] = solver.density()
 
     e2e_step()
@@ -309,7 +347,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
         solver.solve_device(E_d, W_d, SR_d, SL_d, first_energy_index=int(my[0]), out_gr=gr_d, out_gless=gl_d,
                             sync=False)
         if world > 1:
-            solver.allreduce_density()
+            reduce_density()
         s2.wait_stream(stream)
         with torch.cuda.stream(s2):
             gr_t.copy_(gr_d, non_blocking=True)
@@ -399,7 +437,9 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
         "config": {"workload": w.name, "description": w.problem and w.description, "n_dofs": w.n,
                    "clusters": info.n_clusters, "levels": info.levels, "max_block": info.max_block,
                    "energies_per_step_per_gpu": per_rank, "energy_grid_points": len(w.energies),
-                   "parallelism": f"energy-sharded x{world}, NCCL allreduce of density" if world > 1 else "single GPU",
+                   "parallelism": (f"energy-sharded x{world}, density reduced once per step "
+                                   f"({'C-ABI NCCL all-gather + rank-ordered sum' if reduce_mode == 'negf-nccl' else 'torch.distributed all-gather + rank-ordered sum'})")
+                                  if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2 (per-energy arena {info.arena_bytes_per_energy / 2**20:.0f} MiB "
                          f"x {per_rank} energies)",
                    "exec_gflop_per_energy": info.exec_flops / 1e9,

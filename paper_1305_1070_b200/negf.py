@@ -570,6 +570,11 @@ class HscGpuSolver:
     def stream_ptr(self) -> int:
         return int(_lib.negf_gpu_stream(self._h) or 0)
 
+    @property
+    def density_ptr(self) -> int:
+        """Device address of the unscaled density accumulator (n float64)."""
+        return int(_lib.negf_gpu_density_device(self._h) or 0)
+
     def set_residual_check(self, raise_error: bool) -> None:
         """True (default): ResidualTooLarge like electron_density; False: record only."""
         _lib.negf_gpu_set_residual_check(self._h, int(bool(raise_error)))

@@ -171,3 +171,26 @@ def test_residual_guard_records(cuda_ok):
     s.set_residual_check(False)
     s.solve(rp.energies, rp.weights, sr, sl)
     assert 0.0 <= s.max_real_residual < 1e-8
+
+
+@pytest.mark.gpu
+def test_density_accumulator_device_view(cuda_ok):
+    """The solver's device density accumulator can be viewed zero-copy from
+    torch (bench.py's fallback reduction over the torch process group)."""
+    import torch
+
+    rp, prob, _, _ = load_golden("syn_24x20_s5_fuzz")
+    s = negf.HscGpuSolver(negf.HscPlan(prob))
+    sr, sl = rp.values(np.arange(len(rp.energies)))
+    s.solve(rp.energies, rp.weights, sr, sl)
+
+    class View:
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+    t = torch.as_tensor(View(s.density_ptr, rp.n), device="cuda")
+    dens = s.density()
+    assert np.allclose(t.cpu().numpy() / (2 * np.pi), dens, rtol=1e-15, atol=0)
+    t.mul_(2.0)  # writes through to the accumulator
+    torch.cuda.synchronize()
+    assert np.allclose(s.density(), 2 * dens, rtol=1e-15, atol=0)
