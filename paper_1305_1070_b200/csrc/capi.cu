@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <memory>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "capi_util.hpp"
@@ -76,6 +77,10 @@ struct negf_gpu {
   const Plan* plan = nullptr;
   int device = 0;
   cudaStream_t stream = nullptr;
+  // host-buffer solves: Sigma^< in and G^r out on a copy stream, overlapping
+  // the fold / the G^< sweep (created on first use)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_sl = nullptr, ev_gr = nullptr;
   std::vector<void*> owned;
   int capacity = 1;
   double2* arena = nullptr;
@@ -183,26 +188,50 @@ void reset_status(negf_gpu* g) {
   ck(cudaMemcpyAsync(g->d_status, &h, sizeof h, cudaMemcpyHostToDevice, g->stream), "status reset");
 }
 
+// Host-side hooks of a batch replay: `lesser_in` enqueues the Sigma^< upload
+// (it runs right before the first Sigma^< reader is enqueued, so the fold is
+// already queued while a pageable copy stages); with `gr_early`, the G^r
+// diagonal is written as soon as it is final and `gr_ready` recorded after it.
+struct BatchHooks {
+  std::function<void()> lesser_in;
+  bool gr_early = false;
+  cudaEvent_t gr_ready = nullptr;
+};
+
 // Replays the plan's schedule for one batch (all inputs on device).
 void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double* d_w,
-               const double2* d_sr, const double2* d_sl, double2* d_gr, double2* d_gl) {
+               const double2* d_sr, const double2* d_sl, double2* d_gr, double2* d_gl,
+               const BatchHooks* hk = nullptr) {
   const Plan& P = *g->plan;
   BatchArgs b{g->arena, P.arena, nE, e_base};
   cudaStream_t s = g->stream;
   int64_t& L = g->launches;
   {
     Bracket br(g, NEGF_KSTAT_ASSEMBLE, 0.0);
-    launch_assemble(b, P, g->d_h_pos, g->d_h_val, g->d_init_zero, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr, g->d_sr_src,
-                    static_cast<int64_t>(P.desc.sr_rows.size()), d_sr, g->d_sl_pos, g->d_sl_ptr, g->d_sl_src,
-                    static_cast<int64_t>(P.desc.sl_rows.size()), d_sl, s, L);
-    launch_skew_check(b, d_sl, static_cast<int64_t>(P.desc.sl_rows.size()), g->d_cslots, g->d_cslot_ptr,
-                      g->d_sl_ptr, g->d_sl_src, g->d_sl_partner, static_cast<int>(P.seeded_ids.size()), g->d_seeded,
-                      g->d_skew, g->d_status, s, L);
+    launch_assemble(b, P, g->d_h_pos, g->d_h_val, g->d_init_zero, g->d_diag_pos, d_E, g->d_sr_pos, g->d_sr_ptr,
+                    g->d_sr_src, static_cast<int64_t>(P.desc.sr_rows.size()), d_sr, s, L);
   }
+  const auto lesser = [&] {
+    if (hk && hk->lesser_in) hk->lesser_in();
+    Bracket br(g, NEGF_KSTAT_ASSEMBLE, 0.0);
+    const int64_t sl_nnz = static_cast<int64_t>(P.desc.sl_rows.size());
+    launch_scatter_lesser(b, P, d_E, g->d_sl_pos, g->d_sl_ptr, g->d_sl_src, sl_nnz, d_sl, s, L);
+    launch_skew_check(b, d_sl, sl_nnz, g->d_cslots, g->d_cslot_ptr, g->d_sl_ptr, g->d_sl_src, g->d_sl_partner,
+                      static_cast<int>(P.seeded_ids.size()), g->d_seeded, g->d_skew, g->d_status, s, L);
+  };
+  const bool gr_early = hk && hk->gr_early && d_gr;
+  const auto gr_out = [&] {
+    if (!gr_early) return;
+    Bracket br(g, NEGF_KSTAT_OUTPUT, 0.0);
+    launch_output_gr(b, P.desc.n, g->d_gr_pos, d_gr, s, L);
+    if (hk->gr_ready) ck(cudaEventRecord(hk->gr_ready, s), "event");
+  };
   static const int kind_stat[8] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE,
                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE};
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
+    if (static_cast<int>(oi) == P.gr_done_op) gr_out();
+    if (static_cast<int>(oi) == P.lesser_op) lesser();
     const Op& op = P.ops[oi];
     Bracket br(g, kind_stat[op.kind], op.cmul * nE, static_cast<int>(oi));
     switch (op.kind) {
@@ -232,9 +261,12 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         break;
     }
   }
+  if (P.gr_done_op >= static_cast<int>(P.ops.size())) gr_out();
+  if (P.lesser_op >= static_cast<int>(P.ops.size())) lesser();
   {
     Bracket br(g, NEGF_KSTAT_OUTPUT, 0.0);
-    launch_output(b, P.desc.n, g->d_gr_pos, g->d_gl_pos, d_w, d_gr, d_gl, g->d_density, g->d_status, s, L);
+    launch_output(b, P.desc.n, g->d_gr_pos, g->d_gl_pos, d_w, gr_early ? nullptr : d_gr, d_gl, g->d_density,
+                  g->d_status, s, L);
   }
   ck(cudaGetLastError(), "kernel launch");
 }
@@ -529,23 +561,39 @@ int negf_gpu_solve_batch(negf_gpu* g, int nE, const double* energies, const doub
     g->launches = 0;
     ck(cudaSetDevice(g->device), "cudaSetDevice");
     reset_status(g);
+    if (!g->copy_stream) {
+      ck(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking), "stream");
+      ck(cudaEventCreateWithFlags(&g->ev_sl, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&g->ev_gr, cudaEventDisableTiming), "event");
+    }
     for (int e0 = 0; e0 < nE; e0 += g->capacity) {
       const int m = std::min(g->capacity, nE - e0);
-      cudaStream_t s = g->stream;
+      cudaStream_t s = g->stream, cs = g->copy_stream;
       ck(cudaMemcpyAsync(g->d_energies, energies + e0, sizeof(double) * m, cudaMemcpyHostToDevice, s), "h2d");
       ck(cudaMemcpyAsync(g->d_weights, weights + e0, sizeof(double) * m, cudaMemcpyHostToDevice, s), "h2d");
       if (sr)
         ck(cudaMemcpyAsync(g->d_sigma_r, sigma_r + 2 * sr * size_t(e0), 16 * sr * m, cudaMemcpyHostToDevice, s),
            "h2d");
-      if (sl)
-        ck(cudaMemcpyAsync(g->d_sigma_l, sigma_lesser + 2 * sl * size_t(e0), 16 * sl * m,
-                           cudaMemcpyHostToDevice, s),
+      // Sigma^< goes in on the copy stream while the fold and the G^r sweep
+      // run; G^r comes out on it while the G^< sweep runs.
+      BatchHooks hk;
+      hk.lesser_in = [&] {
+        if (!sl) return;
+        ck(cudaMemcpyAsync(g->d_sigma_l, sigma_lesser + 2 * sl * size_t(e0), 16 * sl * m, cudaMemcpyHostToDevice,
+                           cs),
            "h2d");
+        ck(cudaEventRecord(g->ev_sl, cs), "event");
+        ck(cudaStreamWaitEvent(s, g->ev_sl, 0), "event wait");
+      };
+      hk.gr_early = gr != nullptr;
+      hk.gr_ready = g->ev_gr;
       run_batch(g, m, first + e0, g->d_energies, g->d_weights, g->d_sigma_r, g->d_sigma_l,
-                gr ? g->d_gr : nullptr, gless ? g->d_gl : nullptr);
-      if (gr)
-        ck(cudaMemcpyAsync(gr + 2 * size_t(n) * e0, g->d_gr, 16 * size_t(n) * m, cudaMemcpyDeviceToHost, s),
+                gr ? g->d_gr : nullptr, gless ? g->d_gl : nullptr, &hk);
+      if (gr) {
+        ck(cudaStreamWaitEvent(cs, g->ev_gr, 0), "event wait");
+        ck(cudaMemcpyAsync(gr + 2 * size_t(n) * e0, g->d_gr, 16 * size_t(n) * m, cudaMemcpyDeviceToHost, cs),
            "d2h");
+      }
       if (gless)
         ck(cudaMemcpyAsync(gless + 2 * size_t(n) * e0, g->d_gl, 16 * size_t(n) * m, cudaMemcpyDeviceToHost, s),
            "d2h");
@@ -554,6 +602,7 @@ int negf_gpu_solve_batch(negf_gpu* g, int nE, const double* energies, const doub
       DevStatus h;
       ck(cudaMemcpyAsync(&h, g->d_status, sizeof h, cudaMemcpyDeviceToHost, s), "status");
       ck(cudaStreamSynchronize(s), "sync");
+      ck(cudaStreamSynchronize(cs), "sync");
       flush_profile(g);
       if (h.singular_key != ~0ull || h.nonskew_key != ~0ull) break;
     }
@@ -648,6 +697,12 @@ void negf_gpu_destroy(negf_gpu* g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   for (cudaEvent_t e : g->ev) cudaEventDestroy(e);
   for (void* p : g->owned) cudaFree(p);
+  if (g->copy_stream) {
+    cudaStreamSynchronize(g->copy_stream);
+    cudaStreamDestroy(g->copy_stream);
+    cudaEventDestroy(g->ev_sl);
+    cudaEventDestroy(g->ev_gr);
+  }
   if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
 }

@@ -1420,9 +1420,7 @@ int grid_for(int64_t work, int threads, int cap) {
 void launch_assemble(const BatchArgs& b, const Plan& p, const int64_t* d_h_pos, const double2* d_h_val,
                      const InitRegion* d_init_zero, const int64_t* d_diag_pos, const double* d_energies, const int64_t* d_sr_pos,
                      const int* d_sr_ptr, const int* d_sr_src, int64_t sr_nnz,
-                     const double2* d_sigma_r, const int64_t* d_sl_pos, const int* d_sl_ptr,
-                     const int* d_sl_src, int64_t sl_nnz, const double2* d_sigma_l, cudaStream_t s,
-                     int64_t& launches) {
+                     const double2* d_sigma_r, cudaStream_t s, int64_t& launches) {
   const int nreg = static_cast<int>(p.init_zero.size());
   dim3 g1(std::max(1, std::min(nreg, 1024)), b.nE);
   k_init<<<g1, 256, 0, s>>>(b.arena, b.stride, d_init_zero, nreg);
@@ -1433,10 +1431,9 @@ void launch_assemble(const BatchArgs& b, const Plan& p, const int64_t* d_h_pos, 
     ++launches;
   }
   const int sr_slots = static_cast<int>(p.sr_slot_pos.size());
-  const int sl_slots = static_cast<int>(p.sl_slot_pos.size());
-  dim3 g2(grid_for(std::max<int64_t>(p.desc.n, sl_slots), 256, 1024), b.nE);
-  k_scatter<<<g2, 256, 0, s>>>(b.arena, b.stride, p.desc.n, d_diag_pos, d_energies, d_sl_pos, d_sl_ptr,
-                               d_sl_src, sl_slots, sl_nnz, d_sigma_l);
+  dim3 g2(grid_for(p.desc.n, 256, 1024), b.nE);
+  k_scatter<<<g2, 256, 0, s>>>(b.arena, b.stride, p.desc.n, d_diag_pos, d_energies, nullptr, nullptr, nullptr, 0,
+                               0, nullptr);
   launches += 2;
   if (sr_slots > 0) {
     dim3 g3(grid_for(sr_slots, 256, 1024), b.nE);
@@ -1444,6 +1441,20 @@ void launch_assemble(const BatchArgs& b, const Plan& p, const int64_t* d_h_pos, 
                                          sr_nnz, d_sigma_r);
     ++launches;
   }
+}
+
+// Sigma^< slots into the seed blocks (zeroed by k_init): launched right before
+// the plan's first reader (Plan::lesser_op), so a host-buffer solve can copy
+// Sigma^< in while the fold and the G^r sweep run.
+void launch_scatter_lesser(const BatchArgs& b, const Plan& p, const double* d_energies, const int64_t* d_sl_pos,
+                           const int* d_sl_ptr, const int* d_sl_src, int64_t sl_nnz, const double2* d_sigma_l,
+                           cudaStream_t s, int64_t& launches) {
+  const int sl_slots = static_cast<int>(p.sl_slot_pos.size());
+  if (sl_slots <= 0) return;
+  dim3 g2(grid_for(sl_slots, 256, 1024), b.nE);
+  k_scatter<<<g2, 256, 0, s>>>(b.arena, b.stride, 0, nullptr, d_energies, d_sl_pos, d_sl_ptr, d_sl_src, sl_slots,
+                               sl_nnz, d_sigma_l);
+  ++launches;
 }
 
 // RGF elementwise steps.  skew_half (dense.cpp:136-170): upper triangle of
@@ -1664,6 +1675,22 @@ void launch_skew_check(const BatchArgs& b, const double2* d_sigma_l, int64_t sl_
   const int tot = n_seeded * b.nE;
   k_skew_flag<<<(tot + 255) / 256, 256, 0, s>>>(d_acc, n_seeded, d_seeded_ids, b.nE, b.e_base, st);
   launches += 2;
+}
+
+// G^r diagonal only (Plan::gr_done_op on): lets its device-to-host copy
+// overlap the G^< sweep.
+__global__ void k_output_gr(const double2* __restrict__ arena, int64_t stride, int nE, int n,
+                            const int64_t* __restrict__ gr_pos, double2* gr) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const int64_t pr = gr_pos[d];
+  for (int e = 0; e < nE; ++e) gr[int64_t(e) * n + d] = arena[int64_t(e) * stride + pr];
+}
+
+void launch_output_gr(const BatchArgs& b, int n, const int64_t* d_gr_pos, double2* d_gr, cudaStream_t s,
+                      int64_t& launches) {
+  k_output_gr<<<(n + 255) / 256, 256, 0, s>>>(b.arena, b.stride, b.nE, n, d_gr_pos, d_gr);
+  ++launches;
 }
 
 void launch_output(const BatchArgs& b, int n, const int64_t* d_gr_pos, const int64_t* d_gl_pos,

@@ -26,9 +26,10 @@ struct BatchArgs {
 void launch_assemble(const BatchArgs& b, const Plan& p, const int64_t* d_h_pos, const double2* d_h_val,
                      const InitRegion* d_init_zero, const int64_t* d_diag_pos, const double* d_energies,
                      const int64_t* d_sr_pos, const int* d_sr_ptr, const int* d_sr_src,
-                     int64_t sr_nnz, const double2* d_sigma_r, const int64_t* d_sl_pos,
-                     const int* d_sl_ptr, const int* d_sl_src, int64_t sl_nnz,
-                     const double2* d_sigma_l, cudaStream_t s, int64_t& launches);
+                     int64_t sr_nnz, const double2* d_sigma_r, cudaStream_t s, int64_t& launches);
+void launch_scatter_lesser(const BatchArgs& b, const Plan& p, const double* d_energies, const int64_t* d_sl_pos,
+                           const int* d_sl_ptr, const int* d_sl_src, int64_t sl_nnz, const double2* d_sigma_l,
+                           cudaStream_t s, int64_t& launches);
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
                     DevStatus* st, cudaStream_t s, int64_t& launches);
 void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0,
@@ -51,6 +52,8 @@ void launch_skew(const BatchArgs& b, const SkewTask* d_tasks, const SkewTask* h_
 void launch_combine(const BatchArgs& b, const CombineTask* d_tasks, const CombineTask* h_tasks, int begin, int count,
                     cudaStream_t s, int64_t& launches);
 void launch_ordered_sum(const double* parts, int nranks, int n, double* out, cudaStream_t s, int64_t& launches);
+void launch_output_gr(const BatchArgs& b, int n, const int64_t* d_gr_pos, double2* d_gr, cudaStream_t s,
+                      int64_t& launches);
 void launch_output(const BatchArgs& b, int n, const int64_t* d_gr_pos, const int64_t* d_gl_pos,
                    const double* d_weights, double2* d_gr, double2* d_gl, double* d_density,
                    DevStatus* st, cudaStream_t s, int64_t& launches);

@@ -943,6 +943,15 @@ Plan build_plan(ProblemDesc desc) {
       }
     }
   }
+  // seeds (phase 2) are the first readers of the Sigma^< slots; phases >= 2
+  // never write G^r blocks
+  P.lesser_op = static_cast<int>(P.ops.size());
+  for (std::size_t i = 0; i < P.ops.size(); ++i)
+    if (P.ops[i].phase >= 2) {
+      P.lesser_op = static_cast<int>(i);
+      break;
+    }
+  P.gr_done_op = P.lesser_op;
   return P;
 }
 
@@ -1316,6 +1325,8 @@ Plan build_rgf_plan(ProblemDesc desc, std::vector<std::vector<int>> layers) {
   P.max_block = R.max_layer;
   for (int l = 0; l < L; ++l) P.exec_inv_cmul += double(nl[l]) * nl[l] * nl[l];
   P.rgf_layers = std::move(layers);
+  P.lesser_op = P.rgf_gr_ops;
+  P.gr_done_op = static_cast<int>(P.ops.size());
   return P;
 }
 

@@ -233,6 +233,10 @@ struct Plan {
   std::vector<Op> ops;
   std::vector<std::vector<int>> rgf_layers;  // non-empty: an RGF plan (no tree)
   int rgf_gr_ops = 0;                        // ops [0, rgf_gr_ops) = rgf_gr
+  // Replay split points (host-buffer solves overlap copies with compute):
+  // ops before lesser_op never read the Sigma^< slots; G^r output entries are
+  // final once ops [0, gr_done_op) ran.
+  int lesser_op = 0, gr_done_op = 0;
 
   Ledger ref_fold, ref_gless;   // reference ledger per energy (hsc_fold / hsc_gless)
   double exec_cmul = 0.0;       // executed complex MACs per energy (incl. inversions m^3)
