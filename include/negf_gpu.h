@@ -117,6 +117,10 @@ int negf_plan_fill(const negf_plan* p, int32_t* ptr, int32_t* ids);
  * n_gemm_tasks entries (negf_plan_info); any pointer may be NULL. */
 int negf_plan_gemm_tasks(const negf_plan* p, int32_t* m, int32_t* n, int64_t* k_total, int32_t* phase,
                          int32_t* level);
+/* CTA tiles of the grouped-GEMM launches (introspection): task index, tile
+ * origin and warp arrangement (0: 32x32, 1: 16x64, 2: 64x16), n_gemm_tiles
+ * entries; any pointer may be NULL. */
+int negf_plan_gemm_tiles(const negf_plan* p, int32_t* task, int32_t* m0, int32_t* n0, int32_t* arr);
 void negf_plan_destroy(negf_plan* p);
 
 /* Layered RGF plan: rgf_gr + rgf_gless

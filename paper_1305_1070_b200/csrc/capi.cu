@@ -471,6 +471,19 @@ int negf_plan_gemm_tasks(const negf_plan* h, int32_t* m, int32_t* n, int64_t* k_
   return NEGF_OK;
 }
 
+int negf_plan_gemm_tiles(const negf_plan* h, int32_t* task, int32_t* m0, int32_t* n0, int32_t* arr) {
+  if (!h) return NEGF_CONTRACT_VIOLATION;
+  const Plan& P = h->plan;
+  for (std::size_t i = 0; i < P.gemm_tiles.size(); ++i) {
+    const GemmTile& t = P.gemm_tiles[i];
+    if (task) task[i] = t.task;
+    if (m0) m0[i] = t.m0;
+    if (n0) n0[i] = t.n0;
+    if (arr) arr[i] = t.arr;
+  }
+  return NEGF_OK;
+}
+
 void negf_plan_destroy(negf_plan* p) { delete p; }
 
 int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_gpu** out,

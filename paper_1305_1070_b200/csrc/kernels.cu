@@ -1038,47 +1038,58 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// Stage one K-chunk of op(A) (TM x KC) and op(B) (KC x TN) in the layout of
-// their global source (row- or k-contiguous); zero-fill outside the task.
-template <int WR, int WC>
-__device__ __forceinline__ void load_chunk(double2* st, const double2* base, const GemmTerm& tm, int k0, int m,
-                                           int n, int m0, int n0) {
-  using A = Arr<WR, WC>;
-  double2* As = st;
-  double2* Bs = st + A::OPA;
-  const int tid = threadIdx.x;
-  const int k = tm.k;
-  if (tm.a_op == OP_N) {
-#pragma unroll
-    for (int i = 0; i < (A::TM * KC) / 128; ++i) {
-      const int idx = tid + i * 128, r = idx / KC, kk = idx % KC;
-      const bool v = (m0 + r < m) && (k0 + kk < k);
-      cp_async16(As + r * LD_RK + kk, v ? base + tm.a_off + int64_t(m0 + r) * tm.lda + (k0 + kk) : base, v);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < (A::TM * KC) / 128; ++i) {
-      const int idx = tid + i * 128, kk = idx / A::TM, r = idx % A::TM;
-      const bool v = (m0 + r < m) && (k0 + kk < k);
-      cp_async16(As + kk * A::LDA_KR + r, v ? base + tm.a_off + int64_t(k0 + kk) * tm.lda + (m0 + r) : base, v);
-    }
-  }
-  if (tm.b_op == OP_N || tm.b_op == OP_C) {
-#pragma unroll
-    for (int i = 0; i < (A::TN * KC) / 128; ++i) {
-      const int idx = tid + i * 128, kk = idx / A::TN, c = idx % A::TN;
-      const bool v = (n0 + c < n) && (k0 + kk < k);
-      cp_async16(Bs + kk * A::LDB_KR + c, v ? base + tm.b_off + int64_t(k0 + kk) * tm.ldb + (n0 + c) : base, v);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < (A::TN * KC) / 128; ++i) {
-      const int idx = tid + i * 128, c = idx / KC, kk = idx % KC;
-      const bool v = (n0 + c < n) && (k0 + kk < k);
-      cp_async16(Bs + c * LD_RK + kk, v ? base + tm.b_off + int64_t(n0 + c) * tm.ldb + (k0 + kk) : base, v);
+// Per-thread chunk loader with the addressing hoisted to term changes: a
+// thread's slots of one operand are a fixed stride apart in global memory and
+// in shared memory, so a chunk costs one base add, a k-validity test and one
+// cp.async per slot (the element-wise index arithmetic ran per chunk before).
+// Slot i of thread tid covers element idx = tid + 128 i of the chunk: (row, k)
+// layouts r = idx / KC, kk = idx % KC; (k, row) layouts kk = idx / T,
+// r = idx % T.  Elements outside the task or the term are zero-filled.
+template <int T, int LDKR>
+struct OperandLoader {
+  static constexpr int NS = (T * KC) / 128;  // slots per thread
+  const double2* src;  // slot 0 source at k0 = 0
+  int kmul;            // source advance per unit of k0 (1 for (row, k), ld for (k, row))
+  int gstep;           // source stride between slots (elements)
+  int live;            // (row, k): slots with a live row; (k, row): NS if the row is live, else 0
+  bool rk;
+
+  __device__ __forceinline__ void setup(const double2* base, int64_t off, int ld, bool row_k, int tk_rows, int r0) {
+    const int tid = threadIdx.x;
+    rk = row_k;
+    if (row_k) {
+      const int r = tid / KC, kk = tid % KC;
+      src = base + off + int64_t(r0 + r) * ld + kk;
+      kmul = 1;
+      gstep = (128 / KC) * ld;
+      live = max(0, min(NS, (tk_rows - r0 - r + (128 / KC) - 1) / (128 / KC)));
+    } else {
+      const int kk = tid / T, r = tid % T;
+      src = base + off + int64_t(kk) * ld + (r0 + r);
+      kmul = ld;
+      gstep = (128 / T) * ld;
+      live = (r0 + r < tk_rows) ? NS : 0;
     }
   }
-}
+  __device__ __forceinline__ void issue(double2* sm, const double2* dummy, int k0, int k) const {
+    const int tid = threadIdx.x;
+    const double2* p = src + int64_t(k0) * kmul;
+    // (row, k): one k per thread, all slots live in k together;
+    // (k, row): slot i sits at k = kk + i * (128 / T).
+    const int kk = rk ? tid % KC : tid / T;
+    const int kks = rk ? 0 : 128 / T;
+    const int krem = k - k0 - kk;
+    double2* d = sm + (rk ? (tid / KC) * LD_RK + kk : kk * LDKR + tid % T);
+    const int sstep = rk ? (128 / KC) * LD_RK : (128 / T) * LDKR;
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+      const bool v = (i < live) && (i * kks < krem);
+      cp_async16(d, v ? p : dummy, v);
+      p += gstep;
+      d += sstep;
+    }
+  }
+};
 
 constexpr int kTermCache = 48;  // term descriptors staged in shared memory per item
 
@@ -1110,11 +1121,33 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
       for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = p3[i][j][q] = 0.0;
 
   // Flattened (term, k-chunk) sequence through a 2-stage cp.async ring, one
-  // barrier per chunk.
+  // barrier per chunk.  The loader is re-based only when the term changes.
   const int tend = tk.term_begin + tk.term_count;
   int lt = tk.term_begin, lk0 = 0;
   while (lt < tend && terms[lt].k <= 0) ++lt;
   int ct = lt, ck0 = 0;
+  OperandLoader<A::TM, A::LDA_KR> la;
+  OperandLoader<A::TN, A::LDB_KR> lb;
+  int lk = 0;
+  auto setup = [&](int term) {
+    const GemmTerm& q = terms[term];
+    la.setup(base, q.a_off, q.lda, q.a_op == OP_N, tk.m, tl.m0);
+    lb.setup(base, q.b_off, q.ldb, !(q.b_op == OP_N || q.b_op == OP_C), tk.n, tl.n0);
+    lk = q.k;
+  };
+  auto load = [&](double2* st) {
+    la.issue(st, base, lk0, lk);
+    lb.issue(st + A::OPA, base, lk0, lk);
+  };
+  auto advance_load = [&]() {
+    lk0 += KC;
+    if (lk0 >= lk) {
+      lk0 = 0;
+      ++lt;
+      while (lt < tend && terms[lt].k <= 0) ++lt;
+      if (lt < tend) setup(lt);
+    }
+  };
   auto advance = [&](int& term, int& kq) {
     kq += KC;
     if (kq >= terms[term].k) {
@@ -1124,8 +1157,9 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
     }
   };
   if (lt < tend) {
-    load_chunk<WR, WC>(smem, base, terms[lt], lk0, tk.m, tk.n, tl.m0, tl.n0);
-    advance(lt, lk0);
+    setup(lt);
+    load(smem);
+    advance_load();
   }
   cp_async_commit();
   int stage = 0;
@@ -1133,8 +1167,8 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
     cp_async_wait<0>();
     __syncthreads();
     if (lt < tend) {
-      load_chunk<WR, WC>(smem + (stage ^ 1) * A::STAGE, base, terms[lt], lk0, tk.m, tk.n, tl.m0, tl.n0);
-      advance(lt, lk0);
+      load(smem + (stage ^ 1) * A::STAGE);
+      advance_load();
     }
     cp_async_commit();
     const GemmTerm tm = terms[ct];
@@ -1242,37 +1276,6 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         base[tk.dpart_off + int64_t(r) * tk.dpart_ld + c0 / 16] = s;
       }
     }
-  }
-}
-
-// Persistent launch: CTAs stride over (tile, energy) items, energy fastest;
-// tiles of one arrangement are pre-sorted by decreasing cost in the plan.
-template <int WR, int WC>
-__global__ void __launch_bounds__(128) k_gemm(double2* arena, int64_t stride, int nE,
-                                              const GemmTask* __restrict__ tasks,
-                                              const GemmTerm* __restrict__ terms,
-                                              const GemmTile* __restrict__ tiles, int tile_begin,
-                                              int64_t items) {
-  extern __shared__ double2 gsm[];
-  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
-    const int64_t ti = w / nE;
-    const int e = static_cast<int>(w - ti * nE);
-    const GemmTile tl = tiles[tile_begin + ti];
-    const GemmTask tk = tasks[tl.task];
-    // Stage the task's term descriptors in shared memory (read every chunk).
-    GemmTerm* tsm = reinterpret_cast<GemmTerm*>(gsm + 2 * Arr<WR, WC>::STAGE);
-    const GemmTerm* tp = terms;
-    if (tk.term_count <= kTermCache) {
-      const int2* src = reinterpret_cast<const int2*>(terms + tk.term_begin);
-      int2* dst = reinterpret_cast<int2*>(tsm);
-      constexpr int W = sizeof(GemmTerm) / 8;
-      static_assert(sizeof(GemmTerm) % 8 == 0, "term copy granule");
-      for (int q = threadIdx.x; q < tk.term_count * W; q += blockDim.x) dst[q] = src[q];
-      __syncthreads();
-      tp = tsm - tk.term_begin;
-    }
-    gemm_item<WR, WC>(arena + e * stride, tk, tp, tl, gsm);
-    __syncthreads();
   }
 }
 
@@ -1586,26 +1589,6 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
   }
 }
 
-template <int WR, int WC>
-static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
-                            const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
-  constexpr size_t smem = sizeof(double2) * 2 * Arr<WR, WC>::STAGE + sizeof(GemmTerm) * kTermCache;
-  static int slots_of[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int& slots = slots_of[dev & 63];
-  if (!slots) {
-    int sms = 0, per_sm = 0;
-    cudaFuncSetAttribute(k_gemm<WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm<WR, WC>, 128, smem);
-    slots = std::max(1, sms * std::max(1, per_sm));
-  }
-  const int64_t items = int64_t(tile_count) * b.nE;
-  const int grid = static_cast<int>(std::min<int64_t>(items, slots));
-  k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
-}
-
 void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0,
                      DevStatus* st, cudaStream_t s, int64_t& launches) {
   if (count <= 0) return;
@@ -1630,6 +1613,56 @@ void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h
   ++launches;
 }
 
+// Persistent launch: CTAs stride over (tile, energy) items, energy fastest;
+// one launch per warp arrangement of an op (a task may mix arrangements,
+// plan.cpp tile_task); tiles pre-sorted by decreasing cost in the plan.
+template <int WR, int WC>
+__global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride, int nE,
+                                                     const GemmTask* __restrict__ tasks,
+                                                     const GemmTerm* __restrict__ terms,
+                                                     const GemmTile* __restrict__ tiles, int tile_begin,
+                                                     int64_t items) {
+  extern __shared__ double2 gsm[];
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    const int64_t ti = w / nE;
+    const int e = static_cast<int>(w - ti * nE);
+    const GemmTile tl = tiles[tile_begin + ti];
+    const GemmTask tk = tasks[tl.task];
+    // Stage the task's term descriptors in shared memory (read every chunk).
+    GemmTerm* tsm = reinterpret_cast<GemmTerm*>(gsm + 2 * Arr<WR, WC>::STAGE);
+    const GemmTerm* tp = terms;
+    if (tk.term_count <= kTermCache) {
+      const int2* src = reinterpret_cast<const int2*>(terms + tk.term_begin);
+      int2* dst = reinterpret_cast<int2*>(tsm);
+      constexpr int W = sizeof(GemmTerm) / 8;
+      static_assert(sizeof(GemmTerm) % 8 == 0, "term copy granule");
+      for (int q = threadIdx.x; q < tk.term_count * W; q += blockDim.x) dst[q] = src[q];
+      __syncthreads();
+      tp = tsm - tk.term_begin;
+    }
+    gemm_item<WR, WC>(arena + e * stride, tk, tp, tl, gsm);
+    __syncthreads();
+  }
+}
+template <int WR, int WC>
+static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
+                            const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
+  constexpr size_t smem = sizeof(double2) * 2 * Arr<WR, WC>::STAGE + sizeof(GemmTerm) * kTermCache;
+  static int slots_of[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& slots = slots_of[dev & 63];
+  if (!slots) {
+    int sms = 0, per_sm = 0;
+    cudaFuncSetAttribute(k_gemm<WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm<WR, WC>, 128, smem);
+    slots = std::max(1, sms * std::max(1, per_sm));
+  }
+  const int64_t items = int64_t(tile_count) * b.nE;
+  const int grid = static_cast<int>(std::min<int64_t>(items, slots));
+  k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
+}
 void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                  const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
                  cudaStream_t s, int64_t& launches) {

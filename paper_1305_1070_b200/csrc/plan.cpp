@@ -2,6 +2,8 @@
 // given inline; all of this runs once per device, never per energy.
 #include "plan.hpp"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <map>
 #include <numeric>
@@ -105,6 +107,7 @@ struct Builder {
         const int64_t lm = std::min(kArrTM[tl.arr], tk.m - tl.m0), ln = std::min(kArrTN[tl.arr], tk.n - tl.n0);
         return ((lm + 7) / 8) * ((ln + 7) / 8) * (ks + 16);
       };
+      // one launch per op (tiles carry their arrangement), longest first
       // grouped by arrangement (one launch each), longest first within one
       std::stable_sort(P.gemm_tiles.begin() + cur.begin, P.gemm_tiles.end(),
                        [&](const GemmTile& a, const GemmTile& b) {
@@ -148,19 +151,7 @@ struct Builder {
     P.gemm_tasks.push_back(tk);
     for (int t2 = tk.term_begin; t2 < tk.term_begin + tk.term_count; ++t2)
       cur.cmul += static_cast<double>(m) * n * P.gemm_terms[t2].k;
-    // Warp arrangement with the fewest live-warp slots (each warp owns a
-    // 16x16 region); ties prefer the square 2x2 CTA.
-    int best = 0;
-    int64_t best_slots = -1;
-    for (int a : {0, 1, 2}) {
-      const int64_t slots = int64_t((m + kArrTM[a] - 1) / kArrTM[a]) * ((n + kArrTN[a] - 1) / kArrTN[a]) * 4;
-      if (best_slots < 0 || slots < best_slots) {
-        best_slots = slots;
-        best = a;
-      }
-    }
-    for (int m0 = 0; m0 < m; m0 += kArrTM[best])
-      for (int n0 = 0; n0 < n; n0 += kArrTN[best]) P.gemm_tiles.push_back(GemmTile{id, m0, n0, best});
+    tile_task(id, m, n, P.gemm_tiles);
   }
 
   // Inverses of one group: shared-memory kernels by size class, then the
@@ -234,6 +225,89 @@ struct Builder {
 };
 
 }  // namespace
+
+namespace {
+// Tile cost in units of one full 32x32 tile-chunk: kTileFixed for issuing
+// and synchronising the chunk regardless of content, the rest per live 8x8
+// subtile (16 per tile).  Measured with tools/gemm_bench: an 8x8 live tile
+// costs 0.40 of a full one.
+constexpr double kTileFixed = 0.36;
+double tile_cost(int arr, int m, int n, int m0, int n0) {
+  const int wr = arr == 1 ? 1 : arr == 2 ? 4 : 2, wc = 4 / wr;
+  int live = 0;
+  for (int a = 0; a < wr; ++a)
+    for (int b = 0; b < wc; ++b) {
+      const int li = std::min(2, std::max(0, (m - m0 - 16 * a + 7) / 8));
+      const int lj = std::min(2, std::max(0, (n - n0 - 16 * b + 7) / 8));
+      live += li * lj;
+    }
+  return kTileFixed + (1.0 - kTileFixed) * live / 16.0;
+}
+// Tiles of arrangement `arr` over rows [r0, r1) x cols [c0, c1) of an m x n task.
+double grid_tiles(int arr, int m, int n, int r0, int r1, int c0, int c1, int task, std::vector<GemmTile>* out) {
+  double cost = 0.0;
+  for (int y = r0; y < r1; y += kArrTM[arr])
+    for (int x = c0; x < c1; x += kArrTN[arr]) {
+      cost += tile_cost(arr, std::min(m, r1), std::min(n, c1), y, x);
+      if (out) out->push_back(GemmTile{task, y, x, arr});
+    }
+  return cost;
+}
+}  // namespace
+
+void tile_task(int task, int m, int n, std::vector<GemmTile>& out) {
+  static const bool uniform_only = getenv("NEGF_TILE_UNIFORM") != nullptr;  // A/B experiments
+  // Uniform grids.
+  int best_arr = 0;
+  double best = -1.0;
+  for (int a : {0, 1, 2}) {
+    const double c = grid_tiles(a, m, n, 0, m, 0, n, task, nullptr);
+    if (best < 0 || c < best - 1e-9) {
+      best = c;
+      best_arr = a;
+    }
+  }
+  // 32x32 core + remainder strips.
+  const int M32 = (m / 32) * 32, N32 = (n / 32) * 32;
+  int bot_arr = -1, rgt_arr = -1;
+  double mixed = -1.0;
+  if ((M32 > 0 || N32 > 0) && (M32 < m || N32 < n)) {
+    mixed = grid_tiles(0, m, n, 0, M32, 0, N32, task, nullptr);
+    if (M32 < m) {  // bottom strip, full width
+      double bc = -1.0;
+      for (int a : {0, 1}) {
+        const double c = grid_tiles(a, m, n, M32, m, 0, n, task, nullptr);
+        if (bc < 0 || c < bc - 1e-9) { bc = c; bot_arr = a; }
+      }
+      mixed += bc;
+    }
+    if (N32 < n && M32 > 0) {  // right strip above the bottom strip
+      // 64x16 tiles must not reach into the bottom strip (MODE_ADD tasks
+      // may not compute an entry twice): a 32-row remainder takes 32x32.
+      const int M64 = (M32 / 64) * 64;
+      const double c0 = grid_tiles(0, M32, n, 0, M32, N32, n, task, nullptr);
+      const double c2 = grid_tiles(2, M32, n, 0, M64, N32, n, task, nullptr) +
+                        grid_tiles(0, M32, n, M64, M32, N32, n, task, nullptr);
+      rgt_arr = c2 < c0 - 1e-9 ? 2 : 0;
+      mixed += std::min(c0, c2);
+    }
+  }
+  if (!uniform_only && mixed >= 0 && mixed < best - 1e-9) {
+    grid_tiles(0, m, n, 0, M32, 0, N32, task, &out);
+    if (M32 < m) grid_tiles(bot_arr, m, n, M32, m, 0, n, task, &out);
+    if (N32 < n && M32 > 0) {
+      if (rgt_arr == 2) {
+        const int M64 = (M32 / 64) * 64;
+        grid_tiles(2, M32, n, 0, M64, N32, n, task, &out);
+        grid_tiles(0, M32, n, M64, M32, N32, n, task, &out);
+      } else {
+        grid_tiles(0, M32, n, 0, M32, N32, n, task, &out);
+      }
+    }
+  } else {
+    grid_tiles(best_arr, m, n, 0, m, 0, n, task, &out);
+  }
+}
 
 Plan build_plan(ProblemDesc desc) {
   Plan P;

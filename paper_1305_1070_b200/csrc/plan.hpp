@@ -249,6 +249,14 @@ constexpr int kSmemInvMax = 112;  // largest block inverted wholly in shared mem
 constexpr int kArrTM[3] = {32, 16, 64};
 constexpr int kArrTN[3] = {32, 64, 16};
 
+// Cover an m x n output block with CTA tiles (appended to `out`).  The
+// candidates are the three uniform grids and a 32x32 core with its bottom /
+// right remainder strips covered by 32x32, 16x64 or 64x16 tiles; the
+// cheapest under the measured tile cost model (a fixed part per tile-chunk
+// plus a part proportional to the live 8x8 DMMA subtiles; tools/gemm_bench)
+// wins.
+void tile_task(int task, int m, int n, std::vector<GemmTile>& out);
+
 Plan build_plan(ProblemDesc desc);
 
 // Batched energy-doubling decimation of one dense lead, the restatement of

@@ -172,6 +172,7 @@ def _load() -> C.CDLL:
         "negf_plan_tree": ([vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_fill": ([vp, vp, vp], i32),
         "negf_plan_gemm_tasks": ([vp, vp, vp, vp, vp, vp], i32),
+        "negf_plan_gemm_tiles": ([vp, vp, vp, vp, vp], i32),
         "negf_plan_destroy": ([vp], None),
         "negf_rgf_plan_create": ([C.POINTER(_Problem), i32, vp, vp, C.POINTER(vp), st], i32),
         "negf_gpu_create": ([vp, i32, i32, C.POINTER(vp), st], i32),
@@ -218,7 +219,7 @@ def _load() -> C.CDLL:
 
 _lib = _load()
 ABI_SYMBOLS = (
-    "negf_rgf_plan_create negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_gemm_tasks negf_plan_destroy "
+    "negf_rgf_plan_create negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_gemm_tasks negf_plan_gemm_tiles negf_plan_destroy "
     "negf_gpu_create negf_gpu_batch_capacity negf_gpu_solve_batch negf_gpu_solve_batch_device "
     "negf_gpu_check negf_gpu_density negf_gpu_stream negf_gpu_density_device "
     "negf_gpu_last_launches negf_gpu_destroy negf_nccl_unique_id negf_gpu_nccl_init "
@@ -444,6 +445,13 @@ class HscPlan:
         out = {k: np.zeros(t, np.int64 if k == "k" else np.int32) for k in ("m", "n", "k", "phase", "level")}
         _lib.negf_plan_gemm_tasks(self._h, _ptr(out["m"]), _ptr(out["n"]), _ptr(out["k"]), _ptr(out["phase"]),
                                   _ptr(out["level"]))
+        return out
+
+    def gemm_tiles(self) -> dict:
+        """CTA tiles of the grouped-GEMM launches: task, m0, n0, arrangement."""
+        t = self.info().n_gemm_tiles
+        out = {k: np.zeros(t, np.int32) for k in ("task", "m0", "n0", "arr")}
+        _lib.negf_plan_gemm_tiles(self._h, _ptr(out["task"]), _ptr(out["m0"]), _ptr(out["n0"]), _ptr(out["arr"]))
         return out
 
     def fill_sets(self) -> list:

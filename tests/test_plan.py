@@ -120,3 +120,31 @@ def test_gpu_handle_fails_loudly_without_device():
     rp, prob, _, _ = load_golden("syn_5x6_s24")
     with pytest.raises(negf.CudaError):
         negf.HscGpuSolver(negf.HscPlan(prob))
+
+
+def _check_tiles_cover_exactly(plan):
+    tk = plan.gemm_tasks()
+    tl = plan.gemm_tiles()
+    tm = np.array([32, 16, 64])
+    tn = np.array([32, 64, 16])
+    cover = [np.zeros((int(m), int(n)), np.int32) for m, n in zip(tk["m"], tk["n"])]
+    for t, m0, n0, a in zip(tl["task"], tl["m0"], tl["n0"], tl["arr"]):
+        c = cover[t]
+        c[m0 : m0 + tm[a], n0 : n0 + tn[a]] += 1  # numpy clips at the task edge
+    for t, c in enumerate(cover):
+        assert c.min() == 1 and c.max() == 1, f"task {t} ({c.shape}) covered {c.min()}..{c.max()} times"
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_gemm_tiles_cover_every_task_exactly_once(name):
+    """Mixed 32x32 / 16x64 / 64x16 tiling: every output entry of every grouped
+    GEMM task is computed by exactly one CTA tile (accumulating tasks would
+    double-add otherwise)."""
+    _, prob, _, _ = load_golden(name)
+    _check_tiles_cover_exactly(negf.HscPlan(prob))
+
+
+def test_gemm_tiles_cover_config2_exactly_once():
+    from paper_1305_1070_b200 import devices
+
+    _check_tiles_cover_exactly(negf.HscPlan(devices.config2(n_energies=2).problem))

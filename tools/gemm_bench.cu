@@ -1,12 +1,16 @@
 // Micro-benchmark of the grouped complex GEMM kernel on uniform tasks:
-//   gemm_bench M N K tasks energies
+//   gemm_bench M N K tasks energies [opa opb kterm arr]   (arr 3: the plan's mixed tiling)
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude tools/gemm_bench.cu \
+//        paper_1305_1070_b200/csrc/plan.cpp paper_1305_1070_b200/csrc/tree.cpp -o tools/gemm_bench
 // Every task: C (M x N) = A (M x K) * B (K x N), one term, per energy arena.
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
 #include <algorithm>
+#include <cmath>
 
 #include "../paper_1305_1070_b200/csrc/kernels.cu"
+#include "../paper_1305_1070_b200/csrc/plan.hpp"
 
 using namespace negfb;
 
@@ -45,8 +49,12 @@ int main(int argc, char** argv) {
     tk.term_begin = tb;
     tk.term_count = static_cast<int>(terms.size()) - tb;
     tasks.push_back(tk);
-    for (int m0 = 0; m0 < M; m0 += kArrTM[ARR])
-      for (int n0 = 0; n0 < N; n0 += kArrTN[ARR]) tiles[0].push_back(GemmTile{t, m0, n0, ARR});
+    if (ARR == 3) {
+      tile_task(t, M, N, tiles[0]);  // the plan's mixed tiling
+    } else {
+      for (int m0 = 0; m0 < M; m0 += kArrTM[ARR])
+        for (int n0 = 0; n0 < N; n0 += kArrTN[ARR]) tiles[0].push_back(GemmTile{t, m0, n0, ARR});
+    }
   }
   double2* arena;
   cudaMalloc(&arena, sizeof(double2) * stride * nE);
@@ -85,6 +93,31 @@ int main(int argc, char** argv) {
     }
     printf("M=%d N=%d K=%d T=%d nE=%d ops=%d/%d arr=%d: %.3f ms  %.2f TF/s  (%s)\n", M, N, K, T, nE, opa, opb,
            ARR, best, flops / best / 1e9, cudaGetErrorString(cudaGetLastError()));
+  }
+  // Correctness: task 0..3 of the last energy against a host product.
+  {
+    std::vector<double2> h(stride);
+    cudaMemcpy(h.data(), arena + int64_t(nE - 1) * stride, sizeof(double2) * stride, cudaMemcpyDeviceToHost);
+    double err = 0, mx = 0;
+    for (int t = 0; t < std::min(T, 4); ++t) {
+      const int64_t base = per_task * t;
+      for (int i = 0; i < M; ++i)
+        for (int j = 0; j < N; ++j) {
+          double cr = 0, ci = 0;
+          for (int k = 0; k < K; ++k) {
+            const double2 a = opa == OP_N ? h[base + int64_t(i) * K + k] : h[base + int64_t(k) * M + i];
+            double2 b = (opb == OP_N || opb == OP_C) ? h[base + int64_t(M) * K + int64_t(k) * N + j]
+                                                     : h[base + int64_t(M) * K + int64_t(j) * K + k];
+            if (opb == OP_C || opb == OP_H) b.y = -b.y;
+            cr += a.x * b.x - a.y * b.y;
+            ci += a.x * b.y + a.y * b.x;
+          }
+          const double2 c = h[base + int64_t(M) * K + int64_t(K) * N + int64_t(i) * N + j];
+          err = std::max(err, std::max(std::abs(c.x - cr), std::abs(c.y - ci)));
+          mx = std::max(mx, std::max(std::abs(cr), std::abs(ci)));
+        }
+    }
+    printf("  check: max abs err %.3e (max |C| %.3e) %s\n", err, mx, err <= 1e-12 * std::max(1.0, mx) ? "OK" : "FAIL");
   }
   return 0;
 }
