@@ -177,6 +177,22 @@ def bench_reference(args, rank: int, world: int) -> None:
     }))
 
 
+def level_breakdown(ops, op_ms, energies_timed, steps):
+    """FP64 rate of the GEMM and inverse ops by tree-level class (leaves /
+    small separators / large separators), from per-op CUDA events."""
+    classes = (("leaves (level 1)", 1, 1), ("separators, levels 2-4", 2, 4), ("separators, levels >= 5", 5, 99))
+    out = {}
+    for kname, kinds in (("gemm", (1,)), ("inverse", (0, 4, 5))):
+        for cname, lo, hi in classes:
+            sel = np.isin(ops["kind"], kinds) & (ops["level"] >= lo) & (ops["level"] <= hi)
+            ms = float(op_ms[sel].sum())
+            fl = 8.0 * float(ops["cmul"][sel].sum()) * energies_timed
+            if ms > 0:
+                out[f"{kname}: {cname}"] = {"ms_per_step": ms / steps, "tflops": fl / (ms * 1e-3) / 1e12,
+                                             "frac": fl / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS}
+    return out
+
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -280,7 +296,9 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
     kstats = solver.profile_read(reset=True)
+    op_ms = solver.profile_ops(reset=True)
     solver.profile(False)
+    by_level = level_breakdown(plan.ops(), op_ms, per_rank * args.steps, args.steps)
     clk = clocks.stop()
     solver.check()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -456,7 +474,8 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
                      "kernels": {k: {"ms_per_step": v["ms"] / args.steps,
                                      "tflops": (8.0 * v["cmul"] / (v["ms"] * 1e-3) / 1e12) if v["ms"] > 0 and v["cmul"] > 0 else None,
                                      "launches_per_step": v["launches"] / args.steps}
-                                 for k, v in kstats.items()}},
+                                 for k, v in kstats.items()},
+                     "by_level": by_level},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "e2e_gpu_sigma": {"value": e2g_value, "unit": UNIT, "h2d_bytes_per_step": int(e_h.nbytes + w_h.nbytes),

@@ -121,6 +121,13 @@ int negf_plan_gemm_tasks(const negf_plan* p, int32_t* m, int32_t* n, int64_t* k_
  * origin and warp arrangement (0: 32x32, 1: 16x64, 2: 64x16), n_gemm_tiles
  * entries; any pointer may be NULL. */
 int negf_plan_gemm_tiles(const negf_plan* p, int32_t* task, int32_t* m0, int32_t* n0, int32_t* arr);
+/* The replayed op list (introspection, n_ops entries): kind (0 inverse,
+ * 1 grouped GEMM, 2 diagonal, 3 seed scaling, 4 panel, 5 permutation, ...),
+ * phase (0 fold, 1 G^r, 2 seed, 3 N fold, 4 G^<), tree level, range in the
+ * kind's task (GEMM: tile) array, executed complex MACs per energy; any
+ * pointer may be NULL. */
+int negf_plan_ops(const negf_plan* p, int32_t* kind, int32_t* phase, int32_t* level, int32_t* begin,
+                  int32_t* count, double* cmul);
 void negf_plan_destroy(negf_plan* p);
 
 /* Layered RGF plan: rgf_gr + rgf_gless
@@ -187,6 +194,9 @@ enum { NEGF_KSTAT_GEMM = 0, NEGF_KSTAT_INVERSE = 1, NEGF_KSTAT_DIAG = 2, NEGF_KS
        NEGF_KSTAT_ASSEMBLE = 4, NEGF_KSTAT_OUTPUT = 5, NEGF_KSTAT_COUNT = 6 };
 int negf_gpu_profile(negf_gpu* g, int enable);
 int negf_gpu_profile_read(negf_gpu* g, negf_kernel_stat* out /* [NEGF_KSTAT_COUNT] */, int reset);
+/* Per plan op (negf_plan_ops order): summed CUDA-event milliseconds of the
+ * profiled solves (n_ops entries). */
+int negf_gpu_profile_ops(negf_gpu* g, double* ms_out, int reset);
 void negf_gpu_destroy(negf_gpu* g);
 
 /* NCCL: one communicator per handle, bootstrapped by the caller (e.g. a

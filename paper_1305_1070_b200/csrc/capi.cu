@@ -126,6 +126,7 @@ struct negf_gpu {
   };
   std::vector<Rec> recs;
   negf_kernel_stat stats[NEGF_KSTAT_COUNT] = {};
+  std::vector<double> op_ms;  // per plan op, summed over profiled solves
 };
 
 namespace {
@@ -170,6 +171,10 @@ void flush_profile(negf_gpu* g) {
       std::fprintf(stderr, "[negf-prof] op %3d kind %d phase %d level %2d count %6d ms %9.3f TF/s %7.2f\n",
                    g->recs[r].op, op.kind, op.phase, op.level, op.count, ms,
                    ms > 0 ? 8.0 * g->recs[r].cmul / (ms * 1e-3) / 1e12 : 0.0);
+    }
+    if (g->recs[r].op >= 0) {
+      if (g->op_ms.size() < g->plan->ops.size()) g->op_ms.assign(g->plan->ops.size(), 0.0);
+      g->op_ms[g->recs[r].op] += ms;
     }
     negf_kernel_stat& s = g->stats[g->recs[r].kind];
     s.ms += ms;
@@ -484,6 +489,22 @@ int negf_plan_gemm_tiles(const negf_plan* h, int32_t* task, int32_t* m0, int32_t
   return NEGF_OK;
 }
 
+int negf_plan_ops(const negf_plan* h, int32_t* kind, int32_t* phase, int32_t* level, int32_t* begin,
+                  int32_t* count, double* cmul) {
+  if (!h) return NEGF_CONTRACT_VIOLATION;
+  const Plan& P = h->plan;
+  for (std::size_t i = 0; i < P.ops.size(); ++i) {
+    const Op& o = P.ops[i];
+    if (kind) kind[i] = o.kind;
+    if (phase) phase[i] = o.phase;
+    if (level) level[i] = o.level;
+    if (begin) begin[i] = o.begin;
+    if (count) count[i] = o.count;
+    if (cmul) cmul[i] = o.cmul;
+  }
+  return NEGF_OK;
+}
+
 void negf_plan_destroy(negf_plan* p) { delete p; }
 
 int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_gpu** out,
@@ -696,6 +717,15 @@ int negf_gpu_profile_read(negf_gpu* g, negf_kernel_stat* out, int reset) {
   for (int k = 0; k < NEGF_KSTAT_COUNT; ++k) out[k] = g->stats[k];
   if (reset)
     for (auto& s : g->stats) s = negf_kernel_stat{};
+  return NEGF_OK;
+}
+
+int negf_gpu_profile_ops(negf_gpu* g, double* ms_out, int reset) {
+  if (!g || !ms_out) return NEGF_CONTRACT_VIOLATION;
+  flush_profile(g);
+  const std::size_t n = g->plan->ops.size();
+  for (std::size_t i = 0; i < n; ++i) ms_out[i] = i < g->op_ms.size() ? g->op_ms[i] : 0.0;
+  if (reset) g->op_ms.assign(n, 0.0);
   return NEGF_OK;
 }
 

@@ -173,6 +173,7 @@ def _load() -> C.CDLL:
         "negf_plan_fill": ([vp, vp, vp], i32),
         "negf_plan_gemm_tasks": ([vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_gemm_tiles": ([vp, vp, vp, vp, vp], i32),
+        "negf_plan_ops": ([vp, vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_destroy": ([vp], None),
         "negf_rgf_plan_create": ([C.POINTER(_Problem), i32, vp, vp, C.POINTER(vp), st], i32),
         "negf_gpu_create": ([vp, i32, i32, C.POINTER(vp), st], i32),
@@ -193,6 +194,7 @@ def _load() -> C.CDLL:
         "negf_gpu_set_residual_check": ([vp, i32], i32),
         "negf_gpu_max_real_residual": ([vp], C.c_double),
         "negf_gpu_profile_read": ([vp, vp, i32], i32),
+        "negf_gpu_profile_ops": ([vp, vp, i32], i32),
         "negf_lead_create": ([i32, i32, vp, vp, C.c_double, i32, C.c_double, i32, C.POINTER(vp), st], i32),
         "negf_lead_sigma": ([vp, i32, vp, i32, vp, st], i32),
         "negf_lead_sigma_device": ([vp, i32, vp, i32, vp, i64, st], i32),
@@ -219,11 +221,11 @@ def _load() -> C.CDLL:
 
 _lib = _load()
 ABI_SYMBOLS = (
-    "negf_rgf_plan_create negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_gemm_tasks negf_plan_gemm_tiles negf_plan_destroy "
+    "negf_rgf_plan_create negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_gemm_tasks negf_plan_gemm_tiles negf_plan_ops negf_plan_destroy "
     "negf_gpu_create negf_gpu_batch_capacity negf_gpu_solve_batch negf_gpu_solve_batch_device "
     "negf_gpu_check negf_gpu_density negf_gpu_stream negf_gpu_density_device "
     "negf_gpu_last_launches negf_gpu_destroy negf_nccl_unique_id negf_gpu_nccl_init "
-    "negf_gpu_allreduce_density negf_gpu_set_ordered_reduce negf_gpu_profile negf_gpu_profile_read negf_gpu_set_residual_check "
+    "negf_gpu_allreduce_density negf_gpu_set_ordered_reduce negf_gpu_profile negf_gpu_profile_read negf_gpu_profile_ops negf_gpu_set_residual_check "
     "negf_gpu_max_real_residual negf_lead_create negf_lead_sigma negf_lead_sigma_device negf_lead_last_sweeps "
     "negf_lead_last_launches negf_lead_stream negf_lead_destroy negf_lead_modes_sigma_device "
     "negf_contacts_fill_device negf_format_double negf_write_solve_csv negf_shard_writer_open "
@@ -454,6 +456,14 @@ class HscPlan:
         _lib.negf_plan_gemm_tiles(self._h, _ptr(out["task"]), _ptr(out["m0"]), _ptr(out["n0"]), _ptr(out["arr"]))
         return out
 
+    def ops(self) -> dict:
+        """The replayed op list: kind, phase, level, begin, count, cmul per op."""
+        t = self.info().n_ops
+        out = {k: np.zeros(t, np.int32) for k in ("kind", "phase", "level", "begin", "count")}
+        out["cmul"] = np.zeros(t, np.float64)
+        _lib.negf_plan_ops(self._h, *(_ptr(out[k]) for k in ("kind", "phase", "level", "begin", "count", "cmul")))
+        return out
+
     def fill_sets(self) -> list:
         nc = self.info().n_clusters
         ptr = np.zeros(nc + 1, np.int32)
@@ -601,6 +611,12 @@ class HscGpuSolver:
         _lib.negf_gpu_profile_read(self._h, C.cast(arr, C.c_void_p), int(bool(reset)))
         return {k: {"ms": arr[i].ms, "cmul": arr[i].cmul, "launches": arr[i].launches}
                 for i, k in enumerate(KSTAT_NAMES)}
+
+    def profile_ops(self, reset: bool = False) -> np.ndarray:
+        """Per plan op (HscPlan.ops order): summed CUDA-event ms of the profiled solves."""
+        out = np.zeros(max(self.plan.info().n_ops, 1), np.float64)
+        _lib.negf_gpu_profile_ops(self._h, _ptr(out), int(bool(reset)))
+        return out[: self.plan.info().n_ops]
 
     def nccl_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = C.create_string_buffer(bytes(unique_id), 128)
