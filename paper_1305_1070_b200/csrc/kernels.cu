@@ -1252,7 +1252,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         if (tk.c2_off >= 0) base[tk.c2_off + int64_t(r) * tk.ldc + c] = make_double2(2.0 * v.x, 2.0 * v.y);
         if (tk.dmode) {
           const double2 psi = base[tk.dpsi_off + int64_t(r) * tk.dpsi_ld + c];
-          if (tk.dmode == 2) v.y = -v.y;
+          if (tk.dmode >= 2) v.y = -v.y;
           rs[i] = cadd(rs[i], cmul(psi, v));
         }
       }
@@ -1272,7 +1272,9 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
       for (int i = 0; i < 2; ++i) {
         const int r = tl.m0 + wm + 8 * i + g;
         if (r >= tk.m) continue;
-        const double2 s = tk.dmode == 2 ? make_double2(-rs[i].x, -rs[i].y) : rs[i];
+        // dmode 3: the anti-Hermitian form, imaginary part only (plan.cpp)
+        const double2 s = tk.dmode == 3 ? make_double2(0.0, -rs[i].y)
+                          : tk.dmode == 2 ? make_double2(-rs[i].x, -rs[i].y) : rs[i];
         base[tk.dpart_off + int64_t(r) * tk.dpart_ld + c0 / 16] = s;
       }
     }

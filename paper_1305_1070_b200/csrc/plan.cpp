@@ -895,14 +895,23 @@ Plan build_plan(ProblemDesc desc) {
       B.open(K_GEMM, 4, l);
       for (int x : xs) {
         const ClusterInfo& X = B.I(x);
+        // Symmetric form of a diagonal-only, unseeded P row set:
+        // diag(P_xx) = diag(Psi P_SS Psi^H) with P_SS anti-Hermitian (P_{j,k} =
+        // -P_{k,j}^H, hsc.cpp:204-206), so the (k, j) and (j, k) block pairs sum to
+        // w - conj(w) = 2i Im(w): each pair once from 2 Psi, imaginary part kept
+        // (dmode 3).  The diagonal blocks' own real parts are rounding noise
+        // (G^< is anti-Hermitian), so the whole sum keeps only its imaginary part.
+        const bool psym = !X.full_p && X.off_ppart >= 0 && X.off_psi2 >= 0 && X.ncols.empty() && !X.has_nd;
         for (std::size_t jj = 0; jj < X.pcols.size(); ++jj) {
           const int j = X.pcols[jj];
           const int tb = static_cast<int>(T.size());
           const int np = find_pos(X.ncols, j);
+          const int jpos = find_pos(X.S, j);
           if (np >= 0) B.add_term(T, X.m, OP_N, X.off_d, X.m, OP_N, X.off_nrow + X.ncol_off[np], X.WN, +1);
           for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
             const int k = X.S[kk];
-            const int64_t a = X.off_psi + X.s_col[kk];
+            if (psym && static_cast<int>(kk) > jpos) continue;
+            const int64_t a = (psym && static_cast<int>(kk) < jpos ? X.off_psi2 : X.off_psi) + X.s_col[kk];
             if (k == j) B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N, B.I(j).off_pd, B.msz(j), +1);
             else if (B.lev(k) < B.lev(j))
               B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N,
@@ -916,7 +925,7 @@ Plan build_plan(ProblemDesc desc) {
             for (std::size_t q = 0; q < jj; ++q) gb += (B.msz(X.pcols[q]) + 15) / 16;
             const int kk = find_pos(X.S, j);
             if (kk < 0) fail(kInternal, "plan: diagonal-only row outside the fill set");
-            B.pend_diag.dmode = 2;
+            B.pend_diag.dmode = psym ? 3 : 2;
             B.pend_diag.nostore = 1;
             B.pend_diag.dpsi_off = X.off_psi + X.s_col[static_cast<std::size_t>(kk)];
             B.pend_diag.dpsi_ld = X.K;

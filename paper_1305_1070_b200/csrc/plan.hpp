@@ -63,8 +63,8 @@ struct GemmTask {
   // Fused diagonal (rows of never-referenced clusters, whose G / P rows feed
   // only diag(G_xx) / diag(P_xx)): the epilogue forms, per output row r and
   // 16-column warp group, sum_c Psi[r][c] * op(C[r][c]) (dmode 1: +C, 2:
-  // -conj(C)) into partials[dpart_off + r * dpart_ld + group]; nostore skips
-  // writing C itself.
+  // -conj(C), 3: i Im(-conj(C)) -- the anti-Hermitian symmetric form) into
+  // partials[dpart_off + r * dpart_ld + group]; nostore skips writing C itself.
   int dmode, nostore;
   int dpsi_ld, dpart_ld;
   int64_t dpsi_off, dpart_off;
