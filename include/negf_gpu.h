@@ -118,9 +118,11 @@ int negf_plan_fill(const negf_plan* p, int32_t* ptr, int32_t* ids);
 int negf_plan_gemm_tasks(const negf_plan* p, int32_t* m, int32_t* n, int64_t* k_total, int32_t* phase,
                          int32_t* level);
 /* CTA tiles of the grouped-GEMM launches (introspection): task index, tile
- * origin and warp arrangement (0: 32x32, 1: 16x64, 2: 64x16), n_gemm_tiles
- * entries; any pointer may be NULL. */
-int negf_plan_gemm_tiles(const negf_plan* p, int32_t* task, int32_t* m0, int32_t* n0, int32_t* arr);
+ * origin, warp arrangement (0: 32x32, 1: 16x64, 2: 64x16) and whether the
+ * tile also writes its transpose (symmetric tasks), n_gemm_tiles entries;
+ * any pointer may be NULL. */
+int negf_plan_gemm_tiles(const negf_plan* p, int32_t* task, int32_t* m0, int32_t* n0, int32_t* arr,
+                         int32_t* mirrored);
 /* The replayed op list (introspection, n_ops entries): kind (0 inverse,
  * 1 grouped GEMM, 2 diagonal, 3 seed scaling, 4 panel, 5 permutation, ...),
  * phase (0 fold, 1 G^r, 2 seed, 3 N fold, 4 G^<), tree level, range in the

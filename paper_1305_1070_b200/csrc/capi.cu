@@ -476,7 +476,8 @@ int negf_plan_gemm_tasks(const negf_plan* h, int32_t* m, int32_t* n, int64_t* k_
   return NEGF_OK;
 }
 
-int negf_plan_gemm_tiles(const negf_plan* h, int32_t* task, int32_t* m0, int32_t* n0, int32_t* arr) {
+int negf_plan_gemm_tiles(const negf_plan* h, int32_t* task, int32_t* m0, int32_t* n0, int32_t* arr,
+                         int32_t* mirrored) {
   if (!h) return NEGF_CONTRACT_VIOLATION;
   const Plan& P = h->plan;
   for (std::size_t i = 0; i < P.gemm_tiles.size(); ++i) {
@@ -485,6 +486,7 @@ int negf_plan_gemm_tiles(const negf_plan* h, int32_t* task, int32_t* m0, int32_t
     if (m0) m0[i] = t.m0;
     if (n0) n0[i] = t.n0;
     if (arr) arr[i] = t.arr;
+    if (mirrored) mirrored[i] = (P.gemm_tasks[t.task].mirror && t.n0 > t.m0) ? 1 : 0;
   }
   return NEGF_OK;
 }

@@ -1234,6 +1234,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
   // Epilogue: lane owns C[r][c], C[r][c+1] of each 8x8 subtile.  Fused
   // diagonal (GemmTask::dmode): row sums of Psi[r][c] op(C[r][c]).
   double2 rs[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+  const bool mir = tk.mirror && tl.n0 > tl.m0;  // aligned 32x32 tiles: every entry has c > r
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int r = tl.m0 + wm + 8 * i + g;
@@ -1245,6 +1246,12 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         const int c = tl.n0 + wn + 8 * j + 2 * t + q;
         if (c >= tk.n) continue;
         double2 v = make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
+        if (mir) {  // strictly-upper tile of a symmetric task: the (c, r) entry too
+          double2* d2 = base + tk.c_off + int64_t(c) * tk.ldc + r;
+          if (tk.mode == MODE_ADD) *d2 = cadd(*d2, v);
+          else if (tk.mode == MODE_INIT) *d2 = cadd(base[tk.init_off + int64_t(c) * tk.ld_init + r], v);
+          else *d2 = v;
+        }
         double2* dst = base + tk.c_off + int64_t(r) * tk.ldc + c;
         if (tk.mode == MODE_ADD) v = cadd(*dst, v);
         else if (tk.mode == MODE_INIT) v = cadd(base[tk.init_off + int64_t(r) * tk.ld_init + c], v);

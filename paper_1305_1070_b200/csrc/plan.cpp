@@ -148,10 +148,14 @@ struct Builder {
     tk.term_begin = term_begin;
     tk.term_count = static_cast<int>(P.gemm_terms.size()) - term_begin;
     const int id = static_cast<int>(P.gemm_tasks.size());
+    if (tk.mirror && (m != n || tk.nostore || tk.dmode || tk.c2_off >= 0)) fail(kInternal, "plan: bad mirror task");
     P.gemm_tasks.push_back(tk);
+    // executed work: the entries the tiles compute (a mirrored task computes
+    // its upper triangle of 32x32 tiles)
+    const double area = tk.mirror ? static_cast<double>(tile_task_sym(id, m, P.gemm_tiles))
+                                  : (tile_task(id, m, n, P.gemm_tiles), static_cast<double>(m) * n);
     for (int t2 = tk.term_begin; t2 < tk.term_begin + tk.term_count; ++t2)
-      cur.cmul += static_cast<double>(m) * n * P.gemm_terms[t2].k;
-    tile_task(id, m, n, P.gemm_tiles);
+      cur.cmul += area * P.gemm_terms[t2].k;
   }
 
   // Inverses of one group: shared-memory kernels by size class, then the
@@ -307,6 +311,16 @@ void tile_task(int task, int m, int n, std::vector<GemmTile>& out) {
   } else {
     grid_tiles(best_arr, m, n, 0, m, 0, n, task, &out);
   }
+}
+
+int64_t tile_task_sym(int task, int m, std::vector<GemmTile>& out) {
+  int64_t area = 0;
+  for (int y = 0; y < m; y += 32)
+    for (int x = y; x < m; x += 32) {
+      out.push_back(GemmTile{task, y, x, 0});
+      area += int64_t(std::min(32, m - y)) * std::min(32, m - x);
+    }
+  return area;
 }
 
 Plan build_plan(ProblemDesc desc) {
@@ -713,7 +727,10 @@ Plan build_plan(ProblemDesc desc) {
         const ClusterInfo& X = B.I(c3[0]);
         B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N, X.off_arow + X.s_col[c3[2]], X.K, +1);
       }
-      if (jp == jq) B.gemm_task(J.m, J.m, J.off_d, J.m, MODE_ADD, 0, 0, tb);
+      if (jp == jq) {  // A_jj += sum Psi^T A_{i,j}: complex symmetric
+        B.pend_diag.mirror = 1;
+        B.gemm_task(J.m, J.m, J.off_d, J.m, MODE_ADD, 0, 0, tb);
+      }
       else {
         const int p = find_pos(J.S, jq);
         if (p < 0) fail(kInternal, "plan: fill block missing from S");
@@ -793,6 +810,7 @@ Plan build_plan(ProblemDesc desc) {
       for (std::size_t kk = 0; kk < X.S.size(); ++kk)
         B.add_term(T, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_T,
                    X.off_grow + B.col_of(X.gcols, X.gcol_off, X.S[kk]), X.WG, +1);
+      B.pend_diag.mirror = 1;  // G_xx = inv_x + Psi G_{x,S}^T: complex symmetric
       B.gemm_task(X.m, X.m, X.off_gd, X.m, MODE_INIT, X.off_d, X.m, tb);
     }
     B.close();

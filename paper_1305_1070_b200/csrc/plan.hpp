@@ -67,6 +67,11 @@ struct GemmTask {
   // partials[dpart_off + r * dpart_ld + group]; nostore skips writing C itself.
   int dmode, nostore;
   int dpsi_ld, dpart_ld;
+  // Symmetric output (m == n, C = C^T up to rounding: the Schur update of a
+  // diagonal block, a full G_xx): only 32x32 tiles on or above the diagonal
+  // run; a tile strictly above it also writes its transpose into the lower
+  // triangle with the same mode (ADD / INIT read their own (c, r) entry).
+  int mirror;
   int64_t dpsi_off, dpart_off;
   // Second output 2*C at c2_off (same ldc) when >= 0: the doubled Psi of
   // clusters whose symmetric diagonal quadratic form uses each block pair once.
@@ -256,6 +261,9 @@ constexpr int kArrTN[3] = {32, 64, 16};
 // plus a part proportional to the live 8x8 DMMA subtiles; tools/gemm_bench)
 // wins.
 void tile_task(int task, int m, int n, std::vector<GemmTile>& out);
+// Upper-triangular 32x32 tiles of a symmetric m x m task (GemmTask::mirror);
+// returns the number of output entries the tiles compute.
+int64_t tile_task_sym(int task, int m, std::vector<GemmTile>& out);
 
 Plan build_plan(ProblemDesc desc);
 

@@ -172,7 +172,7 @@ def _load() -> C.CDLL:
         "negf_plan_tree": ([vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_fill": ([vp, vp, vp], i32),
         "negf_plan_gemm_tasks": ([vp, vp, vp, vp, vp, vp], i32),
-        "negf_plan_gemm_tiles": ([vp, vp, vp, vp, vp], i32),
+        "negf_plan_gemm_tiles": ([vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_ops": ([vp, vp, vp, vp, vp, vp, vp], i32),
         "negf_plan_destroy": ([vp], None),
         "negf_rgf_plan_create": ([C.POINTER(_Problem), i32, vp, vp, C.POINTER(vp), st], i32),
@@ -450,10 +450,11 @@ class HscPlan:
         return out
 
     def gemm_tiles(self) -> dict:
-        """CTA tiles of the grouped-GEMM launches: task, m0, n0, arrangement."""
+        """CTA tiles of the grouped-GEMM launches: task, m0, n0, arrangement,
+        mirrored (the tile also writes its transpose: symmetric tasks)."""
         t = self.info().n_gemm_tiles
-        out = {k: np.zeros(t, np.int32) for k in ("task", "m0", "n0", "arr")}
-        _lib.negf_plan_gemm_tiles(self._h, _ptr(out["task"]), _ptr(out["m0"]), _ptr(out["n0"]), _ptr(out["arr"]))
+        out = {k: np.zeros(t, np.int32) for k in ("task", "m0", "n0", "arr", "mirrored")}
+        _lib.negf_plan_gemm_tiles(self._h, *(_ptr(out[k]) for k in ("task", "m0", "n0", "arr", "mirrored")))
         return out
 
     def ops(self) -> dict:

@@ -128,9 +128,12 @@ def _check_tiles_cover_exactly(plan):
     tm = np.array([32, 16, 64])
     tn = np.array([32, 64, 16])
     cover = [np.zeros((int(m), int(n)), np.int32) for m, n in zip(tk["m"], tk["n"])]
-    for t, m0, n0, a in zip(tl["task"], tl["m0"], tl["n0"], tl["arr"]):
+    for t, m0, n0, a, mir in zip(tl["task"], tl["m0"], tl["n0"], tl["arr"], tl["mirrored"]):
         c = cover[t]
         c[m0 : m0 + tm[a], n0 : n0 + tn[a]] += 1  # numpy clips at the task edge
+        if mir:  # a symmetric task's strictly-upper tile writes its transpose too
+            assert c.shape[0] == c.shape[1] and n0 >= m0 + tm[a]
+            c[n0 : n0 + tn[a], m0 : m0 + tm[a]] += 1
     for t, c in enumerate(cover):
         assert c.min() == 1 and c.max() == 1, f"task {t} ({c.shape}) covered {c.min()}..{c.max()} times"
 
