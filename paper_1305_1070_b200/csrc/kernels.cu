@@ -1248,7 +1248,8 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         double2 v = make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
         if (mir) {  // strictly-upper tile of a symmetric task: the (c, r) entry too
           double2* d2 = base + tk.c_off + int64_t(c) * tk.ldc + r;
-          if (tk.mode == MODE_ADD) *d2 = cadd(*d2, v);
+          if (tk.mirror == 2) *d2 = make_double2(-v.x, v.y);  // anti-Hermitian: -conj
+          else if (tk.mode == MODE_ADD) *d2 = cadd(*d2, v);
           else if (tk.mode == MODE_INIT) *d2 = cadd(base[tk.init_off + int64_t(c) * tk.ld_init + r], v);
           else *d2 = v;
         }

@@ -148,7 +148,8 @@ struct Builder {
     tk.term_begin = term_begin;
     tk.term_count = static_cast<int>(P.gemm_terms.size()) - term_begin;
     const int id = static_cast<int>(P.gemm_tasks.size());
-    if (tk.mirror && (m != n || tk.nostore || tk.dmode || tk.c2_off >= 0)) fail(kInternal, "plan: bad mirror task");
+    if (tk.mirror && (m != n || tk.nostore || tk.dmode || tk.c2_off >= 0 || (tk.mirror == 2 && mode != MODE_SET)))
+      fail(kInternal, "plan: bad mirror task");
     P.gemm_tasks.push_back(tk);
     // executed work: the entries the tiles compute (a mirrored task computes
     // its upper triangle of 32x32 tiles)
@@ -963,6 +964,7 @@ Plan build_plan(ProblemDesc desc) {
         for (std::size_t kk = 0; kk < X.S.size(); ++kk)
           B.add_term(T, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_H,
                      X.off_prow + B.col_of(X.pcols, X.pcol_off, X.S[kk]), X.WP, -1);
+        B.pend_diag.mirror = 2;  // P_xx = G^<_xx: anti-Hermitian
         B.gemm_task(X.m, X.m, X.off_pd, X.m, MODE_SET, 0, 0, tb);
       }
       B.close();

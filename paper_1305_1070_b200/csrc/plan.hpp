@@ -67,10 +67,11 @@ struct GemmTask {
   // partials[dpart_off + r * dpart_ld + group]; nostore skips writing C itself.
   int dmode, nostore;
   int dpsi_ld, dpart_ld;
-  // Symmetric output (m == n, C = C^T up to rounding: the Schur update of a
-  // diagonal block, a full G_xx): only 32x32 tiles on or above the diagonal
-  // run; a tile strictly above it also writes its transpose into the lower
-  // triangle with the same mode (ADD / INIT read their own (c, r) entry).
+  // Symmetric output (m == n): only 32x32 tiles on or above the diagonal
+  // run; a tile strictly above it also writes the lower triangle.  mirror 1:
+  // C = C^T up to rounding (the Schur update of a diagonal block, a full
+  // G_xx), written with the task's mode (ADD / INIT read their own (c, r)
+  // entry); mirror 2: C = -C^H (a full P_xx = G^<_xx), MODE_SET only.
   int mirror;
   int64_t dpsi_off, dpart_off;
   // Second output 2*C at c2_off (same ldc) when >= 0: the doubled Psi of
