@@ -1623,6 +1623,35 @@ void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h
   ++launches;
 }
 
+// Sparse leaf Psi (K_SPSI): Psi_x[r][c] = -sum_e inv_x[r][t_e] a_e over the
+// stencil entries of column c of A_{x,S} (ascending t, fixed order); one CTA
+// per (leaf, energy), consecutive threads on consecutive columns of a Psi row
+// (coalesced stores; inv_x is re-read from L1).
+__global__ void __launch_bounds__(256) k_spsi(double2* arena, int64_t stride, const SpsiTask* __restrict__ tasks,
+                                              const int* __restrict__ colptr, const int* __restrict__ rows,
+                                              const double2* __restrict__ vals, int begin) {
+  const SpsiTask tk = tasks[begin + blockIdx.x];
+  double2* base = arena + int64_t(blockIdx.y) * stride;
+  const double2* inv = base + tk.off_inv;
+  const int* cp = colptr + tk.col_begin;
+  const int total = tk.m * tk.K;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int r = idx / tk.K, c = idx - r * tk.K;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int e = cp[c]; e < cp[c + 1]; ++e) acc = cadd(acc, cmul(inv[int64_t(r) * tk.m + rows[e]], vals[e]));
+    const double2 v = make_double2(-acc.x, -acc.y);
+    base[tk.off_psi + idx] = v;
+    if (tk.off_psi2 >= 0) base[tk.off_psi2 + idx] = make_double2(2.0 * v.x, 2.0 * v.y);
+  }
+}
+
+void launch_spsi(const BatchArgs& b, const SpsiTask* d_tasks, const int* d_colptr, const int* d_rows,
+                 const double2* d_vals, int begin, int count, cudaStream_t s, int64_t& launches) {
+  if (count <= 0) return;
+  k_spsi<<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, d_colptr, d_rows, d_vals, begin);
+  ++launches;
+}
+
 // Persistent launch: CTAs stride over (tile, energy) items, energy fastest;
 // one launch per warp arrangement of an op (a task may mix arrangements,
 // plan.cpp tile_task); tiles pre-sorted by decreasing cost in the plan.

@@ -39,6 +39,8 @@ void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h
 void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                  const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
                  cudaStream_t s, int64_t& launches);
+void launch_spsi(const BatchArgs& b, const SpsiTask* d_tasks, const int* d_colptr, const int* d_rows,
+                 const double2* d_vals, int begin, int count, cudaStream_t s, int64_t& launches);
 void launch_diag(const BatchArgs& b, const DiagTask* d_tasks, const GemmTerm* d_terms, int begin,
                  int count, cudaStream_t s, int64_t& launches);
 void launch_scale(const BatchArgs& b, const ScaleTask* d_tasks, int begin, int count,

@@ -2,6 +2,8 @@
 // given inline; all of this runs once per device, never per energy.
 #include "plan.hpp"
 
+#include <limits>
+
 #include <cstdlib>
 
 #include <algorithm>
@@ -82,6 +84,7 @@ struct Builder {
       case K_DIAG: cur.begin = static_cast<int>(P.diag_tasks.size()); break;
       case K_PANEL:
       case K_PERM: cur.begin = static_cast<int>(P.big_tasks.size()); break;
+      case K_SPSI: cur.begin = static_cast<int>(P.spsi_tasks.size()); break;
       default: cur.begin = static_cast<int>(P.scale_tasks.size()); break;
     }
   }
@@ -95,6 +98,7 @@ struct Builder {
       case K_DIAG: cur.count = static_cast<int>(P.diag_tasks.size()) - cur.begin; break;
       case K_PANEL:
       case K_PERM: cur.count = static_cast<int>(P.big_tasks.size()) - cur.begin; break;
+      case K_SPSI: cur.count = static_cast<int>(P.spsi_tasks.size()) - cur.begin; break;
       default: cur.count = static_cast<int>(P.scale_tasks.size()) - cur.begin; break;
     }
     if (cur.kind == K_GEMM && cur.count > 1) {
@@ -718,6 +722,44 @@ Plan build_plan(ProblemDesc desc) {
     for (int x : xs) items.push_back(InvItem{B.msz(x), x, fold_pos[x], B.I(x).off_d});
     B.emit_inverses(l, 0, items, P.big_scratch);
   };
+  // Leaves whose coupling block A_{x,S(x)} is the -H template alone: no Schur
+  // fill (no descendants), every S entry original, no Sigma^r slot inside it.
+  // Their Psi is formed from the stencil entries (K_SPSI).
+  std::vector<char> leaf_sparse(static_cast<std::size_t>(nc), 0);
+  std::vector<std::vector<std::vector<std::pair<int, cplx>>>> leaf_cols(static_cast<std::size_t>(nc));
+  {
+    std::vector<std::pair<int64_t, int>> arows;  // (off_arow, cluster) of candidate leaves
+    for (int c = 0; c < nc; ++c) {
+      const ClusterInfo& I = B.I(c);
+      if (!t.cluster(c).children.empty() || c == root || I.K == 0 || I.K0 != I.K) continue;
+      bool orig = true;
+      for (char o : I.s_orig) orig = orig && o;
+      if (!orig) continue;
+      leaf_sparse[static_cast<std::size_t>(c)] = 1;
+      leaf_cols[static_cast<std::size_t>(c)].resize(static_cast<std::size_t>(I.K));
+      arows.push_back({I.off_arow, c});
+    }
+    std::sort(arows.begin(), arows.end());
+    auto owner = [&](int64_t pos) -> int {  // candidate leaf whose Arow holds pos, or -1
+      auto it = std::upper_bound(arows.begin(), arows.end(), std::make_pair(pos, std::numeric_limits<int>::max()));
+      if (it == arows.begin()) return -1;
+      --it;
+      const ClusterInfo& I = B.I(it->second);
+      return pos < I.off_arow + int64_t(I.m) * I.K ? it->second : -1;
+    };
+    for (int64_t pos : P.sr_slot_pos) {
+      const int c = owner(pos);
+      if (c >= 0) leaf_sparse[static_cast<std::size_t>(c)] = 0;
+    }
+    for (std::size_t q = 0; q < P.h_pos.size(); ++q) {
+      const int c = owner(P.h_pos[q]);
+      if (c < 0 || !leaf_sparse[static_cast<std::size_t>(c)]) continue;
+      const ClusterInfo& I = B.I(c);
+      const int64_t rel = P.h_pos[q] - I.off_arow;
+      leaf_cols[static_cast<std::size_t>(c)][static_cast<std::size_t>(rel % I.K)].push_back(
+          {static_cast<int>(rel / I.K), P.h_val[q]});
+    }
+  }
   auto gather_schur = [&](int l) {
     B.open(K_GEMM, 0, l);
     for (const auto& kv : schur[l]) {
@@ -745,16 +787,46 @@ Plan build_plan(ProblemDesc desc) {
     const auto& xs = by_level[l];
     gather_schur(l);
     emit_inverses(l, xs);
+    std::vector<int> sparse;  // leaves whose coupling block is the -H template alone
     B.open(K_GEMM, 0, l);  // Psi_x = -inv_x A_{x,S(x)}
     for (int x : xs) {
       const ClusterInfo& I = B.I(x);
       if (!I.K) continue;
+      if (leaf_sparse[static_cast<std::size_t>(x)]) {
+        sparse.push_back(x);
+        continue;
+      }
       const int tb = static_cast<int>(T.size());
       B.add_term(T, I.m, OP_N, I.off_d, I.m, OP_N, I.off_arow, I.K, -1);
       if (I.off_psi2 >= 0) B.pend_diag.c2_off = I.off_psi2;
       B.gemm_task(I.m, I.K, I.off_psi, I.K, MODE_SET, 0, 0, tb);
     }
     B.close();
+    if (!sparse.empty()) {
+      B.open(K_SPSI, 0, l);
+      for (int x : sparse) {
+        const ClusterInfo& I = B.I(x);
+        const auto& cols = leaf_cols[static_cast<std::size_t>(x)];
+        SpsiTask st{};
+        st.m = I.m;
+        st.K = I.K;
+        st.col_begin = static_cast<int>(P.spsi_colptr.size());
+        st.off_inv = I.off_d;
+        st.off_psi = I.off_psi;
+        st.off_psi2 = I.off_psi2;
+        for (int c = 0; c < I.K; ++c) {
+          P.spsi_colptr.push_back(static_cast<int>(P.spsi_row.size()));
+          for (const auto& e : cols[static_cast<std::size_t>(c)]) {
+            P.spsi_row.push_back(e.first);
+            P.spsi_val.push_back(e.second);
+          }
+        }
+        P.spsi_colptr.push_back(static_cast<int>(P.spsi_row.size()));
+        B.cur.cmul += double(I.m) * (P.spsi_colptr.back() - P.spsi_colptr[static_cast<std::size_t>(st.col_begin)]);
+        P.spsi_tasks.push_back(st);
+      }
+      B.close();
+    }
   }
   gather_schur(t.levels());
   emit_inverses(t.levels(), std::vector<int>{root});

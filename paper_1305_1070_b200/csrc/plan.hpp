@@ -143,7 +143,21 @@ struct BigTask {
 };
 
 enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL = 4, K_PERM = 5, K_SKEW = 6,
-                    K_COMBINE = 7 };
+                    K_COMBINE = 7, K_SPSI = 8 };
+
+// Psi_x = -inv_x A_{x,S(x)} for a leaf whose coupling block holds only the
+// energy-independent -H entries (no Schur fill below a leaf; contact and
+// phonon self-energies never leave a cluster): A_{x,S} is a few stencil
+// entries per column, so Psi is formed column by column from those entries
+// (CSC in SpsiTask's ranges) instead of a dense m x m x K product.
+struct SpsiTask {
+  int m, K;
+  int col_begin;      // K + 1 entries of Plan::spsi_colptr from here
+  int pad;
+  int64_t off_inv;    // inv_x (m x m, row-major; the D block after inversion)
+  int64_t off_psi;    // Psi_x (m x K)
+  int64_t off_psi2;   // 2 Psi_x, or -1
+};
 
 struct Op {
   int kind;
@@ -236,6 +250,10 @@ struct Plan {
   std::vector<BigTask> big_tasks;
   std::vector<SkewTask> skew_tasks;      // RGF path only
   std::vector<CombineTask> comb_tasks;   // RGF path only
+  std::vector<SpsiTask> spsi_tasks;      // sparse leaf Psi (K_SPSI)
+  std::vector<int> spsi_colptr;          // per task: K + 1 offsets into spsi_row / spsi_val
+  std::vector<int> spsi_row;             // local row t of the entry
+  std::vector<cplx> spsi_val;            // A_{x,S}[t][c] (= -H)
   std::vector<Op> ops;
   std::vector<std::vector<int>> rgf_layers;  // non-empty: an RGF plan (no tree)
   int rgf_gr_ops = 0;                        // ops [0, rgf_gr_ops) = rgf_gr
