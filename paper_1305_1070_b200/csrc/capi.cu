@@ -105,6 +105,8 @@ struct negf_gpu {
   int* d_spsi_colptr = nullptr;
   int* d_spsi_row = nullptr;
   double2* d_spsi_val = nullptr;
+  SschurTask* d_sschur = nullptr;
+  SschurContrib* d_sschur_contrib = nullptr;
   CombineTask* d_comb_tasks = nullptr;
   // per-batch staging
   double *d_energies = nullptr, *d_weights = nullptr;
@@ -235,9 +237,10 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
     launch_output_gr(b, P.desc.n, g->d_gr_pos, d_gr, s, L);
     if (hk->gr_ready) ck(cudaEventRecord(hk->gr_ready, s), "event");
   };
-  static const int kind_stat[9] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
+  static const int kind_stat[10] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE,
-                                   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE};  // K_SPSI: sparse, with the scalings
+                                   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,
+                                    NEGF_KSTAT_SCALE};  // K_SPSI / K_SSCHUR: sparse, with the scalings
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
     if (static_cast<int>(oi) == P.gr_done_op) gr_out();
     if (static_cast<int>(oi) == P.lesser_op) lesser();
@@ -267,6 +270,10 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         break;
       case K_SPSI:
         launch_spsi(b, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row, g->d_spsi_val, op.begin, op.count, s, L);
+        break;
+      case K_SSCHUR:
+        launch_sschur(b, g->d_sschur, g->d_sschur_contrib, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row,
+                      g->d_spsi_val, op.begin, op.count, s, L);
         break;
       default:
         launch_scale(b, g->d_scale, op.begin, op.count, s, L);
@@ -557,6 +564,8 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     g->d_spsi_colptr = dev_upload(P.spsi_colptr, o);
     g->d_spsi_row = dev_upload(P.spsi_row, o);
     g->d_spsi_val = reinterpret_cast<double2*>(dev_upload(P.spsi_val, o));
+    g->d_sschur = dev_upload(P.sschur_tasks, o);
+    g->d_sschur_contrib = dev_upload(P.sschur_contrib, o);
     g->d_comb_tasks = dev_upload(P.comb_tasks, o);
     const int n = P.desc.n;
     const size_t sr = P.desc.sr_rows.size(), sl = P.desc.sl_rows.size();

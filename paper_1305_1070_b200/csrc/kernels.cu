@@ -1652,6 +1652,43 @@ void launch_spsi(const BatchArgs& b, const SpsiTask* d_tasks, const int* d_colpt
   ++launches;
 }
 
+// Sparse leaf Schur contributions (K_SSCHUR): for a target block,
+// T[r][c] (+)= sum over its leaves i (in gather order) of
+// sum_e Psi_i[t_e][p_off + r] a_e over the stencil entries of column q_off + c
+// of the leaf's A_{i,S}.  One CTA per (target, energy), consecutive threads on
+// consecutive columns of a target row.
+__global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, const SschurTask* __restrict__ tasks,
+                                                const SschurContrib* __restrict__ contrib,
+                                                const SpsiTask* __restrict__ spsi, const int* __restrict__ colptr,
+                                                const int* __restrict__ rows, const double2* __restrict__ vals,
+                                                int begin) {
+  const SschurTask tk = tasks[begin + blockIdx.x];
+  double2* base = arena + int64_t(blockIdx.y) * stride;
+  const int total = tk.mp * tk.mq;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int r = idx / tk.mq, c = idx - r * tk.mq;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int q = 0; q < tk.contrib_count; ++q) {
+      const SschurContrib ct = contrib[tk.contrib_begin + q];
+      const SpsiTask& lt = spsi[ct.spsi];
+      const int* cp = colptr + lt.col_begin + ct.q_off + c;
+      const double2* psi = base + lt.off_psi + ct.p_off + r;
+      for (int e = cp[0]; e < cp[1]; ++e) acc = cadd(acc, cmul(psi[int64_t(rows[e]) * lt.K], vals[e]));
+    }
+    double2* dst = base + tk.off + int64_t(r) * tk.ld + c;
+    *dst = tk.mode == MODE_ADD ? cadd(*dst, acc) : acc;
+  }
+}
+
+void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurContrib* d_contrib,
+                   const SpsiTask* d_spsi, const int* d_colptr, const int* d_rows, const double2* d_vals, int begin,
+                   int count, cudaStream_t s, int64_t& launches) {
+  if (count <= 0) return;
+  k_sschur<<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, d_contrib, d_spsi, d_colptr, d_rows,
+                                              d_vals, begin);
+  ++launches;
+}
+
 // Persistent launch: CTAs stride over (tile, energy) items, energy fastest;
 // one launch per warp arrangement of an op (a task may mix arrangements,
 // plan.cpp tile_task); tiles pre-sorted by decreasing cost in the plan.

@@ -85,6 +85,7 @@ struct Builder {
       case K_PANEL:
       case K_PERM: cur.begin = static_cast<int>(P.big_tasks.size()); break;
       case K_SPSI: cur.begin = static_cast<int>(P.spsi_tasks.size()); break;
+      case K_SSCHUR: cur.begin = static_cast<int>(P.sschur_tasks.size()); break;
       default: cur.begin = static_cast<int>(P.scale_tasks.size()); break;
     }
   }
@@ -99,6 +100,7 @@ struct Builder {
       case K_PANEL:
       case K_PERM: cur.count = static_cast<int>(P.big_tasks.size()) - cur.begin; break;
       case K_SPSI: cur.count = static_cast<int>(P.spsi_tasks.size()) - cur.begin; break;
+      case K_SSCHUR: cur.count = static_cast<int>(P.sschur_tasks.size()) - cur.begin; break;
       default: cur.count = static_cast<int>(P.scale_tasks.size()) - cur.begin; break;
     }
     if (cur.kind == K_GEMM && cur.count > 1) {
@@ -760,25 +762,71 @@ Plan build_plan(ProblemDesc desc) {
           {static_cast<int>(rel / I.K), P.h_val[q]});
     }
   }
+  // Leaf -> SpsiTask index (leaves' Psi tasks are emitted at level 1, before
+  // any gather that reads them).
+  std::vector<int> spsi_of(static_cast<std::size_t>(nc), -1);
   auto gather_schur = [&](int l) {
-    B.open(K_GEMM, 0, l);
+    // sparse leaf contributions first (their own op), then the dense gather
+    std::vector<char> had_sparse;
+    B.open(K_SSCHUR, 0, l);
     for (const auto& kv : schur[l]) {
       const int jp = kv.first.first, jq = kv.first.second;
       const ClusterInfo& J = B.I(jp);
+      SschurTask st{};
+      st.contrib_begin = static_cast<int>(P.sschur_contrib.size());
+      double cm = 0.0;
+      for (const auto& c3 : kv.second) {
+        const int i = c3[0];
+        const int sp = spsi_of[static_cast<std::size_t>(i)];
+        if (sp < 0) continue;
+        const ClusterInfo& X = B.I(i);
+        P.sschur_contrib.push_back(SschurContrib{sp, static_cast<int>(X.s_col[c3[1]]), static_cast<int>(X.s_col[c3[2]]), 0});
+        const int* cp = P.spsi_colptr.data() + P.spsi_tasks[static_cast<std::size_t>(sp)].col_begin + X.s_col[c3[2]];
+        cm += double(B.msz(jp)) * (cp[B.msz(jq)] - cp[0]);
+      }
+      st.contrib_count = static_cast<int>(P.sschur_contrib.size()) - st.contrib_begin;
+      had_sparse.push_back(st.contrib_count > 0);
+      if (!st.contrib_count) continue;
+      st.mp = J.m;
+      st.mq = B.msz(jq);
+      if (jp == jq) {
+        st.ld = J.m;
+        st.mode = MODE_ADD;
+        st.off = J.off_d;
+      } else {
+        const int p = find_pos(J.S, jq);
+        if (p < 0) fail(kInternal, "plan: fill block missing from S");
+        st.ld = J.K;
+        st.mode = J.s_orig[p] ? MODE_ADD : MODE_SET;
+        st.off = J.off_arow + J.s_col[p];
+      }
+      P.sschur_tasks.push_back(st);
+      B.cur.cmul += cm;
+    }
+    B.close();
+    B.open(K_GEMM, 0, l);
+    std::size_t q = 0;
+    for (const auto& kv : schur[l]) {
+      const int jp = kv.first.first, jq = kv.first.second;
+      const bool sparse_done = had_sparse[q++];
+      const ClusterInfo& J = B.I(jp);
       const int tb = static_cast<int>(T.size());
       for (const auto& c3 : kv.second) {
+        if (spsi_of[static_cast<std::size_t>(c3[0])] >= 0) continue;
         const ClusterInfo& X = B.I(c3[0]);
         B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N, X.off_arow + X.s_col[c3[2]], X.K, +1);
       }
+      if (static_cast<int>(T.size()) == tb) continue;  // leaves only: done by the sparse op
       if (jp == jq) {  // A_jj += sum Psi^T A_{i,j}: complex symmetric
         B.pend_diag.mirror = 1;
         B.gemm_task(J.m, J.m, J.off_d, J.m, MODE_ADD, 0, 0, tb);
-      }
-      else {
+      } else {
         const int p = find_pos(J.S, jq);
         if (p < 0) fail(kInternal, "plan: fill block missing from S");
-        // a pure fill block is produced by this single gather task
-        B.gemm_task(J.m, B.msz(jq), J.off_arow + J.s_col[p], J.K, J.s_orig[p] ? MODE_ADD : MODE_SET, 0, 0, tb);
+        // a pure fill block is produced by this single gather task (or
+        // started by the sparse op, then accumulated)
+        B.gemm_task(J.m, B.msz(jq), J.off_arow + J.s_col[p], J.K,
+                    (J.s_orig[p] || sparse_done) ? MODE_ADD : MODE_SET, 0, 0, tb);
       }
     }
     B.close();
@@ -823,6 +871,7 @@ Plan build_plan(ProblemDesc desc) {
         }
         P.spsi_colptr.push_back(static_cast<int>(P.spsi_row.size()));
         B.cur.cmul += double(I.m) * (P.spsi_colptr.back() - P.spsi_colptr[static_cast<std::size_t>(st.col_begin)]);
+        spsi_of[static_cast<std::size_t>(x)] = static_cast<int>(P.spsi_tasks.size());
         P.spsi_tasks.push_back(st);
       }
       B.close();

@@ -143,7 +143,7 @@ struct BigTask {
 };
 
 enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL = 4, K_PERM = 5, K_SKEW = 6,
-                    K_COMBINE = 7, K_SPSI = 8 };
+                    K_COMBINE = 7, K_SPSI = 8, K_SSCHUR = 9 };
 
 // Psi_x = -inv_x A_{x,S(x)} for a leaf whose coupling block holds only the
 // energy-independent -H entries (no Schur fill below a leaf; contact and
@@ -157,6 +157,21 @@ struct SpsiTask {
   int64_t off_inv;    // inv_x (m x m, row-major; the D block after inversion)
   int64_t off_psi;    // Psi_x (m x K)
   int64_t off_psi2;   // 2 Psi_x, or -1
+};
+
+// The leaves' share of a gathered Schur update (hsc.cpp:501-511):
+// A_{jp,jq} (+)= sum over leaves i of Psi_{i,jp}^T A_{i,jq}, with A_{i,jq} the
+// leaf's stencil entries (SpsiTask CSC): m_p x m_q outputs, a few products
+// each.  Runs before the block's dense gather GEMM (which then accumulates).
+struct SschurTask {
+  int mp, mq, ld, mode;         // mode: MODE_ADD or MODE_SET
+  int contrib_begin, contrib_count;
+  int64_t off;                  // target block
+};
+struct SschurContrib {
+  int spsi;                     // the leaf's SpsiTask (Psi, K, CSC)
+  int p_off, q_off;             // column offsets of jp in Psi_i and of jq in A_{i,S}
+  int pad;
 };
 
 struct Op {
@@ -254,6 +269,8 @@ struct Plan {
   std::vector<int> spsi_colptr;          // per task: K + 1 offsets into spsi_row / spsi_val
   std::vector<int> spsi_row;             // local row t of the entry
   std::vector<cplx> spsi_val;            // A_{x,S}[t][c] (= -H)
+  std::vector<SschurTask> sschur_tasks;  // sparse leaf Schur contributions (K_SSCHUR)
+  std::vector<SschurContrib> sschur_contrib;
   std::vector<Op> ops;
   std::vector<std::vector<int>> rgf_layers;  // non-empty: an RGF plan (no tree)
   int rgf_gr_ops = 0;                        // ops [0, rgf_gr_ops) = rgf_gr
