@@ -125,7 +125,7 @@ int negf_plan_gemm_tiles(const negf_plan* p, int32_t* task, int32_t* m0, int32_t
                          int32_t* mirrored);
 /* The replayed op list (introspection, n_ops entries): kind (0 inverse,
  * 1 grouped GEMM, 2 diagonal, 3 seed scaling, 4 panel, 5 permutation, 6 skew,
- * 7 combine, 8 sparse leaf Psi, 9 sparse leaf Schur contributions),
+ * 7 combine, 8 sparse leaf Psi, 9 sparse leaf Schur contributions, 10 leaf Woodbury diagonals),
  * phase (0 fold, 1 G^r, 2 seed, 3 N fold, 4 G^<), tree level, range in the
  * kind's task (GEMM: tile) array, executed complex MACs per energy; any
  * pointer may be NULL. */

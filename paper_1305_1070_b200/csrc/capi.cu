@@ -107,6 +107,10 @@ struct negf_gpu {
   double2* d_spsi_val = nullptr;
   SschurTask* d_sschur = nullptr;
   SschurContrib* d_sschur_contrib = nullptr;
+  LeafDiagTask* d_ld = nullptr;
+  int* d_ld_rows = nullptr;
+  int* d_ld_optr = nullptr;
+  LeafDiagEntry* d_ld_entries = nullptr;
   CombineTask* d_comb_tasks = nullptr;
   // per-batch staging
   double *d_energies = nullptr, *d_weights = nullptr;
@@ -237,10 +241,11 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
     launch_output_gr(b, P.desc.n, g->d_gr_pos, d_gr, s, L);
     if (hk->gr_ready) ck(cudaEventRecord(hk->gr_ready, s), "event");
   };
-  static const int kind_stat[10] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
+  static const int kind_stat[11] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE,
                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,
-                                    NEGF_KSTAT_SCALE};  // K_SPSI / K_SSCHUR: sparse, with the scalings
+                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_DIAG};  // K_SPSI / K_SSCHUR: sparse, with
+                                                                            // the scalings; K_LEAFDIAG: diagonals
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
     if (static_cast<int>(oi) == P.gr_done_op) gr_out();
     if (static_cast<int>(oi) == P.lesser_op) lesser();
@@ -270,6 +275,10 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         break;
       case K_SPSI:
         launch_spsi(b, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row, g->d_spsi_val, op.begin, op.count, s, L);
+        break;
+      case K_LEAFDIAG:
+        launch_leafdiag(b, g->d_ld, P.ld_tasks.data(), g->d_ld_rows, g->d_ld_optr, g->d_ld_entries, op.begin,
+                        op.count, s, L);
         break;
       case K_SSCHUR:
         launch_sschur(b, g->d_sschur, g->d_sschur_contrib, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row,
@@ -566,6 +575,10 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     g->d_spsi_val = reinterpret_cast<double2*>(dev_upload(P.spsi_val, o));
     g->d_sschur = dev_upload(P.sschur_tasks, o);
     g->d_sschur_contrib = dev_upload(P.sschur_contrib, o);
+    g->d_ld = dev_upload(P.ld_tasks, o);
+    g->d_ld_rows = dev_upload(P.ld_rows, o);
+    g->d_ld_optr = dev_upload(P.ld_optr, o);
+    g->d_ld_entries = dev_upload(P.ld_entries, o);
     g->d_comb_tasks = dev_upload(P.comb_tasks, o);
     const int n = P.desc.n;
     const size_t sr = P.desc.sr_rows.size(), sl = P.desc.sl_rows.size();

@@ -1689,6 +1689,76 @@ void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurCo
   ++launches;
 }
 
+// Woodbury diagonals of sparse leaves (K_LEAFDIAG, plan.hpp LeafDiagTask):
+// M (nT x nT) gathered from the stored G / P blocks (upper triangle, one
+// thread per output, fixed entry order), mirrored; W = inv_x[:, T] staged;
+// then one thread per row r: sum_{i1,i2} W[r][i1] M[i1][i2] op(W[r][i2]).
+__global__ void __launch_bounds__(128) k_leafdiag(double2* arena, int64_t stride,
+                                                  const LeafDiagTask* __restrict__ tasks,
+                                                  const int* __restrict__ trows, const int* __restrict__ optr,
+                                                  const LeafDiagEntry* __restrict__ ent, int begin) {
+  extern __shared__ double2 sm[];
+  const LeafDiagTask tk = tasks[begin + blockIdx.x];
+  double2* base = arena + int64_t(blockIdx.y) * stride;
+  const int nT = tk.nT, m = tk.m;
+  const int wp = nT | 1;  // odd pitch: conflict-free column reads of W
+  double2* M = sm;
+  double2* W = sm + nT * nT;
+  const int* T = trows + tk.t_begin;
+  const int* op = optr + tk.out_begin;
+  const int nO = nT * (nT + 1) / 2;
+  for (int o = threadIdx.x; o < nO; o += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    int out = 0;
+    for (int e = op[o]; e < op[o + 1]; ++e) {
+      const LeafDiagEntry en = ent[e];
+      double2 v = base[en.pos];
+      if (en.flag) v = make_double2(-v.x, v.y);
+      const double* cf = reinterpret_cast<const double*>(&en.coef);  // std::complex: (re, im)
+      acc = cadd(acc, cmul(make_double2(cf[0], cf[1]), v));
+      out = en.out;
+    }
+    const int i1 = out >> 16, i2 = out & 0xffff;
+    M[i1 * nT + i2] = acc;
+    if (i1 != i2) M[i2 * nT + i1] = tk.mode == 0 ? acc : make_double2(-acc.x, acc.y);
+  }
+  for (int idx = threadIdx.x; idx < m * nT; idx += blockDim.x) {
+    const int r = idx / nT, i = idx - r * nT;
+    W[r * wp + i] = base[tk.off_inv + int64_t(r) * m + T[i]];
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    const double2* w = W + r * wp;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i1 = 0; i1 < nT; ++i1) {
+      double2 y = make_double2(0.0, 0.0);
+      for (int i2 = 0; i2 < nT; ++i2) {
+        double2 w2 = w[i2];
+        if (tk.mode) w2.y = -w2.y;
+        y = cadd(y, cmul(M[i1 * nT + i2], w2));
+      }
+      acc = cadd(acc, cmul(w[i1], y));
+    }
+    if (tk.mode == 0) acc = cadd(base[tk.off_inv + int64_t(r) * m + r], acc);
+    base[tk.off_out + r] = acc;
+  }
+}
+
+void launch_leafdiag(const BatchArgs& b, const LeafDiagTask* d_tasks, const LeafDiagTask* h_tasks,
+                     const int* d_rows, const int* d_optr, const LeafDiagEntry* d_ent, int begin, int count,
+                     cudaStream_t s, int64_t& launches) {
+  if (count <= 0) return;
+  size_t smem = 0;
+  for (int i = begin; i < begin + count; ++i) {
+    const LeafDiagTask& t = h_tasks[i];
+    smem = std::max(smem, sizeof(double2) * (size_t(t.nT) * t.nT + size_t(t.m) * (t.nT | 1)));
+  }
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr)) cudaFuncSetAttribute(k_leafdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  k_leafdiag<<<dim3(count, b.nE), 128, smem, s>>>(b.arena, b.stride, d_tasks, d_rows, d_optr, d_ent, begin);
+  ++launches;
+}
+
 // Persistent launch: CTAs stride over (tile, energy) items, energy fastest;
 // one launch per warp arrangement of an op (a task may mix arrangements,
 // plan.cpp tile_task); tiles pre-sorted by decreasing cost in the plan.

@@ -86,6 +86,7 @@ struct Builder {
       case K_PERM: cur.begin = static_cast<int>(P.big_tasks.size()); break;
       case K_SPSI: cur.begin = static_cast<int>(P.spsi_tasks.size()); break;
       case K_SSCHUR: cur.begin = static_cast<int>(P.sschur_tasks.size()); break;
+      case K_LEAFDIAG: cur.begin = static_cast<int>(P.ld_tasks.size()); break;
       default: cur.begin = static_cast<int>(P.scale_tasks.size()); break;
     }
   }
@@ -101,6 +102,7 @@ struct Builder {
       case K_PERM: cur.count = static_cast<int>(P.big_tasks.size()) - cur.begin; break;
       case K_SPSI: cur.count = static_cast<int>(P.spsi_tasks.size()) - cur.begin; break;
       case K_SSCHUR: cur.count = static_cast<int>(P.sschur_tasks.size()) - cur.begin; break;
+      case K_LEAFDIAG: cur.count = static_cast<int>(P.ld_tasks.size()) - cur.begin; break;
       default: cur.count = static_cast<int>(P.scale_tasks.size()) - cur.begin; break;
     }
     if (cur.kind == K_GEMM && cur.count > 1) {
@@ -762,6 +764,80 @@ Plan build_plan(ProblemDesc desc) {
           {static_cast<int>(rel / I.K), P.h_val[q]});
     }
   }
+  // Woodbury diagonals of the sparse, never-referenced, unseeded leaves
+  // (LeafDiagTask): per leaf its boundary rows T and, per mode, the gathered
+  // upper triangle of M.
+  std::vector<char> leaf_wood(static_cast<std::size_t>(nc), 0);
+  auto emit_leafdiag = [&](int x, int mode) {
+    const ClusterInfo& X = B.I(x);
+    // rows of A_{x,S}: (column in S space, value), from the column lists
+    std::vector<std::vector<std::pair<int, cplx>>> rows(static_cast<std::size_t>(X.m));
+    const auto& cols = leaf_cols[static_cast<std::size_t>(x)];
+    for (int c = 0; c < X.K; ++c)
+      for (const auto& e : cols[static_cast<std::size_t>(c)]) rows[static_cast<std::size_t>(e.first)].push_back({c, e.second});
+    std::vector<int> T;
+    for (int r = 0; r < X.m; ++r)
+      if (!rows[static_cast<std::size_t>(r)].empty()) T.push_back(r);
+    auto where = [&](int cc, int& k, int& l) {  // S-space column -> (cluster, local index)
+      for (std::size_t q = 0; q < X.S.size(); ++q)
+        if (cc >= X.s_col[q] && cc < X.s_col[q] + B.msz(X.S[q])) {
+          k = X.S[q];
+          l = static_cast<int>(cc - X.s_col[q]);
+          return;
+        }
+      fail(kInternal, "plan: leaf coupling column outside S");
+    };
+    // arena position of G_SS / P_SS (k1, l1; k2, l2); flag: -conj of that entry
+    auto at = [&](int k1, int l1, int k2, int l2, int& flag) -> int64_t {
+      flag = 0;
+      const ClusterInfo& K1 = B.I(k1);
+      const ClusterInfo& K2 = B.I(k2);
+      if (mode == 0) {
+        if (k1 == k2) return K1.off_gd + int64_t(l1) * K1.m + l2;
+        if (B.lev(k1) < B.lev(k2)) return K1.off_grow + int64_t(l1) * K1.WG + B.col_of(K1.gcols, K1.gcol_off, k2) + l2;
+        return K2.off_grow + int64_t(l2) * K2.WG + B.col_of(K2.gcols, K2.gcol_off, k1) + l1;  // G symmetric
+      }
+      if (k1 == k2) return K1.off_pd + int64_t(l1) * K1.m + l2;
+      if (B.lev(k1) < B.lev(k2)) return K1.off_prow + int64_t(l1) * K1.WP + B.col_of(K1.pcols, K1.pcol_off, k2) + l2;
+      flag = 1;  // P_{k1,k2} = -P_{k2,k1}^H (hsc.cpp:204-206)
+      return K2.off_prow + int64_t(l2) * K2.WP + B.col_of(K2.pcols, K2.pcol_off, k1) + l1;
+    };
+    LeafDiagTask lt{};
+    lt.m = X.m;
+    lt.nT = static_cast<int>(T.size());
+    lt.t_begin = static_cast<int>(P.ld_rows.size());
+    lt.out_begin = static_cast<int>(P.ld_optr.size());
+    lt.mode = mode;
+    lt.off_inv = X.off_d;
+    lt.off_out = mode == 0 ? X.off_gd : X.off_pd;
+    for (int r : T) P.ld_rows.push_back(r);
+    double cm = 0.0;
+    for (int i1 = 0; i1 < lt.nT; ++i1)
+      for (int i2 = i1; i2 < lt.nT; ++i2) {
+        P.ld_optr.push_back(static_cast<int>(P.ld_entries.size()));
+        for (const auto& e1 : rows[static_cast<std::size_t>(T[static_cast<std::size_t>(i1)])])
+          for (const auto& e2 : rows[static_cast<std::size_t>(T[static_cast<std::size_t>(i2)])]) {
+            int k1, l1, k2, l2, flag;
+            where(e1.first, k1, l1);
+            where(e2.first, k2, l2);
+            LeafDiagEntry en{};
+            en.pos = at(k1, l1, k2, l2, flag);
+            en.flag = flag;
+            en.out = (i1 << 16) | i2;
+            en.coef = mode == 0 ? e1.second * e2.second : e1.second * std::conj(e2.second);
+            P.ld_entries.push_back(en);
+            cm += 1.0;
+          }
+      }
+    P.ld_optr.push_back(static_cast<int>(P.ld_entries.size()));
+    B.cur.cmul += cm + double(X.m) * lt.nT * (lt.nT + 1);  // gather + W M W^T per row
+    P.ld_tasks.push_back(lt);
+  };
+  for (int c = 0; c < nc; ++c) {
+    const ClusterInfo& I = B.I(c);
+    leaf_wood[static_cast<std::size_t>(c)] = leaf_sparse[static_cast<std::size_t>(c)] && !I.full_g && !I.full_p &&
+                                             !I.seeded && !I.has_nd && I.ncols.empty() && I.m > 0 && I.m < 65536;
+  }
   // Leaf -> SpsiTask index (leaves' Psi tasks are emitted at level 1, before
   // any gather that reads them).
   std::vector<int> spsi_of(static_cast<std::size_t>(nc), -1);
@@ -861,7 +937,7 @@ Plan build_plan(ProblemDesc desc) {
         st.col_begin = static_cast<int>(P.spsi_colptr.size());
         st.off_inv = I.off_d;
         st.off_psi = I.off_psi;
-        st.off_psi2 = I.off_psi2;
+        st.off_psi2 = leaf_wood[static_cast<std::size_t>(x)] ? -1 : I.off_psi2;  // 2 Psi: the row forms only
         for (int c = 0; c < I.K; ++c) {
           P.spsi_colptr.push_back(static_cast<int>(P.spsi_row.size()));
           for (const auto& e : cols[static_cast<std::size_t>(c)]) {
@@ -889,6 +965,7 @@ Plan build_plan(ProblemDesc desc) {
     B.open(K_GEMM, 1, l);
     for (int x : xs) {
       const ClusterInfo& X = B.I(x);
+      if (leaf_wood[static_cast<std::size_t>(x)]) continue;  // K_LEAFDIAG below
       const bool sym = !X.full_g && X.off_gpart >= 0 && X.off_psi2 >= 0;
       for (std::size_t jj = 0; jj < X.gcols.size(); ++jj) {
         const int j = X.gcols[jj];
@@ -939,7 +1016,7 @@ Plan build_plan(ProblemDesc desc) {
     B.open(K_DIAG, 1, l);  // diagonal entries only (never-referenced, unseeded)
     for (int x : xs) {
       const ClusterInfo& X = B.I(x);
-      if (X.full_g || X.m == 0) continue;
+      if (X.full_g || X.m == 0 || leaf_wood[static_cast<std::size_t>(x)]) continue;
       DiagTask dt{};
       dt.m = X.m;
       dt.init_stride = X.m + 1;
@@ -954,6 +1031,10 @@ Plan build_plan(ProblemDesc desc) {
       dt.term_count = static_cast<int>(P.diag_terms.size()) - dt.term_begin;
       P.diag_tasks.push_back(dt);
     }
+    B.close();
+    B.open(K_LEAFDIAG, 1, l);
+    for (int x : xs)
+      if (leaf_wood[static_cast<std::size_t>(x)]) emit_leafdiag(x, 0);
     B.close();
   }
 
@@ -1035,6 +1116,7 @@ Plan build_plan(ProblemDesc desc) {
       B.open(K_GEMM, 4, l);
       for (int x : xs) {
         const ClusterInfo& X = B.I(x);
+        if (leaf_wood[static_cast<std::size_t>(x)]) continue;  // K_LEAFDIAG below
         // Symmetric form of a diagonal-only, unseeded P row set:
         // diag(P_xx) = diag(Psi P_SS Psi^H) with P_SS anti-Hermitian (P_{j,k} =
         // -P_{k,j}^H, hsc.cpp:204-206), so the (k, j) and (j, k) block pairs sum to
@@ -1092,7 +1174,7 @@ Plan build_plan(ProblemDesc desc) {
       B.open(K_DIAG, 4, l);
       for (int x : xs) {
         const ClusterInfo& X = B.I(x);
-        if (X.full_p || X.m == 0) continue;
+        if (X.full_p || X.m == 0 || leaf_wood[static_cast<std::size_t>(x)]) continue;
         DiagTask dt{};
         dt.m = X.m;
         dt.init_stride = 0;
@@ -1110,6 +1192,10 @@ Plan build_plan(ProblemDesc desc) {
         dt.term_count = static_cast<int>(P.diag_terms.size()) - dt.term_begin;
         P.diag_tasks.push_back(dt);
       }
+      B.close();
+      B.open(K_LEAFDIAG, 4, l);
+      for (int x : xs)
+        if (leaf_wood[static_cast<std::size_t>(x)]) emit_leafdiag(x, 1);
       B.close();
     }
   }

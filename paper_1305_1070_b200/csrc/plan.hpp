@@ -143,7 +143,7 @@ struct BigTask {
 };
 
 enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL = 4, K_PERM = 5, K_SKEW = 6,
-                    K_COMBINE = 7, K_SPSI = 8, K_SSCHUR = 9 };
+                    K_COMBINE = 7, K_SPSI = 8, K_SSCHUR = 9, K_LEAFDIAG = 10 };
 
 // Psi_x = -inv_x A_{x,S(x)} for a leaf whose coupling block holds only the
 // energy-independent -H entries (no Schur fill below a leaf; contact and
@@ -168,6 +168,31 @@ struct SschurTask {
   int contrib_begin, contrib_count;
   int64_t off;                  // target block
 };
+// diag(G_xx) / diag(P_xx) of a never-referenced, unseeded sparse leaf by the
+// Woodbury form of hsc.cpp:220-226 / 289-300: with Psi = -inv_x A_{x,S} and
+// A_{x,S} nonzero only on the rows T of boundary dofs,
+//   diag(G_xx) = diag(inv_x) + diag(W M W^T),  M = A_{T,S} G_SS A_{T,S}^T,
+//   diag(P_xx) =               diag(W M W^H),  M = A_{T,S} P_SS A_{T,S}^H,
+// W = inv_x[:, T]: |T|^2 entries of M gathered from the stored G / P blocks
+// instead of the m x K x K row products.  M is complex symmetric (G) /
+// anti-Hermitian (P): its upper triangle is gathered (CSR over the
+// |T|(|T|+1)/2 outputs of LeafDiagTask), the lower one mirrored.
+struct LeafDiagTask {
+  int m, nT;
+  int t_begin;        // nT local rows in Plan::ld_rows
+  int out_begin;      // nT(nT+1)/2 + 1 entries of Plan::ld_optr
+  int mode;           // 0: G (symmetric, + diag inv), 1: P (anti-Hermitian)
+  int pad;
+  int64_t off_inv;    // inv_x (m x m)
+  int64_t off_out;    // diag vector (m)
+};
+struct LeafDiagEntry {
+  int64_t pos;        // arena position of the G / P entry
+  int flag;           // 1: use -conj(value) (P block read in the other orientation)
+  int out;            // packed (i1 << 16) | i2 of the output (redundant, for checks)
+  cplx coef;          // a1 a2 (G) or a1 conj(a2) (P)
+};
+
 struct SschurContrib {
   int spsi;                     // the leaf's SpsiTask (Psi, K, CSC)
   int p_off, q_off;             // column offsets of jp in Psi_i and of jq in A_{i,S}
@@ -271,6 +296,10 @@ struct Plan {
   std::vector<cplx> spsi_val;            // A_{x,S}[t][c] (= -H)
   std::vector<SschurTask> sschur_tasks;  // sparse leaf Schur contributions (K_SSCHUR)
   std::vector<SschurContrib> sschur_contrib;
+  std::vector<LeafDiagTask> ld_tasks;    // K_LEAFDIAG
+  std::vector<int> ld_rows;              // T lists
+  std::vector<int> ld_optr;              // per task: CSR over its upper-triangle outputs
+  std::vector<LeafDiagEntry> ld_entries;
   std::vector<Op> ops;
   std::vector<std::vector<int>> rgf_layers;  // non-empty: an RGF plan (no tree)
   int rgf_gr_ops = 0;                        // ops [0, rgf_gr_ops) = rgf_gr
