@@ -1654,8 +1654,9 @@ void launch_spsi(const BatchArgs& b, const SpsiTask* d_tasks, const int* d_colpt
 
 // Sparse leaf Schur contributions (K_SSCHUR): for a target block,
 // T[r][c] (+)= sum over its leaves i (in gather order) of
-// sum_e Psi_i[t_e][p_off + r] a_e over the stencil entries of column q_off + c
-// of the leaf's A_{i,S}.  One CTA per (target, energy), consecutive threads on
+// (Psi_i^T A_i)[p_off + r][q_off + c] = -sum inv_i[t][t'] a(t', p_off + r) a(t, q_off + c)
+// over the stencil entries of the two columns of the leaf's A_{i,S} (Psi_i
+// itself is not needed).  One CTA per (target, energy), consecutive threads on
 // consecutive columns of a target row.
 __global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, const SschurTask* __restrict__ tasks,
                                                 const SschurContrib* __restrict__ contrib,
@@ -1669,11 +1670,19 @@ __global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, 
     const int r = idx / tk.mq, c = idx - r * tk.mq;
     double2 acc = make_double2(0.0, 0.0);
     for (int q = 0; q < tk.contrib_count; ++q) {
+      // Psi_i^T A_i = -A_{i,jp}^T inv_i A_{i,jq}: the stencil entries of
+      // column p_off + r (rows t', a1) and of column q_off + c (rows t, a2)
       const SschurContrib ct = contrib[tk.contrib_begin + q];
       const SpsiTask& lt = spsi[ct.spsi];
-      const int* cp = colptr + lt.col_begin + ct.q_off + c;
-      const double2* psi = base + lt.off_psi + ct.p_off + r;
-      for (int e = cp[0]; e < cp[1]; ++e) acc = cadd(acc, cmul(psi[int64_t(rows[e]) * lt.K], vals[e]));
+      const int* cp = colptr + lt.col_begin + ct.p_off + r;
+      const int* cq = colptr + lt.col_begin + ct.q_off + c;
+      const double2* inv = base + lt.off_inv;
+      for (int e2 = cq[0]; e2 < cq[1]; ++e2) {
+        const double2* irow = inv + int64_t(rows[e2]) * lt.m;
+        double2 z = make_double2(0.0, 0.0);
+        for (int e1 = cp[0]; e1 < cp[1]; ++e1) z = cadd(z, cmul(irow[rows[e1]], vals[e1]));
+        acc = csub(acc, cmul(z, vals[e2]));
+      }
     }
     double2* dst = base + tk.off + int64_t(r) * tk.ld + c;
     *dst = tk.mode == MODE_ADD ? cadd(*dst, acc) : acc;

@@ -857,8 +857,10 @@ Plan build_plan(ProblemDesc desc) {
         if (sp < 0) continue;
         const ClusterInfo& X = B.I(i);
         P.sschur_contrib.push_back(SschurContrib{sp, static_cast<int>(X.s_col[c3[1]]), static_cast<int>(X.s_col[c3[2]]), 0});
-        const int* cp = P.spsi_colptr.data() + P.spsi_tasks[static_cast<std::size_t>(sp)].col_begin + X.s_col[c3[2]];
-        cm += double(B.msz(jp)) * (cp[B.msz(jq)] - cp[0]);
+        const int* cb = P.spsi_colptr.data() + P.spsi_tasks[static_cast<std::size_t>(sp)].col_begin;
+        const int* cpp = cb + X.s_col[c3[1]];
+        const int* cpq = cb + X.s_col[c3[2]];
+        cm += double(cpp[B.msz(jp)] - cpp[0]) * (cpq[B.msz(jq)] - cpq[0]);  // entry pairs
       }
       st.contrib_count = static_cast<int>(P.sschur_contrib.size()) - st.contrib_begin;
       had_sparse.push_back(st.contrib_count > 0);
@@ -927,8 +929,18 @@ Plan build_plan(ProblemDesc desc) {
     }
     B.close();
     if (!sparse.empty()) {
+      // leaves whose Psi is read (G / P rows) first: the op launches them;
+      // the Woodbury leaves only keep their CSC record (K_SSCHUR reads
+      // A_{x,S} and inv_x directly)
+      std::stable_partition(sparse.begin(), sparse.end(),
+                            [&](int x) { return !leaf_wood[static_cast<std::size_t>(x)]; });
+      bool closed = false;
       B.open(K_SPSI, 0, l);
       for (int x : sparse) {
+        if (!closed && leaf_wood[static_cast<std::size_t>(x)]) {
+          B.close();
+          closed = true;
+        }
         const ClusterInfo& I = B.I(x);
         const auto& cols = leaf_cols[static_cast<std::size_t>(x)];
         SpsiTask st{};
@@ -946,11 +958,11 @@ Plan build_plan(ProblemDesc desc) {
           }
         }
         P.spsi_colptr.push_back(static_cast<int>(P.spsi_row.size()));
-        B.cur.cmul += double(I.m) * (P.spsi_colptr.back() - P.spsi_colptr[static_cast<std::size_t>(st.col_begin)]);
+        if (!closed) B.cur.cmul += double(I.m) * (P.spsi_colptr.back() - P.spsi_colptr[static_cast<std::size_t>(st.col_begin)]);
         spsi_of[static_cast<std::size_t>(x)] = static_cast<int>(P.spsi_tasks.size());
         P.spsi_tasks.push_back(st);
       }
-      B.close();
+      if (!closed) B.close();
     }
   }
   gather_schur(t.levels());
