@@ -151,3 +151,28 @@ def test_gemm_tiles_cover_config2_exactly_once():
     from paper_1305_1070_b200 import devices
 
     _check_tiles_cover_exactly(negf.HscPlan(devices.config2(n_energies=2).problem))
+
+
+def test_sparse_leaf_paths_are_exercised():
+    """The sparse-leaf ops (K_SPSI 8, K_SSCHUR 9, K_LEAFDIAG 10) replace dense
+    products only where the plan proves them exact; the golden problems the
+    GPU parity tests run must cover each of them and the dense fallback
+    (seeded / fuzzed leaves), and config 2 sends every unseeded leaf down the
+    Woodbury path."""
+    seen = {8: 0, 9: 0, 10: 0}
+    dense_leaf_fallback = False
+    for name in golden_names():
+        _, prob, _, _ = load_golden(name)
+        o = negf.HscPlan(prob).ops()
+        for k in seen:
+            seen[k] += int(o["count"][o["kind"] == k].sum())
+        dense_leaf_fallback |= bool((o["kind"] == 8).any() and not (o["kind"] == 10).any())
+    assert all(v > 0 for v in seen.values()), seen
+    assert dense_leaf_fallback
+    from paper_1305_1070_b200 import devices
+
+    plan = negf.HscPlan(devices.config2(n_energies=2).problem)
+    o = plan.ops()
+    t = plan.tree()
+    leaves = int((np.asarray(t.level) == 1).sum())
+    assert o["count"][o["kind"] == 10].tolist() == [leaves - 2, leaves - 2]  # all but the two contact leaves
