@@ -107,6 +107,7 @@ struct negf_gpu {
   double2* d_spsi_val = nullptr;
   SschurTask* d_sschur = nullptr;
   SschurContrib* d_sschur_contrib = nullptr;
+  int* d_sschur_rc = nullptr;
   LeafDiagTask* d_ld = nullptr;
   int* d_ld_rows = nullptr;
   int* d_ld_optr = nullptr;
@@ -282,7 +283,7 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         break;
       case K_SSCHUR:
         launch_sschur(b, g->d_sschur, g->d_sschur_contrib, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row,
-                      g->d_spsi_val, op.begin, op.count, s, L);
+                      g->d_spsi_val, g->d_sschur_rc, op.begin, op.count, s, L);
         break;
       default:
         launch_scale(b, g->d_scale, op.begin, op.count, s, L);
@@ -575,6 +576,7 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     g->d_spsi_val = reinterpret_cast<double2*>(dev_upload(P.spsi_val, o));
     g->d_sschur = dev_upload(P.sschur_tasks, o);
     g->d_sschur_contrib = dev_upload(P.sschur_contrib, o);
+    g->d_sschur_rc = dev_upload(P.sschur_rc, o);
     g->d_ld = dev_upload(P.ld_tasks, o);
     g->d_ld_rows = dev_upload(P.ld_rows, o);
     g->d_ld_optr = dev_upload(P.ld_optr, o);

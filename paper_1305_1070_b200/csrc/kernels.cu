@@ -1662,39 +1662,49 @@ __global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, 
                                                 const SschurContrib* __restrict__ contrib,
                                                 const SpsiTask* __restrict__ spsi, const int* __restrict__ colptr,
                                                 const int* __restrict__ rows, const double2* __restrict__ vals,
-                                                int begin) {
+                                                const int* __restrict__ rc, int begin) {
   const SschurTask tk = tasks[begin + blockIdx.x];
   double2* base = arena + int64_t(blockIdx.y) * stride;
-  const int total = tk.mp * tk.mq;
-  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    const int r = idx / tk.mq, c = idx - r * tk.mq;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int q = 0; q < tk.contrib_count; ++q) {
-      // Psi_i^T A_i = -A_{i,jp}^T inv_i A_{i,jq}: the stencil entries of
-      // column p_off + r (rows t', a1) and of column q_off + c (rows t, a2)
-      const SschurContrib ct = contrib[tk.contrib_begin + q];
-      const SpsiTask& lt = spsi[ct.spsi];
-      const int* cp = colptr + lt.col_begin + ct.p_off + r;
-      const int* cq = colptr + lt.col_begin + ct.q_off + c;
-      const double2* inv = base + lt.off_inv;
+  double2* tgt = base + tk.off;
+  if (tk.mode != MODE_ADD) {  // a pure fill block starts from zero
+    for (int idx = threadIdx.x; idx < tk.mp * tk.mq; idx += blockDim.x) {
+      const int r = idx / tk.mq, c = idx - r * tk.mq;
+      tgt[int64_t(r) * tk.ld + c] = make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+  }
+  // leaves in gather order; within one leaf its touched rows x columns in parallel
+  for (int q = 0; q < tk.contrib_count; ++q) {
+    const SschurContrib ct = contrib[tk.contrib_begin + q];
+    const SpsiTask& lt = spsi[ct.spsi];
+    const int* R = rc + ct.rc_begin;
+    const int* Cc = R + ct.nr;
+    const double2* inv = base + lt.off_inv;
+    const int* cb = colptr + lt.col_begin;
+    for (int idx = threadIdx.x; idx < ct.nr * ct.nc; idx += blockDim.x) {
+      const int r = R[idx / ct.nc], c = Cc[idx % ct.nc];
+      const int* cp = cb + ct.p_off + r;
+      const int* cq = cb + ct.q_off + c;
+      double2 acc = make_double2(0.0, 0.0);
       for (int e2 = cq[0]; e2 < cq[1]; ++e2) {
         const double2* irow = inv + int64_t(rows[e2]) * lt.m;
         double2 z = make_double2(0.0, 0.0);
         for (int e1 = cp[0]; e1 < cp[1]; ++e1) z = cadd(z, cmul(irow[rows[e1]], vals[e1]));
         acc = csub(acc, cmul(z, vals[e2]));
       }
+      double2* dst = tgt + int64_t(r) * tk.ld + c;
+      *dst = cadd(*dst, acc);
     }
-    double2* dst = base + tk.off + int64_t(r) * tk.ld + c;
-    *dst = tk.mode == MODE_ADD ? cadd(*dst, acc) : acc;
+    __syncthreads();
   }
 }
 
 void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurContrib* d_contrib,
-                   const SpsiTask* d_spsi, const int* d_colptr, const int* d_rows, const double2* d_vals, int begin,
-                   int count, cudaStream_t s, int64_t& launches) {
+                   const SpsiTask* d_spsi, const int* d_colptr, const int* d_rows, const double2* d_vals,
+                   const int* d_rc, int begin, int count, cudaStream_t s, int64_t& launches) {
   if (count <= 0) return;
   k_sschur<<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, d_contrib, d_spsi, d_colptr, d_rows,
-                                              d_vals, begin);
+                                              d_vals, d_rc, begin);
   ++launches;
 }
 

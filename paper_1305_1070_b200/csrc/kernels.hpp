@@ -42,8 +42,8 @@ void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_
 void launch_spsi(const BatchArgs& b, const SpsiTask* d_tasks, const int* d_colptr, const int* d_rows,
                  const double2* d_vals, int begin, int count, cudaStream_t s, int64_t& launches);
 void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurContrib* d_contrib,
-                   const SpsiTask* d_spsi, const int* d_colptr, const int* d_rows, const double2* d_vals, int begin,
-                   int count, cudaStream_t s, int64_t& launches);
+                   const SpsiTask* d_spsi, const int* d_colptr, const int* d_rows, const double2* d_vals,
+                   const int* d_rc, int begin, int count, cudaStream_t s, int64_t& launches);
 void launch_leafdiag(const BatchArgs& b, const LeafDiagTask* d_tasks, const LeafDiagTask* h_tasks,
                      const int* d_rows, const int* d_optr, const LeafDiagEntry* d_ent, int begin, int count,
                      cudaStream_t s, int64_t& launches);

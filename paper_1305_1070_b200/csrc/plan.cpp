@@ -856,10 +856,21 @@ Plan build_plan(ProblemDesc desc) {
         const int sp = spsi_of[static_cast<std::size_t>(i)];
         if (sp < 0) continue;
         const ClusterInfo& X = B.I(i);
-        P.sschur_contrib.push_back(SschurContrib{sp, static_cast<int>(X.s_col[c3[1]]), static_cast<int>(X.s_col[c3[2]]), 0});
+        SschurContrib ct{};
+        ct.spsi = sp;
+        ct.p_off = static_cast<int>(X.s_col[c3[1]]);
+        ct.q_off = static_cast<int>(X.s_col[c3[2]]);
+        ct.rc_begin = static_cast<int>(P.sschur_rc.size());
         const int* cb = P.spsi_colptr.data() + P.spsi_tasks[static_cast<std::size_t>(sp)].col_begin;
-        const int* cpp = cb + X.s_col[c3[1]];
-        const int* cpq = cb + X.s_col[c3[2]];
+        for (int r = 0; r < B.msz(jp); ++r)
+          if (cb[ct.p_off + r + 1] > cb[ct.p_off + r]) P.sschur_rc.push_back(r);
+        ct.nr = static_cast<int>(P.sschur_rc.size()) - ct.rc_begin;
+        for (int c = 0; c < B.msz(jq); ++c)
+          if (cb[ct.q_off + c + 1] > cb[ct.q_off + c]) P.sschur_rc.push_back(c);
+        ct.nc = static_cast<int>(P.sschur_rc.size()) - ct.rc_begin - ct.nr;
+        P.sschur_contrib.push_back(ct);
+        const int* cpp = cb + ct.p_off;
+        const int* cpq = cb + ct.q_off;
         cm += double(cpp[B.msz(jp)] - cpp[0]) * (cpq[B.msz(jq)] - cpq[0]);  // entry pairs
       }
       st.contrib_count = static_cast<int>(P.sschur_contrib.size()) - st.contrib_begin;

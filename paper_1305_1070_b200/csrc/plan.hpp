@@ -194,9 +194,10 @@ struct LeafDiagEntry {
 };
 
 struct SschurContrib {
-  int spsi;                     // the leaf's SpsiTask (Psi, K, CSC)
-  int p_off, q_off;             // column offsets of jp in Psi_i and of jq in A_{i,S}
-  int pad;
+  int spsi;                     // the leaf's SpsiTask (inv_i, CSC of A_{i,S})
+  int p_off, q_off;             // column offsets of jp and of jq in A_{i,S}
+  int nr, nc;                   // target rows / columns the leaf touches (nonempty columns)
+  int rc_begin;                 // nr row then nc column indices in Plan::sschur_rc
 };
 
 struct Op {
@@ -296,6 +297,7 @@ struct Plan {
   std::vector<cplx> spsi_val;            // A_{x,S}[t][c] (= -H)
   std::vector<SschurTask> sschur_tasks;  // sparse leaf Schur contributions (K_SSCHUR)
   std::vector<SschurContrib> sschur_contrib;
+  std::vector<int> sschur_rc;
   std::vector<LeafDiagTask> ld_tasks;    // K_LEAFDIAG
   std::vector<int> ld_rows;              // T lists
   std::vector<int> ld_optr;              // per task: CSR over its upper-triangle outputs
