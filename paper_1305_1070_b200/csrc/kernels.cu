@@ -1711,7 +1711,7 @@ void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurCo
 // Woodbury diagonals of sparse leaves (K_LEAFDIAG, plan.hpp LeafDiagTask):
 // M (nT x nT) gathered from the stored G / P blocks (upper triangle, one
 // thread per output, fixed entry order), mirrored; W = inv_x[:, T] staged;
-// then one thread per row r: sum_{i1,i2} W[r][i1] M[i1][i2] op(W[r][i2]).
+// then one warp per row r: sum_{i1,i2} W[r][i1] M[i1][i2] op(W[r][i2]).
 __global__ void __launch_bounds__(128) k_leafdiag(double2* arena, int64_t stride,
                                                   const LeafDiagTask* __restrict__ tasks,
                                                   const int* __restrict__ trows, const int* __restrict__ optr,
@@ -1720,9 +1720,9 @@ __global__ void __launch_bounds__(128) k_leafdiag(double2* arena, int64_t stride
   const LeafDiagTask tk = tasks[begin + blockIdx.x];
   double2* base = arena + int64_t(blockIdx.y) * stride;
   const int nT = tk.nT, m = tk.m;
-  const int wp = nT | 1;  // odd pitch: conflict-free column reads of W
+  const int wp = nT | 1;  // odd pitches: conflict-free strided reads of W and M
   double2* M = sm;
-  double2* W = sm + nT * nT;
+  double2* W = sm + nT * wp;
   const int* T = trows + tk.t_begin;
   const int* op = optr + tk.out_begin;
   const int nO = nT * (nT + 1) / 2;
@@ -1738,28 +1738,39 @@ __global__ void __launch_bounds__(128) k_leafdiag(double2* arena, int64_t stride
       out = en.out;
     }
     const int i1 = out >> 16, i2 = out & 0xffff;
-    M[i1 * nT + i2] = acc;
-    if (i1 != i2) M[i2 * nT + i1] = tk.mode == 0 ? acc : make_double2(-acc.x, acc.y);
+    M[i1 * wp + i2] = acc;
+    if (i1 != i2) M[i2 * wp + i1] = tk.mode == 0 ? acc : make_double2(-acc.x, acc.y);
   }
   for (int idx = threadIdx.x; idx < m * nT; idx += blockDim.x) {
     const int r = idx / nT, i = idx - r * nT;
     W[r * wp + i] = base[tk.off_inv + int64_t(r) * m + T[i]];
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+  // one warp per row: lane i1 forms W[r][i1] (M[i1][:] . op(W[r][:])); the
+  // lanes' partials are reduced by a fixed xor tree (deterministic)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = warp; r < m; r += nw) {
     const double2* w = W + r * wp;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int i1 = 0; i1 < nT; ++i1) {
+    double2 part = make_double2(0.0, 0.0);
+    for (int i1 = lane; i1 < nT; i1 += 32) {
+      const double2* mr = M + i1 * wp;
       double2 y = make_double2(0.0, 0.0);
       for (int i2 = 0; i2 < nT; ++i2) {
         double2 w2 = w[i2];
         if (tk.mode) w2.y = -w2.y;
-        y = cadd(y, cmul(M[i1 * nT + i2], w2));
+        y = cadd(y, cmul(mr[i2], w2));
       }
-      acc = cadd(acc, cmul(w[i1], y));
+      part = cadd(part, cmul(w[i1], y));
     }
-    if (tk.mode == 0) acc = cadd(base[tk.off_inv + int64_t(r) * m + r], acc);
-    base[tk.off_out + r] = acc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      part.x += __shfl_xor_sync(0xffffffffu, part.x, o);
+      part.y += __shfl_xor_sync(0xffffffffu, part.y, o);
+    }
+    if (lane == 0) {
+      if (tk.mode == 0) part = cadd(base[tk.off_inv + int64_t(r) * m + r], part);
+      base[tk.off_out + r] = part;
+    }
   }
 }
 
@@ -1770,7 +1781,7 @@ void launch_leafdiag(const BatchArgs& b, const LeafDiagTask* d_tasks, const Leaf
   size_t smem = 0;
   for (int i = begin; i < begin + count; ++i) {
     const LeafDiagTask& t = h_tasks[i];
-    smem = std::max(smem, sizeof(double2) * (size_t(t.nT) * t.nT + size_t(t.m) * (t.nT | 1)));
+    smem = std::max(smem, sizeof(double2) * size_t(t.nT + t.m) * (t.nT | 1));
   }
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) cudaFuncSetAttribute(k_leafdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
