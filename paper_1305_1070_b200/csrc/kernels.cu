@@ -1712,7 +1712,10 @@ void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurCo
 // M (nT x nT) gathered from the stored G / P blocks (upper triangle, one
 // thread per output, fixed entry order), mirrored; W = inv_x[:, T] staged;
 // then one warp per row r: sum_{i1,i2} W[r][i1] M[i1][i2] op(W[r][i2]).
-__global__ void __launch_bounds__(128) k_leafdiag(double2* arena, int64_t stride,
+#ifndef NEGF_LD_THREADS
+#define NEGF_LD_THREADS 256
+#endif
+__global__ void __launch_bounds__(NEGF_LD_THREADS) k_leafdiag(double2* arena, int64_t stride,
                                                   const LeafDiagTask* __restrict__ tasks,
                                                   const int* __restrict__ trows, const int* __restrict__ optr,
                                                   const LeafDiagEntry* __restrict__ ent, int begin) {
@@ -1785,7 +1788,7 @@ void launch_leafdiag(const BatchArgs& b, const LeafDiagTask* d_tasks, const Leaf
   }
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) cudaFuncSetAttribute(k_leafdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  k_leafdiag<<<dim3(count, b.nE), 128, smem, s>>>(b.arena, b.stride, d_tasks, d_rows, d_optr, d_ent, begin);
+  k_leafdiag<<<dim3(count, b.nE), NEGF_LD_THREADS, smem, s>>>(b.arena, b.stride, d_tasks, d_rows, d_optr, d_ent, begin);
   ++launches;
 }
 
