@@ -764,6 +764,54 @@ Plan build_plan(ProblemDesc desc) {
           {static_cast<int>(rel / I.K), P.h_val[q]});
     }
   }
+  // Structural nonzero column hull [lo, hi) of every coupling block A_{x,S[q]}
+  // (and so of Psi_{x,S[q]} = -inv_x A_{x,S[q]}): the original -H / Sigma^r
+  // entries, then, in fold order, the Schur fill A_{jp,jq} += Psi_{x,jp}^T
+  // A_{x,jq} whose columns are those of A_{x,jq}.  Columns outside it are
+  // exact zeros, so the row products' inner sums skip them.
+  std::vector<std::vector<std::array<int, 2>>> nzr(static_cast<std::size_t>(nc));
+  {
+    std::vector<std::pair<int64_t, int>> ar;
+    for (int c = 0; c < nc; ++c) {
+      const ClusterInfo& I = B.I(c);
+      nzr[static_cast<std::size_t>(c)].resize(I.S.size());
+      for (std::size_t q = 0; q < I.S.size(); ++q) nzr[static_cast<std::size_t>(c)][q] = {B.msz(I.S[q]), 0};
+      if (I.K > 0 && I.m > 0) ar.push_back({I.off_arow, c});
+    }
+    std::sort(ar.begin(), ar.end());
+    auto mark = [&](int64_t pos) {
+      auto it = std::upper_bound(ar.begin(), ar.end(), std::make_pair(pos, std::numeric_limits<int>::max()));
+      if (it == ar.begin()) return;
+      --it;
+      const ClusterInfo& I = B.I(it->second);
+      if (pos >= I.off_arow + int64_t(I.m) * I.K) return;
+      const int col = static_cast<int>((pos - I.off_arow) % I.K);
+      for (std::size_t q = 0; q < I.S.size(); ++q)
+        if (col >= I.s_col[q] && col < I.s_col[q] + B.msz(I.S[q])) {
+          auto& r = nzr[static_cast<std::size_t>(it->second)][q];
+          const int l = static_cast<int>(col - I.s_col[q]);
+          r[0] = std::min(r[0], l);
+          r[1] = std::max(r[1], l + 1);
+          return;
+        }
+    };
+    for (int64_t pos : P.h_pos) mark(pos);
+    for (int64_t pos : P.sr_slot_pos) mark(pos);
+    for (int x : t.fold_order()) {
+      const ClusterInfo& X = B.I(x);
+      for (std::size_t p = 0; p < X.S.size(); ++p)
+        for (std::size_t q = p + 1; q < X.S.size(); ++q) {
+          const auto& src = nzr[static_cast<std::size_t>(x)][q];
+          if (src[0] >= src[1]) continue;
+          const int jp = X.S[p];
+          const int qq = find_pos(B.I(jp).S, X.S[q]);
+          if (qq < 0) fail(kInternal, "plan: fill block missing from S");
+          auto& r = nzr[static_cast<std::size_t>(jp)][static_cast<std::size_t>(qq)];
+          r[0] = std::min(r[0], src[0]);
+          r[1] = std::max(r[1], src[1]);
+        }
+    }
+  }
   // Woodbury diagonals of the sparse, never-referenced, unseeded leaves
   // (LeafDiagTask): per leaf its boundary rows T and, per mode, the gathered
   // upper triangle of M.
@@ -999,14 +1047,18 @@ Plan build_plan(ProblemDesc desc) {
           // symmetric form: block pair (k, j) once, in the task of the later
           // one, from 2 Psi_k; the diagonal block from Psi_j
           if (sym && static_cast<int>(kk) > jpos) continue;
-          const int64_t a = (sym && static_cast<int>(kk) < jpos ? X.off_psi2 : X.off_psi) + X.s_col[kk];
-          if (k == j) B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N, B.I(j).off_gd, B.msz(j), +1);
+          const auto nz = nzr[static_cast<std::size_t>(x)][kk];
+          if (nz[0] >= nz[1]) continue;  // Psi_{x,k} == 0
+          const int lo = nz[0], kn = nz[1] - nz[0];
+          const int64_t a = (sym && static_cast<int>(kk) < jpos ? X.off_psi2 : X.off_psi) + X.s_col[kk] + lo;
+          if (k == j) B.add_term(T, kn, OP_N, a, X.K, OP_N, B.I(j).off_gd + int64_t(lo) * B.msz(j), B.msz(j), +1);
           else if (B.lev(k) < B.lev(j))
-            B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N,
-                       B.I(k).off_grow + B.col_of(B.I(k).gcols, B.I(k).gcol_off, j), B.I(k).WG, +1);
+            B.add_term(T, kn, OP_N, a, X.K, OP_N,
+                       B.I(k).off_grow + int64_t(lo) * B.I(k).WG + B.col_of(B.I(k).gcols, B.I(k).gcol_off, j),
+                       B.I(k).WG, +1);
           else
-            B.add_term(T, B.msz(k), OP_N, a, X.K, OP_T,
-                       B.I(j).off_grow + B.col_of(B.I(j).gcols, B.I(j).gcol_off, k), B.I(j).WG, +1);
+            B.add_term(T, kn, OP_N, a, X.K, OP_T,
+                       B.I(j).off_grow + B.col_of(B.I(j).gcols, B.I(j).gcol_off, k) + lo, B.I(j).WG, +1);
         }
         if (!X.full_g && X.off_gpart >= 0) {  // rows feed only diag(G_xx): fused, not stored
           int gb = 0;
@@ -1030,8 +1082,12 @@ Plan build_plan(ProblemDesc desc) {
       if (!X.full_g) continue;
       const int tb = static_cast<int>(T.size());
       for (std::size_t kk = 0; kk < X.S.size(); ++kk)
-        B.add_term(T, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_T,
-                   X.off_grow + B.col_of(X.gcols, X.gcol_off, X.S[kk]), X.WG, +1);
+      {
+        const auto nz = nzr[static_cast<std::size_t>(x)][kk];
+        if (nz[0] >= nz[1]) continue;
+        B.add_term(T, nz[1] - nz[0], OP_N, X.off_psi + X.s_col[kk] + nz[0], X.K, OP_T,
+                   X.off_grow + B.col_of(X.gcols, X.gcol_off, X.S[kk]) + nz[0], X.WG, +1);
+      }
       B.pend_diag.mirror = 1;  // G_xx = inv_x + Psi G_{x,S}^T: complex symmetric
       B.gemm_task(X.m, X.m, X.off_gd, X.m, MODE_INIT, X.off_d, X.m, tb);
     }
@@ -1156,14 +1212,18 @@ Plan build_plan(ProblemDesc desc) {
           for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
             const int k = X.S[kk];
             if (psym && static_cast<int>(kk) > jpos) continue;
-            const int64_t a = (psym && static_cast<int>(kk) < jpos ? X.off_psi2 : X.off_psi) + X.s_col[kk];
-            if (k == j) B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N, B.I(j).off_pd, B.msz(j), +1);
+            const auto nz = nzr[static_cast<std::size_t>(x)][kk];
+            if (nz[0] >= nz[1]) continue;  // Psi_{x,k} == 0
+            const int lo = nz[0], kn = nz[1] - nz[0];
+            const int64_t a = (psym && static_cast<int>(kk) < jpos ? X.off_psi2 : X.off_psi) + X.s_col[kk] + lo;
+            if (k == j) B.add_term(T, kn, OP_N, a, X.K, OP_N, B.I(j).off_pd + int64_t(lo) * B.msz(j), B.msz(j), +1);
             else if (B.lev(k) < B.lev(j))
-              B.add_term(T, B.msz(k), OP_N, a, X.K, OP_N,
-                         B.I(k).off_prow + B.col_of(B.I(k).pcols, B.I(k).pcol_off, j), B.I(k).WP, +1);
+              B.add_term(T, kn, OP_N, a, X.K, OP_N,
+                         B.I(k).off_prow + int64_t(lo) * B.I(k).WP + B.col_of(B.I(k).pcols, B.I(k).pcol_off, j),
+                         B.I(k).WP, +1);
             else
-              B.add_term(T, B.msz(k), OP_N, a, X.K, OP_H,
-                         B.I(j).off_prow + B.col_of(B.I(j).pcols, B.I(j).pcol_off, k), B.I(j).WP, -1);
+              B.add_term(T, kn, OP_N, a, X.K, OP_H,
+                         B.I(j).off_prow + B.col_of(B.I(j).pcols, B.I(j).pcol_off, k) + lo, B.I(j).WP, -1);
           }
           if (!X.full_p && X.off_ppart >= 0) {  // rows feed only diag(P_xx): fused, not stored
             int gb = 0;
@@ -1188,8 +1248,12 @@ Plan build_plan(ProblemDesc desc) {
         const int tb = static_cast<int>(T.size());
         if (X.has_nd) B.add_term(T, X.m, OP_N, X.off_d, X.m, OP_N, X.off_nd, X.m, +1);
         for (std::size_t kk = 0; kk < X.S.size(); ++kk)
-          B.add_term(T, B.msz(X.S[kk]), OP_N, X.off_psi + X.s_col[kk], X.K, OP_H,
-                     X.off_prow + B.col_of(X.pcols, X.pcol_off, X.S[kk]), X.WP, -1);
+        {
+          const auto nz = nzr[static_cast<std::size_t>(x)][kk];
+          if (nz[0] >= nz[1]) continue;
+          B.add_term(T, nz[1] - nz[0], OP_N, X.off_psi + X.s_col[kk] + nz[0], X.K, OP_H,
+                     X.off_prow + B.col_of(X.pcols, X.pcol_off, X.S[kk]) + nz[0], X.WP, -1);
+        }
         B.pend_diag.mirror = 2;  // P_xx = G^<_xx: anti-Hermitian
         B.gemm_task(X.m, X.m, X.off_pd, X.m, MODE_SET, 0, 0, tb);
       }
