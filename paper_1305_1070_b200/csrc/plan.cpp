@@ -948,22 +948,42 @@ Plan build_plan(ProblemDesc desc) {
       const bool sparse_done = had_sparse[q++];
       const ClusterInfo& J = B.I(jp);
       const int tb = static_cast<int>(T.size());
+      const int pq = jp == jq ? -1 : find_pos(J.S, jq);
+      if (jp != jq && pq < 0) fail(kInternal, "plan: fill block missing from S");
+      const bool add = jp == jq || J.s_orig[static_cast<std::size_t>(pq)] || sparse_done;
+      // An accumulating target is updated only on the hull of its terms'
+      // nonzero rows (columns of Psi_{i,jp}) x columns (of A_{i,jq}); a pure
+      // fill block written by this task alone keeps its full extent (zeros).
+      int rlo = B.msz(jp), rhi = 0, clo = B.msz(jq), chi = 0;
+      for (const auto& c3 : kv.second) {
+        if (spsi_of[static_cast<std::size_t>(c3[0])] >= 0) continue;
+        const auto& nr = nzr[static_cast<std::size_t>(c3[0])][static_cast<std::size_t>(c3[1])];
+        const auto& nq = nzr[static_cast<std::size_t>(c3[0])][static_cast<std::size_t>(c3[2])];
+        rlo = std::min(rlo, nr[0]); rhi = std::max(rhi, nr[1]);
+        clo = std::min(clo, nq[0]); chi = std::max(chi, nq[1]);
+      }
+      if (jp == jq) {  // square diagonal sub-block (mirror)
+        rlo = clo = std::min(rlo, clo);
+        rhi = chi = std::max(rhi, chi);
+      }
+      if (!add || rlo >= rhi || clo >= chi) {
+        rlo = 0; rhi = B.msz(jp); clo = 0; chi = B.msz(jq);
+      }
       for (const auto& c3 : kv.second) {
         if (spsi_of[static_cast<std::size_t>(c3[0])] >= 0) continue;
         const ClusterInfo& X = B.I(c3[0]);
-        B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]], X.K, OP_N, X.off_arow + X.s_col[c3[2]], X.K, +1);
+        B.add_term(T, X.m, OP_T, X.off_psi + X.s_col[c3[1]] + rlo, X.K, OP_N, X.off_arow + X.s_col[c3[2]] + clo, X.K,
+                   +1);
       }
       if (static_cast<int>(T.size()) == tb) continue;  // leaves only: done by the sparse op
       if (jp == jq) {  // A_jj += sum Psi^T A_{i,j}: complex symmetric
         B.pend_diag.mirror = 1;
-        B.gemm_task(J.m, J.m, J.off_d, J.m, MODE_ADD, 0, 0, tb);
+        B.gemm_task(rhi - rlo, rhi - rlo, J.off_d + int64_t(rlo) * J.m + rlo, J.m, MODE_ADD, 0, 0, tb);
       } else {
-        const int p = find_pos(J.S, jq);
-        if (p < 0) fail(kInternal, "plan: fill block missing from S");
         // a pure fill block is produced by this single gather task (or
         // started by the sparse op, then accumulated)
-        B.gemm_task(J.m, B.msz(jq), J.off_arow + J.s_col[p], J.K,
-                    (J.s_orig[p] || sparse_done) ? MODE_ADD : MODE_SET, 0, 0, tb);
+        B.gemm_task(rhi - rlo, chi - clo, J.off_arow + int64_t(rlo) * J.K + J.s_col[static_cast<std::size_t>(pq)] + clo,
+                    J.K, add ? MODE_ADD : MODE_SET, 0, 0, tb);
       }
     }
     B.close();
