@@ -269,7 +269,6 @@ double grid_tiles(int arr, int m, int n, int r0, int r1, int c0, int c1, int tas
 }  // namespace
 
 void tile_task(int task, int m, int n, std::vector<GemmTile>& out) {
-  static const bool uniform_only = getenv("NEGF_TILE_UNIFORM") != nullptr;  // A/B experiments
   // Uniform grids.
   int best_arr = 0;
   double best = -1.0;
@@ -305,7 +304,7 @@ void tile_task(int task, int m, int n, std::vector<GemmTile>& out) {
       mixed += std::min(c0, c2);
     }
   }
-  if (!uniform_only && mixed >= 0 && mixed < best - 1e-9) {
+  if (mixed >= 0 && mixed < best - 1e-9) {
     grid_tiles(0, m, n, 0, M32, 0, N32, task, &out);
     if (M32 < m) grid_tiles(bot_arr, m, n, M32, m, 0, n, task, &out);
     if (N32 < n && M32 > 0) {
