@@ -278,8 +278,8 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         launch_spsi(b, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row, g->d_spsi_val, op.begin, op.count, s, L);
         break;
       case K_LEAFDIAG:
-        launch_leafdiag(b, g->d_ld, P.ld_tasks.data(), g->d_ld_rows, g->d_ld_optr, g->d_ld_entries, op.begin,
-                        op.count, s, L);
+        launch_leafdiag(b, g->d_ld, P.ld_tasks.data(), g->d_ld_rows, g->d_ld_optr, P.ld_optr.data(),
+                        g->d_ld_entries, op.begin, op.count, s, L);
         break;
       case K_SSCHUR:
         launch_sschur(b, g->d_sschur, g->d_sschur_contrib, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row,

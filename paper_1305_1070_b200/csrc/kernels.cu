@@ -1729,21 +1729,28 @@ __global__ void __launch_bounds__(NEGF_LD_THREADS) k_leafdiag(double2* arena, in
   const int* T = trows + tk.t_begin;
   const int* op = optr + tk.out_begin;
   const int nO = nT * (nT + 1) / 2;
+  // entry products first, all entries in parallel (independent loads) into
+  // the W area (free until the W staging below), then per-output sums in the
+  // fixed entry order
+  const int e0 = op[0], ne = op[nO] - e0;
+  double2* prod = W;
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    const LeafDiagEntry en = ent[e0 + e];
+    double2 v = base[en.pos];
+    if (en.flag) v = make_double2(-v.x, v.y);
+    const double* cf = reinterpret_cast<const double*>(&en.coef);  // std::complex: (re, im)
+    prod[e] = cmul(make_double2(cf[0], cf[1]), v);
+  }
+  __syncthreads();
   for (int o = threadIdx.x; o < nO; o += blockDim.x) {
     double2 acc = make_double2(0.0, 0.0);
-    int out = 0;
-    for (int e = op[o]; e < op[o + 1]; ++e) {
-      const LeafDiagEntry en = ent[e];
-      double2 v = base[en.pos];
-      if (en.flag) v = make_double2(-v.x, v.y);
-      const double* cf = reinterpret_cast<const double*>(&en.coef);  // std::complex: (re, im)
-      acc = cadd(acc, cmul(make_double2(cf[0], cf[1]), v));
-      out = en.out;
-    }
+    for (int e = op[o]; e < op[o + 1]; ++e) acc = cadd(acc, prod[e - e0]);
+    const int out = ent[op[o]].out;
     const int i1 = out >> 16, i2 = out & 0xffff;
     M[i1 * wp + i2] = acc;
     if (i1 != i2) M[i2 * wp + i1] = tk.mode == 0 ? acc : make_double2(-acc.x, acc.y);
   }
+  __syncthreads();
   for (int idx = threadIdx.x; idx < m * nT; idx += blockDim.x) {
     const int r = idx / nT, i = idx - r * nT;
     W[r * wp + i] = base[tk.off_inv + int64_t(r) * m + T[i]];
@@ -1778,13 +1785,14 @@ __global__ void __launch_bounds__(NEGF_LD_THREADS) k_leafdiag(double2* arena, in
 }
 
 void launch_leafdiag(const BatchArgs& b, const LeafDiagTask* d_tasks, const LeafDiagTask* h_tasks,
-                     const int* d_rows, const int* d_optr, const LeafDiagEntry* d_ent, int begin, int count,
-                     cudaStream_t s, int64_t& launches) {
+                     const int* d_rows, const int* d_optr, const int* h_optr, const LeafDiagEntry* d_ent, int begin,
+                     int count, cudaStream_t s, int64_t& launches) {
   if (count <= 0) return;
   size_t smem = 0;
   for (int i = begin; i < begin + count; ++i) {
     const LeafDiagTask& t = h_tasks[i];
-    smem = std::max(smem, sizeof(double2) * size_t(t.nT + t.m) * (t.nT | 1));
+    const size_t ne = size_t(h_optr[t.out_begin + t.nT * (t.nT + 1) / 2] - h_optr[t.out_begin]);
+    smem = std::max(smem, sizeof(double2) * (size_t(t.nT) * (t.nT | 1) + std::max(size_t(t.m) * (t.nT | 1), ne)));
   }
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) cudaFuncSetAttribute(k_leafdiag, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

@@ -45,8 +45,8 @@ void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurCo
                    const SpsiTask* d_spsi, const int* d_colptr, const int* d_rows, const double2* d_vals,
                    const int* d_rc, int begin, int count, cudaStream_t s, int64_t& launches);
 void launch_leafdiag(const BatchArgs& b, const LeafDiagTask* d_tasks, const LeafDiagTask* h_tasks,
-                     const int* d_rows, const int* d_optr, const LeafDiagEntry* d_ent, int begin, int count,
-                     cudaStream_t s, int64_t& launches);
+                     const int* d_rows, const int* d_optr, const int* h_optr, const LeafDiagEntry* d_ent, int begin,
+                     int count, cudaStream_t s, int64_t& launches);
 void launch_diag(const BatchArgs& b, const DiagTask* d_tasks, const GemmTerm* d_terms, int begin,
                  int count, cudaStream_t s, int64_t& launches);
 void launch_scale(const BatchArgs& b, const ScaleTask* d_tasks, int begin, int count,
