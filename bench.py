@@ -102,6 +102,16 @@ def make_workload(n_ranks: int, per_rank: int):
     return devices.config2(n_energies=n_ranks * per_rank)
 
 
+def bench_config(w, world: int, per_rank: int) -> dict:
+    """The workload description both arms print (identical dicts, so the
+    driver can match the reference arm's line with ours)."""
+    return {"workload": w.name, "description": w.description, "n_dofs": w.n,
+            "energy_grid": f"{world * per_rank} uniform points on [0, 0.4] eV, eta = 1e-6 (leads), "
+                           f"rank r owns the contiguous slice of {per_rank}",
+            "energies_per_gpu": per_rank,
+            "l2": "inputs larger than L2: a step streams all per-energy arenas (tens of GiB) through HBM"}
+
+
 def ref_problem_file(w, idx: np.ndarray, path: str) -> None:
     """The reference-arm / cpu_baseline input: the same arrays, in the
     reference's own terms (contacts + phonon diagonal)."""
@@ -153,7 +163,7 @@ def bench_reference(args, rank: int, world: int) -> None:
     if not refio.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver not built"}))
         return
-    w = make_workload(1, args.energies)
+    w = make_workload(world, args.energies)
     cores = host_cores()
     per_step = cores  # one energy point per core per step (bounded sample)
     with tempfile.TemporaryDirectory() as tmp:
@@ -170,8 +180,10 @@ def bench_reference(args, rank: int, world: int) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic",
-        "config": {"workload": w.name, "n_dofs": w.n, "energies_per_step": per_step,
-                   "solver": "reference hsc_fold+hsc_gless (oracle/_ref, OpenBLAS-backed dense shim), std::thread energy pool"},
+        "config": bench_config(w, world, args.energies),
+        "step": {"energies_per_step": per_step,
+                 "solver": "reference hsc_fold+hsc_gless (oracle/_ref, OpenBLAS-backed dense shim), "
+                           "std::thread energy pool (solve_all, run.cpp:218-264)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -190,6 +202,61 @@ def level_breakdown(ops, op_ms, energies_timed, steps):
             if ms > 0:
                 out[f"{kname}: {cname}"] = {"ms_per_step": ms / steps, "tflops": fl / (ms * 1e-3) / 1e12,
                                              "frac": fl / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS}
+    return out
+
+
+def bench_fullsize(cfg: int, local_rank: int, reps: int = 2) -> dict:
+    """One full-size BASELINE config beside the headline (config 4: 1024 x
+    1024, 1024-wide top separators; config 5: 512 x 512 + phonon): a batch at
+    the device's capacity, spread over the config's energy grid, device-
+    resident energies, contact self-energies built on the GPU inside the
+    timed region; one warm-up batch, then `reps` timed batches (CUDA events on
+    the solver stream)."""
+    import torch
+
+    from paper_1305_1070_b200 import devices, negf
+
+    dev = torch.device("cuda", local_rank)
+    w = devices.config4() if cfg == 4 else devices.config5()
+    t0 = time.perf_counter()
+    plan = negf.HscPlan(w.problem)
+    plan_s = time.perf_counter() - t0
+    info = plan.info()
+    solver = negf.HscGpuSolver(plan, device=local_rank)
+    solver.set_residual_check(False)
+    B = solver.capacity
+    idx = np.linspace(0, len(w.energies) - 1, B).round().astype(np.int64)
+    E = torch.from_numpy(w.energies[idx].copy()).to(dev)
+    W = torch.from_numpy(w.weights[idx].copy()).to(dev)
+    gen = devices.GpuSelfEnergies(w, device=local_rank, max_energy_batch=B)
+    stream = torch.cuda.ExternalStream(solver.stream_ptr, device=dev)
+    with torch.cuda.stream(stream):
+        SR, SL = gen(E)
+        solver.solve_device(E, W, SR, SL, sync=False)
+        torch.cuda.synchronize(dev)
+        solver.profile(True)
+        solver.profile_read(reset=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            SR, SL = gen(E, SR, SL)
+            solver.solve_device(E, W, SR, SL, sync=False)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / reps
+    ks = solver.profile_read(reset=True)
+    solver.profile(False)
+    solver.check()
+    gf = info.exec_flops / 1e9
+    out = {"workload": w.name, "n_dofs": w.n, "clusters": info.n_clusters, "max_block": info.max_block,
+           "value": B / (ms / 1e3), "unit": UNIT, "batch": B, "ms_per_batch": ms, "timed_batches": reps,
+           "exec_gflop_per_energy": gf, "ref_ledger_gflop_per_energy": info.ref_ledger_flops / 1e9,
+           "fp64_tflops_step": gf * B / ms, "fp64_peak_frac_step": gf * B / ms / FP64_PEAK_TFLOPS,
+           "kernels_ms_per_batch": {k: round(v["ms"] / reps, 2) for k, v in ks.items()},
+           "plan_seconds": plan_s, "max_real_residual": solver.max_real_residual}
+    del solver, plan, gen, SR, SL
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
     return out
 
 
@@ -420,6 +487,16 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
                "note": "layered RGF on the same GPU and inputs (one timed step, rank-local)"}
         del rs, rplan
 
+    extra = {}
+    if world == 1 and args.extra_configs:
+        del E, Wt, SR, SL
+        torch.cuda.empty_cache()
+        for c in (int(x) for x in args.extra_configs.split(",")):
+            try:
+                extra[f"config{c}"] = bench_fullsize(c, local_rank)
+                log(f"[bench] config {c}: {extra[f'config{c}']['value']:.2f} {UNIT}")
+            except Exception as exc:  # reported, never fatal for the headline
+                extra[f"config{c}"] = {"error": str(exc)}
     if rank != 0:
         return
     g = kstats["gemm"]
@@ -452,20 +529,16 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic",
-        "config": {"workload": w.name, "description": w.problem and w.description, "n_dofs": w.n,
-                   "clusters": info.n_clusters, "levels": info.levels, "max_block": info.max_block,
-                   "energies_per_step_per_gpu": per_rank, "energy_grid_points": len(w.energies),
-                   "parallelism": (f"energy-sharded x{world}, density reduced once per step "
-                                   f"({'C-ABI NCCL all-gather + rank-ordered sum' if reduce_mode == 'negf-nccl' else 'torch.distributed all-gather + rank-ordered sum'})")
-                                  if world > 1 else "single GPU",
-                   "l2": f"inputs larger than L2 (per-energy arena {info.arena_bytes_per_energy / 2**20:.0f} MiB "
-                         f"x {per_rank} energies)",
-                   "exec_gflop_per_energy": info.exec_flops / 1e9,
-                   "ref_ledger_gflop_per_energy": info.ref_ledger_flops / 1e9,
-                   "plan_seconds": plan_s,
-                   "max_real_residual": max_resid,
-                   "fp64_tflops_step": step_tflops,
-                   "fp64_peak_frac_step": step_tflops / FP64_PEAK_TFLOPS},
+        "config": bench_config(w, world, per_rank),
+        "parallelism": (f"energy-sharded x{world}, density reduced once per step "
+                        f"({'C-ABI NCCL all-gather + rank-ordered sum' if reduce_mode == 'negf-nccl' else 'torch.distributed all-gather + rank-ordered sum'})")
+                       if world > 1 else "single GPU",
+        "plan": {"clusters": info.n_clusters, "levels": info.levels, "max_block": info.max_block,
+                 "arena_mib_per_energy": info.arena_bytes_per_energy / 2**20,
+                 "exec_gflop_per_energy": info.exec_flops / 1e9,
+                 "ref_ledger_gflop_per_energy": info.ref_ledger_flops / 1e9,
+                 "plan_seconds": plan_s, "max_real_residual": max_resid,
+                 "fp64_tflops_step": step_tflops, "fp64_peak_frac_step": step_tflops / FP64_PEAK_TFLOPS},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": gemm_tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": "k_gemm (grouped complex GEMM, DMMA.8x8x4)",
@@ -483,12 +556,47 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
                           "note": "energies/weights in; contact self-energies built on the GPU "
                                   "(analytic lead modes + lesser fill) inside the timed region"},
         "rgf_gpu": rgf,
+        "extra_configs": extra or None,
         "gpu_launches": launches_timed,
         "clocks": clk,
     }
     print(json.dumps(out))
     log(f"[bench] {value:.1f} {UNIT}  ({ms_max:.2f} ms/step, gemm {gemm_tflops:.2f} TF/s, step {step_tflops:.2f} TF/s, "
         f"e2e {e2e_value:.1f}, launches/step {launches_per_step})")
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: one rank per GPU through
+    torch.distributed.run on 127.0.0.1 (the form the driver uses for N > 1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"[bench] launching {n} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank: int, world: int) -> None:
+    """Process-group plumbing of the N-rank run without a GPU: gloo barrier +
+    max-over-ranks reduction of a per-rank number, rank 0 prints the line."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "max_over_ranks": float(t.item()),
+                          "backend": "gloo" if world > 1 else "none"}))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main() -> None:
@@ -500,12 +608,21 @@ def main() -> None:
     ap.add_argument("--energies", type=int, default=256, help="energy points per GPU per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rgf", action="store_true", help="skip the GPU RGF comparison line")
+    ap.add_argument("--extra-configs", default="4,5",
+                    help="full-size BASELINE configs timed beside the headline at N=1 ('' = none)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / process-group check only (gloo without CUDA): no solve")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         bench_reference(args, rank, world)
+        return
+    if args.dry_run:
+        dry_run(args, rank, world)
         return
     if world > 1:
         import torch

@@ -165,22 +165,33 @@ int negf_gpu_solve_batch(negf_gpu* g, int n_energies, const double* energies,
                          double* gless_diag, negf_status* st);
 /* Same, with every input and output already resident in device memory
  * (d_gr/d_gless nullable).  Runs on the handle's stream; no host sync unless
- * `sync` is nonzero (errors are then reported by negf_gpu_check). */
+ * `sync` is nonzero (errors are then reported by negf_gpu_check).  The device
+ * status is sticky: every solve since the last negf_gpu_check / synchronous
+ * solve merges into it (lowest energy index first), and only reading it
+ * clears it. */
 int negf_gpu_solve_batch_device(negf_gpu* g, int n_energies, const double* d_energies,
                                 const double* d_weights, const double* d_sigma_r,
                                 const double* d_sigma_lesser, int first_energy_index,
                                 double* d_gr, double* d_gless, int sync, negf_status* st);
 int negf_gpu_check(negf_gpu* g, negf_status* st);
 /* density_out[n] = (1/2pi) sum_k w_k Im G^<_jj(E_k) over all solved energies
- * (observables.cpp:71-91).  reset != 0 zeroes the accumulator afterwards. */
+ * (observables.cpp:71-91): this rank's partial, or the cross-rank sum when
+ * negf_gpu_allreduce_density ran after the last solve.  reset != 0 zeroes
+ * the accumulator afterwards. */
 int negf_gpu_density(negf_gpu* g, double* density_out, int reset, negf_status* st);
 void* negf_gpu_stream(negf_gpu* g);       /* cudaStream_t of the handle */
-void* negf_gpu_density_device(negf_gpu* g); /* double[n] accumulator (unscaled) */
+void* negf_gpu_density_device(negf_gpu* g); /* double[n] this rank's partial (unscaled) */
 /* electron_density's Re-residual guard (observables.cpp:79-84): mode 1
  * (default) raises NEGF_RESIDUAL_TOO_LARGE like the reference; mode 0 only
  * records the largest |Re G^<_jj| / |G^<_jj| (DensityMap::max_real_residual). */
 int negf_gpu_set_residual_check(negf_gpu* g, int mode);
 double negf_gpu_max_real_residual(negf_gpu* g);
+/* Lowest (energy index, dof) whose |Re G^<_jj| > 1e-8 |G^<_jj| since the last
+ * reset, whatever the mode (the quantity electron_density checks first,
+ * observables.cpp:79-84): returns 1 and fills the (nullable) outputs, else 0.
+ * Lets a multi-rank sweep raise ResidualTooLarge only after every rank's
+ * solver errors are settled (run.cpp:258-291). */
+int negf_gpu_residual_violation(negf_gpu* g, int32_t* energy_index, int32_t* dof, int reset);
 
 /* Kernel launches issued by the last solve call (ours only). */
 int64_t negf_gpu_last_launches(const negf_gpu* g);
@@ -206,7 +217,9 @@ void negf_gpu_destroy(negf_gpu* g);
  * torch.distributed broadcast of the 128-byte id). */
 int negf_nccl_unique_id(char id_out[128], negf_status* st);
 int negf_gpu_nccl_init(negf_gpu* g, const char id[128], int nranks, int rank, negf_status* st);
-/* In-place sum of the unscaled density accumulators across ranks.  Default
+/* Sum of the ranks' unscaled density partials into a separate buffer (the
+ * partials keep accumulating; negf_gpu_density returns the sum until the
+ * next solve).  Default
  * (ordered): ncclAllGather of the partials + a device sum in
  * rank order, bit-reproducible for any rank count and NCCL algorithm;
  * negf_gpu_set_ordered_reduce(g, 0) selects a plain ncclAllReduce. */

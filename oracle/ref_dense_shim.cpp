@@ -9,9 +9,13 @@
 // partition.cpp, block.cpp, ...) compile and run unmodified on top of it:
 //   * matmul     (dense.cpp:36-47)  -> OpenBLAS ZGEMM (ILP64, scipy build in
 //                                      numpy.libs), charge rows*inner*cols;
-//   * inverse    (dense.cpp:49-81)  -> ZGETRF (row partial pivoting of the
-//                                      row-major matrix) + ZGETRI, singular
-//                                      when |u_kk| <= 1e-13 * max|a| (first k),
+//   * inverse    (dense.cpp:49-81)  -> blocked right-looking LU with row
+//                                      partial pivoting on |z| (Eigen
+//                                      PartialPivLU's pivot score, dense.cpp:55;
+//                                      ZGETRF's IZAMAX would score |Re|+|Im|),
+//                                      ZTRSM/ZGEMM trailing updates, then
+//                                      ZGETRI; singular when
+//                                      |u_kk| <= 1e-13 * max|a| (first k),
 //                                      charge n^3;
 //   * helpers    (dense.cpp:83-230) -> plain loops, same charges.
 #include "negf/dense.hpp"
@@ -30,6 +34,10 @@ void scipy_zgemm_64_(const char* transa, const char* transb, const long* m,
                      const long* ldc, long la, long lb);
 void scipy_zgetrf_64_(const long* m, const long* n, void* a, const long* lda,
                       long* ipiv, long* info);
+void scipy_ztrsm_64_(const char* side, const char* uplo, const char* transa,
+                     const char* diag, const long* m, const long* n,
+                     const void* alpha, const void* a, const long* lda, void* b,
+                     const long* ldb, long l1, long l2, long l3, long l4);
 void scipy_zgetri_64_(const long* n, void* a, const long* lda,
                       const long* ipiv, void* work, const long* lwork,
                       long* info);
@@ -46,6 +54,51 @@ double max_abs(const CMatrix& m) {
   return mx;
 }
 }  // namespace
+
+// LU of the column-major n x n matrix w in place (LAPACK layout: unit L
+// below, U on and above the diagonal, 1-based ipiv), pivoting each column on
+// the largest |z| (first occurrence), as Eigen's PartialPivLU does.  Panels of
+// 32 columns are factored with plain loops; the trailing matrix is updated
+// with ZTRSM + ZGEMM.
+static void lu_abs_pivot(cplx* w, int n, long* ipiv) {
+  const long ln = n;
+  auto at = [&](int i, int j) -> cplx& { return w[static_cast<std::size_t>(j) * n + i]; };
+  constexpr int nb = 32;
+  for (int k0 = 0; k0 < n; k0 += nb) {
+    const int kb = std::min(nb, n - k0);
+    for (int k = k0; k < k0 + kb; ++k) {
+      int p = k;
+      double best = std::abs(at(k, k));
+      for (int i = k + 1; i < n; ++i) {
+        const double v = std::abs(at(i, k));
+        if (v > best) {
+          best = v;
+          p = i;
+        }
+      }
+      ipiv[k] = p + 1;
+      if (p != k)
+        for (int j = 0; j < n; ++j) std::swap(at(k, j), at(p, j));
+      const cplx piv = at(k, k);
+      if (piv != cplx(0.0, 0.0)) {
+        const cplx r = cplx(1.0, 0.0) / piv;
+        for (int i = k + 1; i < n; ++i) at(i, k) *= r;
+      }
+      for (int j = k + 1; j < k0 + kb; ++j) {
+        const cplx ukj = at(k, j);
+        if (ukj == cplx(0.0, 0.0)) continue;
+        for (int i = k + 1; i < n; ++i) at(i, j) -= at(i, k) * ukj;
+      }
+    }
+    const long rest = n - (k0 + kb);
+    if (rest <= 0) continue;
+    const long lkb = kb;
+    const cplx one(1.0, 0.0), mone(-1.0, 0.0);
+    scipy_ztrsm_64_("L", "L", "N", "U", &lkb, &rest, &one, &at(k0, k0), &ln, &at(k0, k0 + kb), &ln, 1, 1, 1, 1);
+    scipy_zgemm_64_("N", "N", &rest, &rest, &lkb, &mone, &at(k0 + kb, k0), &ln, &at(k0, k0 + kb), &ln, &one,
+                    &at(k0 + kb, k0 + kb), &ln, 1, 1);
+  }
+}
 
 bool CMatrix::all_finite() const {
   for (const cplx& v : data_)
@@ -101,7 +154,7 @@ CMatrix inverse(const CMatrix& a, FlopLedger& ledger) {
   std::vector<long> ipiv(static_cast<std::size_t>(n));
   const long ln = n;
   long info = 0;
-  scipy_zgetrf_64_(&ln, &ln, w.data(), &ln, ipiv.data(), &info);
+  lu_abs_pivot(w.data(), n, ipiv.data());
   const double threshold = 1e-13 * max_abs(a);
   for (int i = 0; i < n; ++i) {
     const double mag = std::abs(w[static_cast<std::size_t>(i) * n + i]);

@@ -122,6 +122,12 @@ struct negf_gpu {
   void* comm = nullptr;
   int nranks = 1;
   double* d_gather = nullptr;  // nranks x n partial densities (ordered reduction)
+  // Cross-rank sum of the partials (negf_gpu_allreduce_density); d_density
+  // itself stays this rank's running partial, so later solves and reductions
+  // never count an earlier contribution twice.
+  double* d_reduced = nullptr;
+  bool reduced_valid = false;       // d_reduced is newer than every solve
+  unsigned long long resid_first = ~0ull;  // lowest (energy << 32 | dof) residual key seen
   int64_t launches = 0;
   int residual_mode = 1;
   int ordered_reduce = 1;
@@ -305,14 +311,21 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
 // before validate_sigma's NonSkewHermitianInput (hsc_fold runs first,
 // run.cpp:164-169); ResidualTooLarge is raised only when every energy solved
 // (electron_density runs after solve_all, run.cpp:285-291).
+//
+// The device status is sticky: every solve since the last collect() merges
+// into it (atomicMin keys), so errors of asynchronous calls (sync = 0) are
+// reported by the next negf_gpu_check / synchronous solve; it is cleared only
+// here, once read.
 int collect(negf_gpu* g, negf_status* st) {
   DevStatus h;
   ck(cudaMemcpyAsync(&h, g->d_status, sizeof h, cudaMemcpyDeviceToHost, g->stream), "status read");
   ck(cudaStreamSynchronize(g->stream), "stream sync");
+  reset_status(g);
   const unsigned long long none = ~0ull;
   double worst;
   std::memcpy(&worst, &h.max_resid_bits, sizeof worst);
   g->max_resid = std::max(g->max_resid, worst);
+  g->resid_first = std::min<unsigned long long>(g->resid_first, h.residual_key);
   const long long es = h.singular_key == none ? -1 : static_cast<long long>(h.singular_key >> 40);
   const long long en = h.nonskew_key == none ? -1 : static_cast<long long>(h.nonskew_key >> 32);
   if (es >= 0 && (en < 0 || es <= en)) {
@@ -588,7 +601,8 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
                               P.seeded_ids.size() * 16;
     size_t free_b = 0, total_b = 0;
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-    int cap = static_cast<int>(std::min<size_t>(size_t(0.85 * double(free_b)) / per_energy, 1 << 20));
+    // energies of a batch go in gridDim.y / gridDim.z: at most kMaxGridYZ
+    int cap = static_cast<int>(std::min<size_t>(size_t(0.85 * double(free_b)) / per_energy, kMaxGridYZ));
     if (max_energy_batch > 0) cap = std::min(cap, max_energy_batch);
     if (cap < 1)
       throw CudaFail{NEGF_OUT_OF_MEMORY, "one energy point needs " + std::to_string(per_energy) +
@@ -630,8 +644,8 @@ int negf_gpu_solve_batch(negf_gpu* g, int nE, const double* energies, const doub
     if ((sr && !sigma_r) || (sl && !sigma_lesser))
       return set_status(st, NEGF_CONTRACT_VIOLATION, "self-energy values missing");
     g->launches = 0;
+    g->reduced_valid = false;
     ck(cudaSetDevice(g->device), "cudaSetDevice");
-    reset_status(g);
     if (!g->copy_stream) {
       ck(cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking), "stream");
       ck(cudaEventCreateWithFlags(&g->ev_sl, cudaEventDisableTiming), "event");
@@ -692,8 +706,8 @@ int negf_gpu_solve_batch_device(negf_gpu* g, int nE, const double* d_E, const do
     const size_t sr = P.desc.sr_rows.size(), sl = P.desc.sl_rows.size();
     const int n = P.desc.n;
     g->launches = 0;
+    g->reduced_valid = false;
     ck(cudaSetDevice(g->device), "cudaSetDevice");
-    reset_status(g);
     for (int e0 = 0; e0 < nE; e0 += g->capacity) {
       const int m = std::min(g->capacity, nE - e0);
       run_batch(g, m, first + e0, d_E + e0, d_w + e0,
@@ -723,8 +737,12 @@ int negf_gpu_density(negf_gpu* g, double* out, int reset, negf_status* st) {
   if (!g || !out) return set_status(st, NEGF_CONTRACT_VIOLATION, "null argument");
   try {
     const int n = g->plan->desc.n;
-    ck(cudaMemcpyAsync(out, g->d_density, sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
-    if (reset) ck(cudaMemsetAsync(g->d_density, 0, sizeof(double) * n, g->stream), "memset");
+    const double* src = g->reduced_valid ? g->d_reduced : g->d_density;
+    ck(cudaMemcpyAsync(out, src, sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream), "d2h");
+    if (reset) {
+      ck(cudaMemsetAsync(g->d_density, 0, sizeof(double) * n, g->stream), "memset");
+      g->reduced_valid = false;
+    }
     ck(cudaStreamSynchronize(g->stream), "sync");
     for (int i = 0; i < n; ++i) out[i] /= kTwoPi;  // observables.cpp:91
     return ok(st);
@@ -740,6 +758,16 @@ int negf_gpu_set_residual_check(negf_gpu* g, int mode) {
 }
 
 double negf_gpu_max_real_residual(negf_gpu* g) { return g ? g->max_resid : 0.0; }
+
+int negf_gpu_residual_violation(negf_gpu* g, int32_t* energy_index, int32_t* dof, int reset) {
+  if (!g) return 0;
+  const unsigned long long k = g->resid_first;
+  if (reset) g->resid_first = ~0ull;
+  if (k == ~0ull) return 0;
+  if (energy_index) *energy_index = static_cast<int32_t>(k >> 32);
+  if (dof) *dof = static_cast<int32_t>(k & 0xFFFFFFFFull);
+  return 1;
+}
 
 int negf_gpu_profile(negf_gpu* g, int enable) {
   if (!g) return NEGF_CONTRACT_VIOLATION;
@@ -809,6 +837,7 @@ int negf_gpu_nccl_init(negf_gpu* g, const char id[128], int nranks, int rank, ne
   g->nranks = nranks;
   try {
     g->d_gather = dev_alloc<double>(size_t(nranks) * g->plan->desc.n, g->owned);
+    g->d_reduced = dev_alloc<double>(size_t(g->plan->desc.n), g->owned);
   } catch (const CudaFail& f) {
     return set_status(st, f.code, f.msg);
   }
@@ -832,16 +861,18 @@ int negf_gpu_allreduce_density(negf_gpu* g, negf_status* st) {
     const int r = api.allgather(g->d_density, g->d_gather, size_t(n), 8, g->comm, g->stream);
     if (r != 0) return set_status(st, NEGF_NCCL_ERROR, api.err ? api.err(r) : "ncclAllGather failed");
     int64_t L = 0;
-    launch_ordered_sum(g->d_gather, g->nranks, n, g->d_density, g->stream, L);
+    launch_ordered_sum(g->d_gather, g->nranks, n, g->d_reduced, g->stream, L);
     if (cudaStreamSynchronize(g->stream) != cudaSuccess)
       return set_status(st, NEGF_CUDA_ERROR, "sync after allgather failed");
+    g->reduced_valid = true;
     return ok(st);
   }
   // ncclFloat64 = 8, ncclSum = 0 (nccl.h)
-  const int r = api.allreduce(g->d_density, g->d_density, size_t(n), 8, 0, g->comm, g->stream);
+  const int r = api.allreduce(g->d_density, g->d_reduced, size_t(n), 8, 0, g->comm, g->stream);
   if (r != 0) return set_status(st, NEGF_NCCL_ERROR, api.err ? api.err(r) : "ncclAllReduce failed");
   if (cudaStreamSynchronize(g->stream) != cudaSuccess)
     return set_status(st, NEGF_CUDA_ERROR, "sync after allreduce failed");
+  g->reduced_valid = true;
   return ok(st);
 }
 

@@ -36,6 +36,10 @@ struct Failure : std::runtime_error {
   Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 
+// Kernels put the energy index of a batch in gridDim.y / gridDim.z, which
+// CUDA limits to 65535: batch capacities never exceed it.
+constexpr int kMaxGridYZ = 65535;
+
 [[noreturn]] inline void fail(int code, const std::string& msg) {
   throw Failure(code, msg);
 }

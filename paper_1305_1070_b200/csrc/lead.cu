@@ -483,7 +483,7 @@ int negf_lead_create(int device, int w, const double* h00, const double* h01, do
     size_t free_b = 0, total_b = 0;
     ck(cudaMemGetInfo(&free_b, &total_b), "meminfo");
     const int64_t per = P.arena * int64_t(sizeof(double2));
-    int cap = max_energy_batch > 0 ? max_energy_batch : 512;
+    int cap = max_energy_batch > 0 ? std::min(max_energy_batch, kMaxGridYZ) : 512;
     cap = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cap, int64_t(0.4 * free_b) / per)));
     l->capacity = cap;
     l->arena = dev_alloc<double2>(static_cast<size_t>(P.arena) * cap, l->owned);
@@ -627,10 +627,15 @@ int negf_lead_modes_sigma_device(int w, double t_ev, double eta_ev, int n_energi
       ck(cudaMalloc(&sc.sig, sizeof(double2) * need), "sigma_m");
       sc.sig_cap = need;
     }
-    k_modes_lambda<<<dim3((w + 127) / 128, n_energies), 128, 0, s>>>(w, t_ev, eta_ev, d_energies, sc.sig);
+    // the energy index lives in gridDim.y / gridDim.z (<= 65535): chunk
     const int nb = (w + 31) / 32;
-    k_modes_sigma<<<dim3(nb, nb, n_energies), dim3(32, 32), 0, s>>>(w, sc.phi, sc.sig,
-                                                                    reinterpret_cast<double2*>(d_sigma_out), ld_out);
+    for (int e0 = 0; e0 < n_energies; e0 += kMaxGridYZ) {
+      const int m = std::min(kMaxGridYZ, n_energies - e0);
+      k_modes_lambda<<<dim3((w + 127) / 128, m), 128, 0, s>>>(w, t_ev, eta_ev, d_energies + e0,
+                                                             sc.sig + size_t(w) * e0);
+      k_modes_sigma<<<dim3(nb, nb, m), dim3(32, 32), 0, s>>>(
+          w, sc.phi, sc.sig + size_t(w) * e0, reinterpret_cast<double2*>(d_sigma_out) + size_t(ld_out) * e0, ld_out);
+    }
     ck(cudaGetLastError(), "modes launch");
   } catch (const CudaFail& f) {
     return set_status(st, f.code, f.msg);
@@ -656,16 +661,26 @@ int negf_contacts_fill_device(int n_energies, const double* d_energies, double k
       if ((cd.sr_off >= 0 && !d_sigma_r) || (cd.sl_off >= 0 && !d_sigma_lesser))
         return set_status(st, NEGF_CONTRACT_VIOLATION, "null pattern array");
       const int w2 = cd.w * cd.w;
-      k_fill_contact<<<dim3(std::max(1, std::min(64, (w2 + 255) / 256)), n_energies), 256, 0, s>>>(
-          cd.w, reinterpret_cast<const double2*>(cd.d_sigma), cd.ld, cd.sr_off, cd.sl_off, cd.mu_ev, kT_ev,
-          d_energies, reinterpret_cast<double2*>(d_sigma_r), sr_stride, reinterpret_cast<double2*>(d_sigma_lesser),
-          sl_stride);
+      for (int e0 = 0; e0 < n_energies; e0 += kMaxGridYZ) {  // energies in gridDim.y: chunk
+        const int m = std::min(kMaxGridYZ, n_energies - e0);
+        k_fill_contact<<<dim3(std::max(1, std::min(64, (w2 + 255) / 256)), m), 256, 0, s>>>(
+            cd.w, reinterpret_cast<const double2*>(cd.d_sigma) + size_t(cd.ld) * e0, cd.ld, cd.sr_off, cd.sl_off,
+            cd.mu_ev, kT_ev, d_energies + e0,
+            d_sigma_r ? reinterpret_cast<double2*>(d_sigma_r) + size_t(sr_stride) * e0 : nullptr, sr_stride,
+            d_sigma_lesser ? reinterpret_cast<double2*>(d_sigma_lesser) + size_t(sl_stride) * e0 : nullptr,
+            sl_stride);
+      }
     }
     if (n_phonon > 0) {
       if (!d_phonon_gamma) return set_status(st, NEGF_CONTRACT_VIOLATION, "null phonon array");
-      k_fill_phonon<<<dim3(std::max(1, std::min(256, (n_phonon + 255) / 256)), n_energies), 256, 0, s>>>(
-          n_phonon, d_phonon_gamma, ph_sr_off, ph_sl_off, mu_phonon_ev, kT_ev, d_energies,
-          reinterpret_cast<double2*>(d_sigma_r), sr_stride, reinterpret_cast<double2*>(d_sigma_lesser), sl_stride);
+      for (int e0 = 0; e0 < n_energies; e0 += kMaxGridYZ) {
+        const int m = std::min(kMaxGridYZ, n_energies - e0);
+        k_fill_phonon<<<dim3(std::max(1, std::min(256, (n_phonon + 255) / 256)), m), 256, 0, s>>>(
+            n_phonon, d_phonon_gamma, ph_sr_off, ph_sl_off, mu_phonon_ev, kT_ev, d_energies + e0,
+            d_sigma_r ? reinterpret_cast<double2*>(d_sigma_r) + size_t(sr_stride) * e0 : nullptr, sr_stride,
+            d_sigma_lesser ? reinterpret_cast<double2*>(d_sigma_lesser) + size_t(sl_stride) * e0 : nullptr,
+            sl_stride);
+      }
     }
     ck(cudaGetLastError(), "fill launch");
   } catch (const CudaFail& f) {

@@ -331,8 +331,25 @@ int64_t tile_task_sym(int task, int m, std::vector<GemmTile>& out) {
   return area;
 }
 
+namespace {
+// Exact-arithmetic rewrite forms of the plan, each of which can
+// be switched off for A/B parity experiments: NEGF_PLAN_DISABLE is a comma list
+// of mirror_schur, mirror_g, mirror_p, symdiag_g, symdiag_p, woodbury, sparse,
+// hull.
+bool form_on(const char* name) {
+  const char* e = std::getenv("NEGF_PLAN_DISABLE");
+  if (!e) return true;
+  const std::string s = std::string(",") + e + ",";
+  return s.find(std::string(",") + name + ",") == std::string::npos;
+}
+}  // namespace
+
 Plan build_plan(ProblemDesc desc) {
   Plan P;
+  const bool f_mirror_schur = form_on("mirror_schur"), f_mirror_g = form_on("mirror_g"),
+             f_mirror_p = form_on("mirror_p"), f_symdiag_g = form_on("symdiag_g"),
+             f_symdiag_p = form_on("symdiag_p"), f_woodbury = form_on("woodbury"), f_sparse = form_on("sparse"),
+             f_hull = form_on("hull");
   P.desc = std::move(desc);
   const ProblemDesc& d = P.desc;
   const int n = d.n;
@@ -738,6 +755,7 @@ Plan build_plan(ProblemDesc desc) {
       bool orig = true;
       for (char o : I.s_orig) orig = orig && o;
       if (!orig) continue;
+      if (!f_sparse) continue;
       leaf_sparse[static_cast<std::size_t>(c)] = 1;
       leaf_cols[static_cast<std::size_t>(c)].resize(static_cast<std::size_t>(I.K));
       arows.push_back({I.off_arow, c});
@@ -811,6 +829,9 @@ Plan build_plan(ProblemDesc desc) {
         }
     }
   }
+  if (!f_hull)
+    for (int c = 0; c < nc; ++c)
+      for (std::size_t q = 0; q < B.I(c).S.size(); ++q) nzr[static_cast<std::size_t>(c)][q] = {0, B.msz(B.I(c).S[q])};
   // Woodbury diagonals of the sparse, never-referenced, unseeded leaves
   // (LeafDiagTask): per leaf its boundary rows T and, per mode, the gathered
   // upper triangle of M.
@@ -882,7 +903,7 @@ Plan build_plan(ProblemDesc desc) {
   };
   for (int c = 0; c < nc; ++c) {
     const ClusterInfo& I = B.I(c);
-    leaf_wood[static_cast<std::size_t>(c)] = leaf_sparse[static_cast<std::size_t>(c)] && !I.full_g && !I.full_p &&
+    leaf_wood[static_cast<std::size_t>(c)] = f_woodbury && leaf_sparse[static_cast<std::size_t>(c)] && !I.full_g && !I.full_p &&
                                              !I.seeded && !I.has_nd && I.ncols.empty() && I.m > 0 && I.m < 65536;
   }
   // Leaf -> SpsiTask index (leaves' Psi tasks are emitted at level 1, before
@@ -976,7 +997,7 @@ Plan build_plan(ProblemDesc desc) {
       }
       if (static_cast<int>(T.size()) == tb) continue;  // leaves only: done by the sparse op
       if (jp == jq) {  // A_jj += sum Psi^T A_{i,j}: complex symmetric
-        B.pend_diag.mirror = 1;
+        B.pend_diag.mirror = f_mirror_schur ? 1 : 0;
         B.gemm_task(rhi - rlo, rhi - rlo, J.off_d + int64_t(rlo) * J.m + rlo, J.m, MODE_ADD, 0, 0, tb);
       } else {
         // a pure fill block is produced by this single gather task (or
@@ -1056,7 +1077,7 @@ Plan build_plan(ProblemDesc desc) {
     for (int x : xs) {
       const ClusterInfo& X = B.I(x);
       if (leaf_wood[static_cast<std::size_t>(x)]) continue;  // K_LEAFDIAG below
-      const bool sym = !X.full_g && X.off_gpart >= 0 && X.off_psi2 >= 0;
+      const bool sym = f_symdiag_g && !X.full_g && X.off_gpart >= 0 && X.off_psi2 >= 0;
       for (std::size_t jj = 0; jj < X.gcols.size(); ++jj) {
         const int j = X.gcols[jj];
         const int tb = static_cast<int>(T.size());
@@ -1107,7 +1128,7 @@ Plan build_plan(ProblemDesc desc) {
         B.add_term(T, nz[1] - nz[0], OP_N, X.off_psi + X.s_col[kk] + nz[0], X.K, OP_T,
                    X.off_grow + B.col_of(X.gcols, X.gcol_off, X.S[kk]) + nz[0], X.WG, +1);
       }
-      B.pend_diag.mirror = 1;  // G_xx = inv_x + Psi G_{x,S}^T: complex symmetric
+      B.pend_diag.mirror = f_mirror_g ? 1 : 0;  // G_xx = inv_x + Psi G_{x,S}^T: complex symmetric
       B.gemm_task(X.m, X.m, X.off_gd, X.m, MODE_INIT, X.off_d, X.m, tb);
     }
     B.close();
@@ -1221,7 +1242,7 @@ Plan build_plan(ProblemDesc desc) {
         // w - conj(w) = 2i Im(w): each pair once from 2 Psi, imaginary part kept
         // (dmode 3).  The diagonal blocks' own real parts are rounding noise
         // (G^< is anti-Hermitian), so the whole sum keeps only its imaginary part.
-        const bool psym = !X.full_p && X.off_ppart >= 0 && X.off_psi2 >= 0 && X.ncols.empty() && !X.has_nd;
+        const bool psym = f_symdiag_p && !X.full_p && X.off_ppart >= 0 && X.off_psi2 >= 0 && X.ncols.empty() && !X.has_nd;
         for (std::size_t jj = 0; jj < X.pcols.size(); ++jj) {
           const int j = X.pcols[jj];
           const int tb = static_cast<int>(T.size());
@@ -1273,7 +1294,7 @@ Plan build_plan(ProblemDesc desc) {
           B.add_term(T, nz[1] - nz[0], OP_N, X.off_psi + X.s_col[kk] + nz[0], X.K, OP_H,
                      X.off_prow + B.col_of(X.pcols, X.pcol_off, X.S[kk]) + nz[0], X.WP, -1);
         }
-        B.pend_diag.mirror = 2;  // P_xx = G^<_xx: anti-Hermitian
+        B.pend_diag.mirror = f_mirror_p ? 2 : 0;  // P_xx = G^<_xx: anti-Hermitian
         B.gemm_task(X.m, X.m, X.off_pd, X.m, MODE_SET, 0, 0, tb);
       }
       B.close();

@@ -174,19 +174,22 @@ def config1() -> Workload:
                                  0.025, description="2D effective mass 64x32, V~U[0,0.1] seed 0, E=0.05")
 
 
-def config2(n_energies: int = 256) -> Workload:
-    """Quantum-well superlattice 400 x 100, 256 energies in [0, 0.4] (configs[1])."""
-    nx, ny = 400, 100
+def config2(n_energies: int = 256, ny: int = 100, complex_energy: bool = False, nx: int = 400) -> Workload:
+    """Quantum-well superlattice 400 x 100, 256 energies in [0, 0.4] (configs[1]).
+    Smaller ``nx`` / ``ny`` give the reduced superlattices of the dense-truth
+    parity study (same barriers and energy grid; the disorder draws cover
+    nx*ny)."""
     x = np.arange(nx)
     barrier = np.where((x // 10) % 2 == 1, 0.3, 0.0)  # 5 nm = 10 points, wells at the leads
     v = np.repeat(barrier, ny) + (MT19937_64(1).uniform01(nx * ny) - 0.5) * 0.01
     e = uniform_grid(0.0, 0.4, n_energies)
-    return effective_mass_device("cfg2_superlattice_400x100", nx, ny, 0.5, 0.067, v, e, 1e-6, 0.1, 0.0, 0.025,
-                                 description="superlattice 400x100, 0.3 eV barriers/wells of 5 nm, "
-                                             "+-5 meV disorder seed 1, 256 E in [0,0.4]")
+    return effective_mass_device(f"cfg2_superlattice_{nx}x{ny}", nx, ny, 0.5, 0.067, v, e, 1e-6, 0.1, 0.0, 0.025,
+                                 description=f"superlattice {nx}x{ny}, 0.3 eV barriers/wells of 5 nm, "
+                                             "+-5 meV disorder seed 1, 256 E in [0,0.4]",
+                                 complex_energy=complex_energy)
 
 
-def config4(n_energies: int = 1024, nx: int = 1024, ny: int = 1024) -> Workload:
+def config4(n_energies: int = 1024, nx: int = 1024, ny: int = 1024, complex_energy: bool = False) -> Workload:
     """Wide 1024 x 1024 device, sum of 16 Gaussians (configs[3])."""
     r = MT19937_64(3)
     cx = r.uniform01(16) * nx
@@ -197,7 +200,8 @@ def config4(n_energies: int = 1024, nx: int = 1024, ny: int = 1024) -> Workload:
         v += 0.05 * np.exp(-((X - cx[i]) ** 2 + (Y - cy[i]) ** 2) / (2.0 * 20.0 ** 2))
     e = uniform_grid(0.0, 0.3, n_energies)
     return effective_mass_device(f"cfg4_em_{nx}x{ny}", nx, ny, 0.5, 0.067, v, e, 1e-6, 0.1, 0.0, 0.025,
-                                 description="2D effective mass, 16 Gaussians 0.05 eV width 20a, seed 3")
+                                 description="2D effective mass, 16 Gaussians 0.05 eV width 20a, seed 3",
+                                 complex_energy=complex_energy)
 
 
 def config5(n_energies: int = 2048, nx: int = 512, ny: int = 512) -> Workload:

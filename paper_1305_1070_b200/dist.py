@@ -55,18 +55,31 @@ def sweep(solver, energies, weights, self_energies, group=None, batch: int | Non
     step = batch or max(1, getattr(solver, "capacity", len(idx)) or len(idx))
     grs, gls = [], []
     err: Exception | None = None
-    for s0 in range(0, len(idx), step):
-        sel = idx[s0:s0 + step]
-        sr, sl = self_energies(sel)
-        try:
-            gr, gl = solver.solve(np.asarray(energies)[sel], np.asarray(weights)[sel], sr, sl,
-                                  first_energy_index=int(sel[0]), want_diagonals=keep_diagonals)
-        except negf.NegfError as exc:
-            err = exc
-            break
-        if keep_diagonals:
-            grs.append(gr)
-            gls.append(gl)
+    # The reference raises any solver error from solve_all before
+    # electron_density checks a residual (run.cpp:258-291): solve with the
+    # residual guard recording only, settle solver errors across ranks, then
+    # apply the guard to the whole grid.
+    guard = bool(getattr(solver, "residual_check", True))
+    if hasattr(solver, "set_residual_check"):
+        solver.set_residual_check(False)
+    if hasattr(solver, "residual_violation"):
+        solver.residual_violation(reset=True)
+    try:
+        for s0 in range(0, len(idx), step):
+            sel = idx[s0:s0 + step]
+            sr, sl = self_energies(sel)
+            try:
+                gr, gl = solver.solve(np.asarray(energies)[sel], np.asarray(weights)[sel], sr, sl,
+                                      first_energy_index=int(sel[0]), want_diagonals=keep_diagonals)
+            except negf.NegfError as exc:
+                err = exc
+                break
+            if keep_diagonals:
+                grs.append(gr)
+                gls.append(gl)
+    finally:
+        if hasattr(solver, "set_residual_check"):
+            solver.set_residual_check(guard)
     if world > 1:
         import torch
 
@@ -83,6 +96,22 @@ def sweep(solver, energies, weights, self_energies, group=None, batch: int | Non
             raise first
     elif err is not None:
         raise err
+    if guard and hasattr(solver, "residual_violation"):
+        v = solver.residual_violation(reset=True)
+        key = (v[0] << 32 | v[1]) if v is not None else 2**62
+        if world > 1:
+            import torch
+
+            t = torch.tensor([key], dtype=torch.int64)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            key = int(t.item())
+        if key < 2**62:
+            e, d = key >> 32, key & 0xFFFFFFFF
+            raise negf.ResidualTooLarge(
+                f"energy point {e}: G^< diagonal entry has a real part beyond the skew-Hermitian tolerance "
+                f"at dof {d}", e, d)
     if world > 1:
         nccl = use_nccl if use_nccl is not None else dist.get_backend(group) == "nccl"
         if nccl:

@@ -193,6 +193,7 @@ def _load() -> C.CDLL:
         "negf_gpu_profile": ([vp, i32], i32),
         "negf_gpu_set_residual_check": ([vp, i32], i32),
         "negf_gpu_max_real_residual": ([vp], C.c_double),
+        "negf_gpu_residual_violation": ([vp, vp, vp, i32], i32),
         "negf_gpu_profile_read": ([vp, vp, i32], i32),
         "negf_gpu_profile_ops": ([vp, vp, i32], i32),
         "negf_lead_create": ([i32, i32, vp, vp, C.c_double, i32, C.c_double, i32, C.POINTER(vp), st], i32),
@@ -219,14 +220,28 @@ def _load() -> C.CDLL:
     return lib
 
 
-_lib = _load()
+class _Lib:
+    """The C ABI library, mapped on first use: importing this module (for
+    Problem / trapezoid_weights, e.g. by the input generators that the
+    reference arm of bench.py shares) does not load libnegf_b200.so; the
+    first ABI call does, and fails loudly if it is missing."""
+
+    _real = None
+
+    def __getattr__(self, name):
+        if _Lib._real is None:
+            _Lib._real = _load()
+        return getattr(_Lib._real, name)
+
+
+_lib = _Lib()
 ABI_SYMBOLS = (
     "negf_rgf_plan_create negf_plan_create negf_plan_info_get negf_plan_tree negf_plan_fill negf_plan_gemm_tasks negf_plan_gemm_tiles negf_plan_ops negf_plan_destroy "
     "negf_gpu_create negf_gpu_batch_capacity negf_gpu_solve_batch negf_gpu_solve_batch_device "
     "negf_gpu_check negf_gpu_density negf_gpu_stream negf_gpu_density_device "
     "negf_gpu_last_launches negf_gpu_destroy negf_nccl_unique_id negf_gpu_nccl_init "
     "negf_gpu_allreduce_density negf_gpu_set_ordered_reduce negf_gpu_profile negf_gpu_profile_read negf_gpu_profile_ops negf_gpu_set_residual_check "
-    "negf_gpu_max_real_residual negf_lead_create negf_lead_sigma negf_lead_sigma_device negf_lead_last_sweeps "
+    "negf_gpu_max_real_residual negf_gpu_residual_violation negf_lead_create negf_lead_sigma negf_lead_sigma_device negf_lead_last_sweeps "
     "negf_lead_last_launches negf_lead_stream negf_lead_destroy negf_lead_modes_sigma_device "
     "negf_contacts_fill_device negf_format_double negf_write_solve_csv negf_shard_writer_open "
     "negf_shard_writer_append negf_shard_writer_append_device negf_shard_writer_close"
@@ -597,6 +612,19 @@ class HscGpuSolver:
     def set_residual_check(self, raise_error: bool) -> None:
         """True (default): ResidualTooLarge like electron_density; False: record only."""
         _lib.negf_gpu_set_residual_check(self._h, int(bool(raise_error)))
+        self._residual_check = bool(raise_error)
+
+    @property
+    def residual_check(self) -> bool:
+        return getattr(self, "_residual_check", True)
+
+    def residual_violation(self, reset: bool = False):
+        """(energy_index, dof) of the lowest entry with |Re G^<_jj| > 1e-8
+        |G^<_jj| recorded since the last reset (whatever the check mode), or
+        None -- electron_density's guard order (observables.cpp:79-84)."""
+        e, d = C.c_int32(-1), C.c_int32(-1)
+        hit = _lib.negf_gpu_residual_violation(self._h, C.byref(e), C.byref(d), int(bool(reset)))
+        return (int(e.value), int(d.value)) if hit else None
 
     @property
     def max_real_residual(self) -> float:

@@ -51,3 +51,55 @@ def rel_err(x: np.ndarray, ref: np.ndarray) -> float:
     den = np.abs(ref).max()
     num = np.abs(x - ref).max()
     return float(num / den) if den > 0 else float(num)
+
+
+def workload_ref_problem(w, idx):
+    """The reference-side problem (NEGFPRB1) of a devices.Workload at energy
+    indices idx: the same H, the same two dense contact blocks and phonon
+    diagonal (the reference's ContactBlock / phonon vector, run.cpp:90-109),
+    the same energies and trapezoid weights.  Returns (RefProblem, sr, sl)
+    with sr / sl the product's pattern values for the same energies."""
+    idx = np.atleast_1d(np.asarray(idx))
+    p = w.problem
+    sr, sl = w.self_energies(idx)
+    ny = w.ny
+    w2 = ny * ny
+    n = p.n
+    L = np.asarray(p.atomic_groups[0], np.int32)
+    R = np.asarray(p.atomic_groups[1], np.int32)
+    n_lesser = len(p.sl_rows)
+    has_ph = n_lesser > 2 * w2
+    ph = phl = None
+    extra = len(p.sr_rows) - n_lesser  # complex_energy: -i eta on every dof
+    if has_ph or extra:
+        ph = np.zeros((len(idx), n), np.complex128)
+        if has_ph:
+            inner = np.asarray(p.sr_rows[2 * w2:n_lesser], np.int64)
+            ph[:, inner] += sr[:, 2 * w2:n_lesser]
+        if extra:
+            ph[:, np.asarray(p.sr_rows[n_lesser:], np.int64)] += sr[:, n_lesser:]
+    if has_ph:
+        inner = np.asarray(p.sl_rows[2 * w2:], np.int64)
+        phl = np.zeros((len(idx), n), np.complex128)
+        phl[:, inner] = sl[:, 2 * w2:]
+    rp = refio.RefProblem(n=n, h_rows=p.h_rows, h_cols=p.h_cols, h_vals=p.h_vals,
+                          layers=[np.asarray(l) for l in p.layers], coords=p.coords, groups=[L, R],
+                          max_leaf=p.max_leaf, dofs_l=L, dofs_r=R, has_ph=ph is not None, has_ph_less=phl is not None,
+                          energies=w.energies[idx], weights=w.weights[idx],
+                          sig_l=sr[:, :w2].reshape(-1, ny, ny), sig_r=sr[:, w2:2 * w2].reshape(-1, ny, ny), ph=ph,
+                          less_l=sl[:, :w2].reshape(-1, ny, ny), less_r=sl[:, w2:2 * w2].reshape(-1, ny, ny),
+                          ph_less=phl)
+    return rp, sr, sl
+
+
+def per_energy_err(x: np.ndarray, ref: np.ndarray) -> np.ndarray:
+    """rel_err per row (energy)."""
+    den = np.abs(ref).max(axis=1)
+    return np.abs(x - ref).max(axis=1) / np.where(den > 0, den, 1.0)
+
+
+def real_residual(gl: np.ndarray) -> np.ndarray:
+    """max_j |Re G^<_jj| / |G^<_jj| per energy (electron_density's guard
+    quantity, observables.cpp:79-84)."""
+    a = np.abs(gl)
+    return (np.abs(gl.real) / np.where(a > 0, a, 1.0)).max(axis=1)
