@@ -194,9 +194,11 @@ def level_breakdown(ops, op_ms, energies_timed, steps):
     small separators / large separators), from per-op CUDA events."""
     classes = (("leaves (level 1)", 1, 1), ("separators, levels 2-4", 2, 4), ("separators, levels >= 5", 5, 99))
     out = {}
-    for kname, kinds in (("gemm", (1,)), ("inverse", (0, 4, 5))):
+    inv_gemm = (ops["kind"] == 1) & (ops["phase"] == 6)  # GEMM updates inside multi-CTA inverses
+    for kname, base in (("gemm", (ops["kind"] == 1) & ~inv_gemm),
+                        ("inverse", np.isin(ops["kind"], (0, 4, 5, 11)) | inv_gemm)):
         for cname, lo, hi in classes:
-            sel = np.isin(ops["kind"], kinds) & (ops["level"] >= lo) & (ops["level"] <= hi)
+            sel = base & (ops["level"] >= lo) & (ops["level"] <= hi)
             ms = float(op_ms[sel].sum())
             fl = 8.0 * float(ops["cmul"][sel].sum()) * energies_timed
             if ms > 0:

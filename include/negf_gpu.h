@@ -125,8 +125,10 @@ int negf_plan_gemm_tiles(const negf_plan* p, int32_t* task, int32_t* m0, int32_t
                          int32_t* mirrored);
 /* The replayed op list (introspection, n_ops entries): kind (0 inverse,
  * 1 grouped GEMM, 2 diagonal, 3 seed scaling, 4 panel, 5 permutation, 6 skew,
- * 7 combine, 8 sparse leaf Psi, 9 sparse leaf Schur contributions, 10 leaf Woodbury diagonals),
- * phase (0 fold, 1 G^r, 2 seed, 3 N fold, 4 G^<), tree level, range in the
+ * 7 combine, 8 sparse leaf Psi, 9 sparse leaf Schur contributions, 10 leaf
+ * Woodbury diagonals, 11 outer-panel interchanges of a multi-CTA inverse),
+ * phase (0 fold, 1 G^r, 2 seed, 3 N fold, 4 G^<, 6 a GEMM update inside a
+ * multi-CTA block inverse), tree level, range in the
  * kind's task (GEMM: tile) array, executed complex MACs per energy; any
  * pointer may be NULL. */
 int negf_plan_ops(const negf_plan* p, int32_t* kind, int32_t* phase, int32_t* level, int32_t* begin,

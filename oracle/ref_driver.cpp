@@ -9,7 +9,7 @@
 // Modes
 //   ref_driver cli solve|bench|partition <config.json>
 //       the reference's own commands (run.cpp:283-447) -> golden CSVs
-//   ref_driver solve <problem.bin> <out.bin> [--threads T] [--solver hsc|dense|rgf]
+//   ref_driver solve <problem.bin> <out.bin> [--threads T] [--solver hsc|dense|rgf|tree]
 //                    [--energies i,j,...]
 //       per-energy pipeline of solve_energy (run.cpp:141-192) over a binary
 //       problem (format in oracle/refio.py), energy pool as solve_all
@@ -258,7 +258,10 @@ int cmd_problem(int argc, char** argv) {
   const Problem p = read_problem(in);
   if (subset.empty())
     for (int e = 0; e < static_cast<int>(p.energies.size()); ++e) subset.push_back(e);
-  const int m = static_cast<int>(subset.size());
+  // --solver tree: build_tree only (the separator tree of the HSC path, no
+  // energy solved)
+  const bool tree_only = solver == "tree";
+  const int m = tree_only ? 0 : static_cast<int>(subset.size());
 
   int status = 0, err_energy = -1;
   std::string msg;
@@ -267,7 +270,7 @@ int cmd_problem(int argc, char** argv) {
   double wall = 0.0, tree_wall = 0.0;
   try {
     const auto t0 = std::chrono::steady_clock::now();
-    if (solver == "hsc") {
+    if (solver == "hsc" || tree_only) {
       // build_tree (run.cpp:123-133): graph of A(E0), contact atomic groups.
       const Graph g = graph_of_pattern(system_at(p, subset.front()));
       tree = std::make_shared<SeparatorTree>(nested_dissection(g, p.groups, p.max_leaf, p.coords));
@@ -288,7 +291,7 @@ int cmd_problem(int argc, char** argv) {
       }
     };
     std::vector<std::thread> pool;
-    const int nt = std::max(1, std::min(threads, m));
+    const int nt = m == 0 ? 0 : std::max(1, std::min(threads, m));
     for (int t = 0; t < nt; ++t) pool.emplace_back(work);
     for (auto& th : pool) th.join();
     wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();

@@ -248,11 +248,12 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
     launch_output_gr(b, P.desc.n, g->d_gr_pos, d_gr, s, L);
     if (hk->gr_ready) ck(cudaEventRecord(hk->gr_ready, s), "event");
   };
-  static const int kind_stat[11] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
-                                   NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE,
-                                   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,
-                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_DIAG};  // K_SPSI / K_SSCHUR: sparse, with
-                                                                            // the scalings; K_LEAFDIAG: diagonals
+  static const int kind_stat[12] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
+                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE,
+                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,
+                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_DIAG,    NEGF_KSTAT_INVERSE};
+  // K_SPSI / K_SSCHUR: sparse, with the scalings; K_LEAFDIAG: diagonals;
+  // K_BIGSWAP: part of the multi-CTA inverse
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
     if (static_cast<int>(oi) == P.gr_done_op) gr_out();
     if (static_cast<int>(oi) == P.lesser_op) lesser();
@@ -269,10 +270,13 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         launch_diag(b, g->d_diag, g->d_diag_terms, op.begin, op.count, s, L);
         break;
       case K_PANEL:
-        launch_bigpanel(b, g->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, op.k0, g->d_status, s, L);
+        launch_bigpanel(b, g->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, op.k0, op.k1, g->d_status, s, L);
         break;
       case K_PERM:
         launch_bigperm(b, g->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, s, L);
+        break;
+      case K_BIGSWAP:
+        launch_bigswap(b, g->d_big + op.begin, op.count, op.k1, s, L);
         break;
       case K_SKEW:
         launch_skew(b, g->d_skew_tasks, P.skew_tasks.data(), op.begin, op.count, s, L);
@@ -535,7 +539,7 @@ int negf_plan_ops(const negf_plan* h, int32_t* kind, int32_t* phase, int32_t* le
   for (std::size_t i = 0; i < P.ops.size(); ++i) {
     const Op& o = P.ops[i];
     if (kind) kind[i] = o.kind;
-    if (phase) phase[i] = o.phase;
+    if (phase) phase[i] = o.kind == K_GEMM && o.inv_update ? 6 : o.phase;
     if (level) level[i] = o.level;
     if (begin) begin[i] = o.begin;
     if (count) count[i] = o.count;

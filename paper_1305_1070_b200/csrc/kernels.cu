@@ -841,17 +841,191 @@ __global__ void __launch_bounds__(INV_THREADS, RPL == 1 ? 6 : 4) k_inverse_la(do
 }
 
 // ---------------------------------------------------------------------------
-// Multi-CTA blocked Gauss-Jordan for large blocks (m > kSmemInvMax).
-// Per kPanel-column panel: k_bigpanel (one CTA per block and energy) factors
-// the panel with row partial pivoting in shared memory, applies the panel's
-// row interchanges to the rest of the block, and stages M_p - I_p and the
-// pivot rows R_p in arena scratch; the rank-kPanel update of all other
-// columns is an ordinary grouped-GEMM task (many CTAs, DMMA).  k_bigperm
-// finally undoes the interchanges as column interchanges.
+// Register-resident Gauss-Jordan for m <= ROWS (<= 96): the whole block lives
+// in the registers of ROWS * H threads -- thread t owns row r = t / H and the
+// columns c = h + H j (h = t % H, j < SLOTS) -- so every pivot step updates
+// all m x m entries at once on the FP64 pipes of all warps (m^3 complex FMAs
+// in total, 8 flops each), instead of a serial 8-column panel on one warp
+// followed by a rank-8 update.  Rows are never moved: partial pivoting keeps
+// the *position* of every physical row (pos), exactly as if rows k and p were
+// interchanged, so the pivot sequence, its tie-break (largest |a_rk|, lowest
+// position) and the singular rule |u_kk| <= 1e-13 max|a| (dense.cpp:56-75)
+// are those of the swapping elimination.  Per pivot: a warp argmax, one
+// barrier, the pivot row's owners publish it normalised, one barrier, update.
 // ---------------------------------------------------------------------------
+struct InvCand {
+  double v;     // |a_pk|^2 of the warp's best candidate (-1: none)
+  int pos, row; // its position and physical row
+  double2 val;  // a_pk
+};
+
+template <int ROWS, int H, int SLOTS>
+__global__ void __launch_bounds__(ROWS * H, (ROWS * H <= 64) ? 8 : (ROWS * H <= 128) ? 3 : 1)
+    k_inverse_rg(double2* arena, int64_t stride, const InvTask* __restrict__ tasks, int e_base, DevStatus* st) {
+  constexpr int NT = ROWS * H, NW = NT / 32, MMAX = H * SLOTS;
+  static_assert(NT % 32 == 0 && (H & (H - 1)) == 0 && MMAX >= ROWS, "bad register inverse shape");
+  __shared__ double2 prow[2][MMAX];
+  __shared__ InvCand cand[2][NW];
+  __shared__ double red[NW];
+  __shared__ int perm[ROWS], pos_of[ROWS];
+  const InvTask tk = tasks[blockIdx.x];
+  const int m = tk.m;
+  double2* g = arena + int64_t(blockIdx.y) * stride + tk.off;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, h = t & (H - 1), r = t / H;
+  const bool live = r < m;
+  double2 a[SLOTS];
+  double mx = 0.0;
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j) {
+    const int c = h + H * j;
+    a[j] = (live && c < m) ? g[int64_t(r) * m + c] : make_double2(0.0, 0.0);
+    mx = fmax(mx, cabs2(a[j]));
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = 0.0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) mx = fmax(mx, red[w]);
+  const double thr2 = (1e-13 * mx) * (1e-13 * mx);
+  int pos = r;  // current position of this physical row
+#ifdef NEGF_RG_CLOCKS
+  long long ck[5] = {0, 0, 0, 0, 0}, c0 = clock64();
+#define RG_TICK(i) { const long long c1 = clock64(); ck[i] += c1 - c0; c0 = c1; }
+#else
+#define RG_TICK(i)
+#endif
+#pragma unroll
+  for (int j = 0; j < SLOTS; ++j) {
+    for (int hh = 0; hh < H; ++hh) {
+      const int k = j * H + hh;
+      if (k >= m) break;  // uniform
+      const int par = k & 1;
+      // column k of my row (held by the row's thread with h == hh, slot j)
+      const int src = (lane & ~(H - 1)) | hh;
+      double2 f;
+      f.x = __shfl_sync(0xffffffffu, a[j].x, src);
+      f.y = __shfl_sync(0xffffffffu, a[j].y, src);
+      // warp argmax over the rows not yet pivoted (pos >= k): largest |a_rk|,
+      // lowest position among equals
+      double best = (live && h == 0 && pos >= k) ? cnorm(f) : -1.0;
+      int bpos = (best >= 0.0) ? pos : 0x7fffffff;
+      const unsigned key = best >= 0.0 ? __float_as_uint(__double2float_ru(best)) : 0u;
+      const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+      const unsigned tied = __ballot_sync(0xffffffffu, key == kmax && best >= 0.0);
+      int wl;  // lane holding the warp's winner
+      if (__popc(tied) <= 1) {
+        wl = tied ? __ffs(tied) - 1 : 0;
+      } else {  // exact order among the lanes whose float images tie
+        double cb = (key == kmax) ? best : -1.0;
+        int cp = (key == kmax) ? bpos : 0x7fffffff, cl = lane;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, cb, o);
+          const int op = __shfl_xor_sync(0xffffffffu, cp, o);
+          const int ol = __shfl_xor_sync(0xffffffffu, cl, o);
+          if (ob > cb || (ob == cb && op < cp)) {
+            cb = ob;
+            cp = op;
+            cl = ol;
+          }
+        }
+        wl = cl;
+      }
+      if (lane == wl) cand[par][warp] = InvCand{best, bpos, r, f};
+      RG_TICK(0)
+      __syncthreads();
+      RG_TICK(1)
+      InvCand w = cand[par][0];
+#pragma unroll
+      for (int q = 1; q < NW; ++q) {
+        const InvCand o = cand[par][q];
+        if (o.v > w.v || (o.v == w.v && o.pos < w.pos)) w = o;
+      }
+      if (!(w.v > thr2)) {  // |u_kk| <= 1e-13 max|a| (uniform across the CTA)
+        if (w.v == w.v) {
+          if (t == 0) report_singular(st, e_base + blockIdx.y, tk.fold_pos, k);
+          return;
+        }
+      }
+      const int p = w.pos;
+      if (t == 0) perm[k] = p;
+      const double rd = 1.0 / fma(w.val.x, w.val.x, w.val.y * w.val.y);
+      const double2 ip = make_double2(w.val.x * rd, -w.val.y * rd);
+      const bool pivot_row = r == w.row;
+      if (pivot_row) {
+#pragma unroll
+        for (int jj = 0; jj < SLOTS; ++jj) {
+          const int c = h + H * jj;
+          if (c < MMAX) prow[par][c] = (jj == j && h == hh) ? ip : cmul(a[jj], ip);
+        }
+      }
+      RG_TICK(2)
+      __syncthreads();
+      RG_TICK(3)
+      if (pivot_row) {
+#pragma unroll
+        for (int jj = 0; jj < SLOTS; ++jj) a[jj] = prow[par][h + H * jj];
+      } else if (live) {
+#pragma unroll
+        for (int jj = 0; jj < SLOTS; ++jj) {
+          const double2 pr = prow[par][h + H * jj];
+          const double2 b = (jj == j && h == hh) ? make_double2(0.0, 0.0) : a[jj];
+          a[jj].x = fma(-f.x, pr.x, fma(f.y, pr.y, b.x));
+          a[jj].y = fma(-f.x, pr.y, fma(-f.y, pr.x, b.y));
+        }
+      }
+      if (pos == k) pos = p;
+      else if (pos == p) pos = k;
+      RG_TICK(4)
+    }
+  }
+#ifdef NEGF_RG_CLOCKS
+  if (blockIdx.x == 0 && blockIdx.y == 0 && (t == 0 || t == NT - 1))
+    printf("[rg clocks] m=%d t=%d argmax %lld bar1 %lld pivrow %lld bar2 %lld update %lld per pivot\n", m, t,
+           ck[0] / m, ck[1] / m, ck[2] / m, ck[3] / m, ck[4] / m);
+#endif
+  // Undo the row interchanges as column interchanges (last first).
+  __syncthreads();
+  if (t == 0) {
+    int* cur_at = pos_of;
+    for (int c = 0; c < m; ++c) cur_at[c] = c;
+    for (int k = m - 1; k >= 0; --k) {
+      const int p = perm[k];
+      const int t2 = cur_at[k];
+      cur_at[k] = cur_at[p];
+      cur_at[p] = t2;
+    }
+    int* inv_pos = perm;  // perm is consumed
+    for (int q = 0; q < m; ++q) inv_pos[cur_at[q]] = q;
+    for (int q = 0; q < m; ++q) pos_of[q] = inv_pos[q];
+  }
+  __syncthreads();
+  if (live) {
+#pragma unroll
+    for (int j = 0; j < SLOTS; ++j) {
+      const int c = h + H * j;
+      if (c < m) g[int64_t(pos) * m + pos_of[c]] = a[j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Multi-CTA blocked Gauss-Jordan for large blocks (m > kSmemInvMax), see
+// plan.hpp: per kPanel-column inner panel, k_bigpanel (one CTA per block and
+// energy) factors the panel with row partial pivoting (in shared memory, or
+// in the arena's panel scratch -- L2 -- beyond kPanelSmemMax rows), applies
+// its row interchanges to the other columns of the outer panel [o0, oe) and
+// stages M_p - I_p and the pivot rows R_p; a grouped-GEMM task applies the
+// rank-kPanel update to the outer panel.  Per outer panel, k_bigswap applies
+// its kOuter interchanges to every other column and stages the rank-kOuter
+// operands of one grouped-GEMM update of the whole block.  k_bigperm finally
+// undoes the interchanges as column interchanges.
+// ---------------------------------------------------------------------------
+template <bool kSmemPanel>
 __global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride, const BigTask* __restrict__ tasks,
-                                                  int k0, int e_base, DevStatus* st) {
-  extern __shared__ double2 pn[];  // m x kPanel panel
+                                                  int k0, int o0, int e_base, DevStatus* st) {
+  extern __shared__ double2 pn_smem[];  // m x kPanel panel
   __shared__ double red_v[8];
   __shared__ int red_i[8];
   __shared__ double s_thr;
@@ -861,6 +1035,8 @@ __global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride
   double2* base = arena + blockIdx.y * stride;
   double2* A = base + tk.off;
   double2* thr = base + tk.off_thr;
+  double2* pn = kSmemPanel ? pn_smem : base + tk.off_mp;
+  const int oe = min(o0 + kOuter, m);
   int* perm = reinterpret_cast<int*>(base + tk.off_perm);
   if (k0 == 0) {  // threshold from the original block (dense.cpp:58)
     double mx = 0.0;
@@ -961,9 +1137,10 @@ __global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride
     if (r == k0 + c) v.x -= 1.0;
     mp[i] = v;
   }
-  // this panel's row interchanges on every other column, then stage R_p
+  // this panel's row interchanges on the outer panel's other columns, then
+  // stage R_p there (the rank-kPanel update covers columns [o0, oe) only)
   double2* rs = base + tk.off_rs;
-  for (int c = tid; c < m; c += 256) {
+  for (int c = o0 + tid; c < oe; c += 256) {
     const bool in_panel = c >= k0 && c < k0 + kPanel;
     if (!in_panel)
       for (int kk = 0; kk < kb; ++kk) {
@@ -980,12 +1157,52 @@ __global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride
   }
 }
 
-// Undo the row interchanges as column interchanges, last first.
+// One outer panel [o0, oe) done: its row interchanges on every column outside
+// it, then the rank-kOuter operands -- R_P = the pivot rows (zero inside the
+// panel) and M_P - I_P = the panel's columns minus the identity on the pivot
+// positions.  Column-parallel (coalesced rows).
+__global__ void __launch_bounds__(256) k_bigswap(double2* arena, int64_t stride, const BigTask* __restrict__ tasks,
+                                                 int o0) {
+  const BigTask tk = tasks[blockIdx.x];
+  const int m = tk.m, tid = threadIdx.x;
+  double2* base = arena + blockIdx.y * stride;
+  if (base[tk.off_thr].y != 0.0) return;  // singular: already reported
+  double2* A = base + tk.off;
+  const int* perm = reinterpret_cast<const int*>(base + tk.off_perm);
+  double2* rs = base + tk.off_rs64;
+  double2* mp = base + tk.off_mp64;
+  const int oe = min(o0 + kOuter, m), kb = oe - o0;
+  for (int c = tid; c < m; c += 256) {
+    const bool inside = c >= o0 && c < oe;
+    if (!inside)
+      for (int kk = 0; kk < kb; ++kk) {
+        const int k = o0 + kk, p = perm[k];
+        if (p != k) {
+          const double2 t2 = A[int64_t(k) * m + c];
+          A[int64_t(k) * m + c] = A[int64_t(p) * m + c];
+          A[int64_t(p) * m + c] = t2;
+        }
+      }
+    for (int kk = 0; kk < kb; ++kk)
+      rs[int64_t(kk) * m + c] = inside ? make_double2(0.0, 0.0) : A[int64_t(o0 + kk) * m + c];
+  }
+  for (int64_t i = tid; i < int64_t(m) * kb; i += 256) {
+    const int r = static_cast<int>(i / kb), kk = static_cast<int>(i - int64_t(r) * kb);
+    double2 v = A[int64_t(r) * m + o0 + kk];
+    if (r == o0 + kk) v.x -= 1.0;
+    mp[int64_t(r) * kOuter + kk] = v;
+  }
+}
+
+// Undo the row interchanges as column interchanges, last first.  The index
+// maps live in shared memory (8 m bytes), the row buffers in the arena's
+// outer-panel scratch (kOuter x m >= 4 rows).
 __global__ void __launch_bounds__(128) k_bigperm(double2* arena, int64_t stride, const BigTask* __restrict__ tasks) {
-  extern __shared__ double2 rowbuf[];  // 4 warps x m
-  __shared__ int pos_of[kBigMax], cur_at[kBigMax];
+  extern __shared__ int pmaps[];  // pos_of[m], cur_at[m]
   const BigTask tk = tasks[blockIdx.x];
   const int m = tk.m, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int* pos_of = pmaps;
+  int* cur_at = pmaps + m;
   double2* base = arena + blockIdx.y * stride;
   double2* thr = base + tk.off_thr;
   if (thr->y != 0.0) return;  // singular: already reported
@@ -1002,7 +1219,7 @@ __global__ void __launch_bounds__(128) k_bigperm(double2* arena, int64_t stride,
     for (int q = 0; q < m; ++q) pos_of[cur_at[q]] = q;
   }
   __syncthreads();
-  double2* buf = rowbuf + warp * m;
+  double2* buf = base + tk.off_rs64 + int64_t(warp) * m;
   for (int r = warp; r < m; r += 4) {
     for (int c = lane; c < m; c += 32) buf[c] = A[int64_t(r) * m + c];
     __syncwarp();
@@ -1109,6 +1326,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
   const int live_i = min(2, max(0, (tk.m - tl.m0 - wm + 7) / 8));
   const int live_j = min(2, max(0, (tk.n - tl.n0 - wn + 7) / 8));
 
+#ifndef NEGF_GEMM_4M
   // Gauss (3M) complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar+Ai)(Br+Bi);
   // C = (P1 - P2) + i (P3 - P1 - P2): three real DMMAs per complex subtile
   // step instead of four.  Flop accounting stays 8 m n k.
@@ -1119,6 +1337,18 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = p3[i][j][q] = 0.0;
+#else
+  // Conventional (4M) complex product: Re C = Ar Br - Ai Bi, Im C = Ar Bi +
+  // Ai Br, four real DMMAs per complex subtile step (componentwise accurate:
+  // no (Ar+Ai)(Br+Bi) cancellation in the imaginary part).
+  double p1[2][2][2], p2[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = 0.0;
+#endif
 
   // Flattened (term, k-chunk) sequence through a 2-stage cp.async ring, one
   // barrier per chunk.  The loader is re-based only when the term changes.
@@ -1197,6 +1427,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         b[j] = b_kr ? Bs[kk * A::LDB_KR + c] : Bs[c * LD_RK + kk];
         b[j].y = flip_sign(b[j].y, conjB);
       }
+#ifndef NEGF_GEMM_4M
       double as[2], bs[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
@@ -1213,6 +1444,23 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
           dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
         }
       }
+#else
+      double nai[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) nai[i] = flip_sign(a[i].y, int(0x80000000));
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (i >= live_i) break;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j >= live_j) break;
+          dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+          dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
+          dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+          dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
+        }
+      }
+#endif
     };
     if (live_i > 0 && live_j > 0) {
       if (ksteps == KC) {  // full chunk: straight-line, loads can be hoisted
@@ -1245,7 +1493,11 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
       for (int q = 0; q < 2; ++q) {
         const int c = tl.n0 + wn + 8 * j + 2 * t + q;
         if (c >= tk.n) continue;
+#ifndef NEGF_GEMM_4M
         double2 v = make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
+#else
+        double2 v = make_double2(p1[i][j][q], p2[i][j][q]);
+#endif
         if (mir) {  // strictly-upper tile of a symmetric task: the (c, r) entry too
           double2* d2 = base + tk.c_off + int64_t(c) * tk.ldc + r;
           if (tk.mirror == 2) *d2 = make_double2(-v.x, v.y);  // anti-Hermitian: -conj
@@ -1540,74 +1792,77 @@ void launch_combine(const BatchArgs& b, const CombineTask* d_tasks, const Combin
 
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
                     DevStatus* st, cudaStream_t s, int64_t& launches) {
-  // Tasks of a level are pre-sorted by size class (see plan.cpp), so each
-  // variant below covers one contiguous range.
-  auto cls = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : 3; };
+  // Tasks of a level are pre-sorted by size class (inv_size_class, shared
+  // with plan.cpp), so each variant below covers one contiguous range.
   int i = 0;
   while (i < count) {
-    const int c = cls(h_tasks[i].m);
-    const int g8 = (h_tasks[i].m + 7) & ~7;
+    const int c = inv_size_class(h_tasks[i].m);
     int j = i;
     int mmax = 0;
-    // one launch per variant; the shared-memory variants per padded size
-    while (j < count && cls(h_tasks[j].m) == c && (c < 1 || ((h_tasks[j].m + 7) & ~7) == g8)) {
+    // the shared-memory variants: one launch per padded size
+    while (j < count && inv_size_class(h_tasks[j].m) == c &&
+           (c < 3 || ((h_tasks[j].m + 7) & ~7) == ((h_tasks[i].m + 7) & ~7))) {
       mmax = std::max(mmax, h_tasks[j].m);
       ++j;
     }
     dim3 grid(j - i, b.nE);
+    const InvTask* dt = d_tasks + i;
     const int m8 = (mmax + 7) & ~7;
-    const size_t tail = size_t(8) * (m8 + 2) * 16 + size_t(2 * m8 + 2) * 4 + 64;
+    const size_t smem = size_t(m8) * (m8 + 2) * 16 + size_t(8) * (m8 + 2) * 16 + size_t(2 * m8 + 2) * 4 + 64;
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr)) {
+      cudaFuncSetAttribute(k_inverse_blocked<false, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(k_inverse_blocked<false, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(k_inverse_la<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    }
+#ifdef NEGF_INV_LEGACY
+    // round-1 kernels (A/B builds): shared-memory blocked Gauss-Jordan from 17 up
+    if (c == 1 || c == 2) {
+      if (mmax <= 32)
+        k_inverse_blocked<false, 1, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
+      else
+        k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
+      ++launches;
+      i = j;
+      continue;
+    }
+#endif
     switch (c) {
-      case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st); break;
-      case 1: {  // 17..32: the blocked kernel beats the register one ~1.8x (tools/inv_bench.cu)
-        const size_t smem = size_t(m8) * (m8 + 2) * 16 + tail;
-        static std::atomic<unsigned long long> attr1{0};
-        if (first_on_device(attr1))
-          cudaFuncSetAttribute(k_inverse_blocked<false, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        k_inverse_blocked<false, 1, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
+      case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
+      case 1: k_inverse_rg<32, 2, 16><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
+      case 2: k_inverse_rg<48, 2, 24><<<grid, 96, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
+      case 3:  // 49..64: 8-column panel on one warp + DMMA rank-8 updates
+        k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
         break;
-      }
-      case 2:
-      case 3: {
-        const size_t smem = size_t(m8) * (m8 + 2) * 16 + tail;
-        static std::atomic<unsigned long long> attr{0};
-        if (first_on_device(attr)) {
-          cudaFuncSetAttribute(k_inverse_blocked<false, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-          cudaFuncSetAttribute(k_inverse_blocked<false, 4, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        }
-        // 65..112: the look-ahead variant (panel p+1 overlaps update p) is
-        // 15-20 % faster there; at <= 64 other CTAs already hide the panel
-        static std::atomic<unsigned long long> attr_la{0};
-        if (first_on_device(attr_la))
-          cudaFuncSetAttribute(k_inverse_la<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        if (mmax <= 64)
-          k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
-        else
-          k_inverse_la<4><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
-        break;
-      }
-      default: {
-        const size_t smem = tail + size_t(8) * m8 * 16;
-        static std::atomic<unsigned long long> attr{0};
-        if (first_on_device(attr))
-          cudaFuncSetAttribute(k_inverse_blocked<true, 1, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        k_inverse_blocked<true, 1, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, d_tasks + i, b.e_base, st);
-      }
+      default:  // 65..kSmemInvMax: the same with look-ahead (panel p+1 overlaps update p)
+        k_inverse_la<4><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
     }
     ++launches;
     i = j;
   }
 }
 
-void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0,
+void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0, int o0,
                      DevStatus* st, cudaStream_t s, int64_t& launches) {
   if (count <= 0) return;
   int mmax = 0;
   for (int i = 0; i < count; ++i) mmax = std::max(mmax, h_tasks[i].m);
-  const size_t smem = size_t(mmax) * kPanel * sizeof(double2);
-  static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr)) cudaFuncSetAttribute(k_bigpanel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  k_bigpanel<<<dim3(count, b.nE), 256, smem, s>>>(b.arena, b.stride, d_tasks, k0, b.e_base, st);
+  if (mmax <= kPanelSmemMax) {
+    const size_t smem = size_t(mmax) * kPanel * sizeof(double2);
+    static std::atomic<unsigned long long> attr{0};
+    if (first_on_device(attr))
+      cudaFuncSetAttribute(k_bigpanel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    k_bigpanel<true><<<dim3(count, b.nE), 256, smem, s>>>(b.arena, b.stride, d_tasks, k0, o0, b.e_base, st);
+  } else {
+    k_bigpanel<false><<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, k0, o0, b.e_base, st);
+  }
+  ++launches;
+}
+
+void launch_bigswap(const BatchArgs& b, const BigTask* d_tasks, int count, int o0, cudaStream_t s,
+                    int64_t& launches) {
+  if (count <= 0) return;
+  k_bigswap<<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, o0);
   ++launches;
 }
 
@@ -1616,7 +1871,7 @@ void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h
   if (count <= 0) return;
   int mmax = 0;
   for (int i = 0; i < count; ++i) mmax = std::max(mmax, h_tasks[i].m);
-  const size_t smem = size_t(4) * mmax * sizeof(double2);
+  const size_t smem = size_t(2) * mmax * sizeof(int);
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) cudaFuncSetAttribute(k_bigperm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   k_bigperm<<<dim3(count, b.nE), 128, smem, s>>>(b.arena, b.stride, d_tasks);

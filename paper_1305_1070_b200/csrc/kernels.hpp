@@ -32,8 +32,10 @@ void launch_scatter_lesser(const BatchArgs& b, const Plan& p, const double* d_en
                            cudaStream_t s, int64_t& launches);
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
                     DevStatus* st, cudaStream_t s, int64_t& launches);
-void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0,
+void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, int k0, int o0,
                      DevStatus* st, cudaStream_t s, int64_t& launches);
+void launch_bigswap(const BatchArgs& b, const BigTask* d_tasks, int count, int o0, cudaStream_t s,
+                    int64_t& launches);
 void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h_tasks, int count, cudaStream_t s,
                     int64_t& launches);
 void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,

@@ -327,11 +327,14 @@ void replay(negf_lead* l, const BatchArgs& b, const int* range) {
                     l->launches);
         break;
       case K_PANEL:
-        launch_bigpanel(b, l->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, op.k0, l->d_status,
+        launch_bigpanel(b, l->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, op.k0, op.k1, l->d_status,
                         l->stream, l->launches);
         break;
       case K_PERM:
         launch_bigperm(b, l->d_big + op.begin, P.big_tasks.data() + op.begin, op.count, l->stream, l->launches);
+        break;
+      case K_BIGSWAP:
+        launch_bigswap(b, l->d_big + op.begin, op.count, op.k1, l->stream, l->launches);
         break;
       default:
         throw Failure(kInternal, "lead: unexpected op kind");
@@ -467,7 +470,7 @@ int negf_lead_create(int device, int w, const double* h00, const double* h01, do
   if (!(eta_ev > 0.0)) return set_status(st, NEGF_CONFIG_ERROR, "contact broadening eta must be positive");
   if (criterion != 0 && criterion != 1) return set_status(st, NEGF_CONTRACT_VIOLATION, "unknown lead criterion");
   if (criterion == 1 && !(tol > 0.0)) return set_status(st, NEGF_CONFIG_ERROR, "decimation tolerance must be positive");
-  if (w <= 0 || w > kBigMax)
+  if (w <= 0)
     return set_status(st, NEGF_CONTRACT_VIOLATION,
                       "surface_self_energy: lead block size " + std::to_string(w) + " out of range");
   auto l = std::make_unique<negf_lead>();

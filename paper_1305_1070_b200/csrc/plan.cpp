@@ -83,6 +83,7 @@ struct Builder {
         break;
       case K_DIAG: cur.begin = static_cast<int>(P.diag_tasks.size()); break;
       case K_PANEL:
+      case K_BIGSWAP:
       case K_PERM: cur.begin = static_cast<int>(P.big_tasks.size()); break;
       case K_SPSI: cur.begin = static_cast<int>(P.spsi_tasks.size()); break;
       case K_SSCHUR: cur.begin = static_cast<int>(P.sschur_tasks.size()); break;
@@ -99,6 +100,7 @@ struct Builder {
         break;
       case K_DIAG: cur.count = static_cast<int>(P.diag_tasks.size()) - cur.begin; break;
       case K_PANEL:
+      case K_BIGSWAP:
       case K_PERM: cur.count = static_cast<int>(P.big_tasks.size()) - cur.begin; break;
       case K_SPSI: cur.count = static_cast<int>(P.spsi_tasks.size()) - cur.begin; break;
       case K_SSCHUR: cur.count = static_cast<int>(P.sschur_tasks.size()) - cur.begin; break;
@@ -173,16 +175,13 @@ struct Builder {
   void emit_inverses(int l, int phase, const std::vector<InvItem>& items, int64_t scratch_off) {
     auto& T = P.gemm_terms;
     open(K_INVERSE, phase, l);
-    auto size_class = [](int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 64 ? 2 : 3; };
-    // Grouped by kernel variant; the shared-memory variants (m > 16) also by
-    // padded size m8 (largest first), so each launch sizes its shared memory
-    // for its own blocks and small blocks get more CTAs per SM.
+    // Grouped by kernel variant (one launch each), largest blocks first
+    // within a variant so the longest CTAs start first.
     std::vector<InvItem> order(items.begin(), items.end());
     std::stable_sort(order.begin(), order.end(), [&](const InvItem& a, const InvItem& b) {
-      const int ca = size_class(a.m), cb = size_class(b.m);
+      const int ca = inv_size_class(a.m), cb = inv_size_class(b.m);
       if (ca != cb) return ca < cb;
-      if (ca >= 1) return ((a.m + 7) & ~7) > ((b.m + 7) & ~7);
-      return false;
+      return a.m > b.m;
     });
     for (const InvItem& it : order)
       if (it.m > 0 && it.m <= kSmemInvMax) {
@@ -205,28 +204,55 @@ struct Builder {
       so += align8(int64_t(m) * kPanel);
       bt.off_rs = so;
       so += align8(int64_t(m) * kPanel);
+      bt.off_mp64 = so;
+      so += align8(int64_t(m) * kOuter);
+      bt.off_rs64 = so;
+      so += align8(int64_t(m) * kOuter);
       bt.off_perm = so;
-      so += align8((m + 3) / 4);
+      so += align8((3 * int64_t(m) + 3) / 4);
       bt.off_thr = so;
       so += 8;
       big.push_back(bt);
       mmax = std::max(mmax, m);
     }
     if (big.empty()) return;
-    for (int k0 = 0; k0 < mmax; k0 += kPanel) {
-      open(K_PANEL, phase, l);
-      cur.k0 = k0;
-      for (const BigTask& bt : big)
-        if (bt.m > k0) {
-          P.big_tasks.push_back(bt);
-          cur.cmul += double(bt.m) * kPanel * kPanel;
+    for (int o0 = 0; o0 < mmax; o0 += kOuter) {
+      for (int k0 = o0; k0 < o0 + kOuter && k0 < mmax; k0 += kPanel) {
+        open(K_PANEL, phase, l);
+        cur.k0 = k0;
+        cur.k1 = o0;
+        for (const BigTask& bt : big)
+          if (bt.m > k0) {
+            P.big_tasks.push_back(bt);
+            cur.cmul += double(bt.m) * kPanel * kPanel;
+          }
+        close();
+        // rank-kPanel update of the outer panel's other columns:
+        // A[:, o0:oe] += (M_p - I_p) R_p (R_p is zero on the inner panel)
+        open(K_GEMM, phase, l);
+        cur.inv_update = 1;
+        for (const BigTask& bt : big) {
+          const int oe = std::min(o0 + kOuter, bt.m);
+          if (bt.m <= k0 || oe - o0 <= kPanel) continue;
+          const int tb = static_cast<int>(T.size());
+          add_term(T, kPanel, OP_N, bt.off_mp, kPanel, OP_N, bt.off_rs + o0, bt.m, +1);
+          gemm_task(bt.m, oe - o0, bt.off + o0, bt.m, MODE_ADD, 0, 0, tb);
         }
+        close();
+      }
+      open(K_BIGSWAP, phase, l);
+      cur.k1 = o0;
+      for (const BigTask& bt : big)
+        if (bt.m > o0 && bt.m > kOuter) P.big_tasks.push_back(bt);
       close();
-      open(K_GEMM, phase, l);  // rank-kPanel update R += (M_p - I_p) R_p
+      // rank-kOuter update of every other column: A += (M_P - I_P) R_P
+      open(K_GEMM, phase, l);
+      cur.inv_update = 1;
       for (const BigTask& bt : big) {
-        if (bt.m <= k0) continue;
+        if (bt.m <= o0 || bt.m <= kOuter) continue;
+        const int kb = std::min(kOuter, bt.m - o0);
         const int tb = static_cast<int>(T.size());
-        add_term(T, kPanel, OP_N, bt.off_mp, kPanel, OP_N, bt.off_rs, bt.m, +1);
+        add_term(T, kb, OP_N, bt.off_mp64, kOuter, OP_N, bt.off_rs64, bt.m, +1);
         gemm_task(bt.m, bt.m, bt.off, bt.m, MODE_ADD, 0, 0, tb);
       }
       close();
@@ -332,15 +358,20 @@ int64_t tile_task_sym(int task, int m, std::vector<GemmTile>& out) {
 }
 
 namespace {
-// Exact-arithmetic rewrite forms of the plan, each of which can
-// be switched off for A/B parity experiments: NEGF_PLAN_DISABLE is a comma list
-// of mirror_schur, mirror_g, mirror_p, symdiag_g, symdiag_p, woodbury, sparse,
-// hull.
+// Exact-arithmetic rewrite forms of the plan.  On by default:
+// symdiag_g / symdiag_p (each off-diagonal block pair of a diagonal-only
+// quadratic form once, from 2 Psi), sparse (stencil-entry leaf Psi / Schur
+// contributions), hull (structural zero columns skipped).  Off by default,
+// because they measurably lose accuracy against the dense truth at
+// ill-conditioned energies (profiles/parity_forms_r02.txt):
+// mirror_schur / mirror_g / mirror_p (upper triangle of a symmetric /
+// anti-Hermitian block computed, the lower one copied) and woodbury (leaf
+// diagonals from diag(inv) + diag(W M W^T)).  NEGF_PLAN_FORMS (a comma list)
+// replaces the set for A/B experiments.
 bool form_on(const char* name) {
-  const char* e = std::getenv("NEGF_PLAN_DISABLE");
-  if (!e) return true;
-  const std::string s = std::string(",") + e + ",";
-  return s.find(std::string(",") + name + ",") == std::string::npos;
+  const char* e = std::getenv("NEGF_PLAN_FORMS");
+  const std::string s = std::string(",") + (e ? e : "symdiag_g,symdiag_p,sparse,hull") + ",";
+  return s.find(std::string(",") + name + ",") != std::string::npos;
 }
 }  // namespace
 
@@ -600,10 +631,7 @@ Plan build_plan(ProblemDesc desc) {
     for (int c = 0; c < nc; ++c) {
       const int64_t m = B.msz(c);
       if (m <= kSmemInvMax) continue;
-      if (m > kBigMax)
-        fail(kContractViolation, "cluster of " + std::to_string(m) + " dofs exceeds the supported block size " +
-                                     std::to_string(kBigMax));
-      need[B.lev(c)] += align8(m * kPanel) * 2 + align8((m + 3) / 4) + 8;
+      need[B.lev(c)] += big_scratch_elems(m);
     }
     P.big_scratch = rows_begin;
     cur = std::max(cur, align8(rows_begin + *std::max_element(need.begin(), need.end())));
@@ -1393,7 +1421,7 @@ Plan build_plan(ProblemDesc desc) {
 }
 
 LeadPlan build_lead_plan(int w) {
-  if (w <= 0 || w > kBigMax) fail(kContractViolation, "lead: block size out of range");
+  if (w <= 0) fail(kContractViolation, "lead: block size out of range");
   LeadPlan L;
   L.w = w;
   Plan& P = L.P;
@@ -1401,7 +1429,7 @@ LeadPlan build_lead_plan(int w) {
   for (int b = 0; b < LB_COUNT; ++b) L.off[b] = b * w2;
   P.big_scratch = LB_COUNT * w2;
   // scratch for two simultaneous big inverses (g and m)
-  const int64_t per = w > kSmemInvMax ? align8(int64_t(w) * kPanel) * 2 + align8((w + 3) / 4) + 8 : 0;
+  const int64_t per = w > kSmemInvMax ? big_scratch_elems(w) : 0;
   P.arena = P.big_scratch + 2 * per;
   Builder B(P);
   auto& T = P.gemm_terms;
@@ -1505,7 +1533,6 @@ Plan build_rgf_plan(ProblemDesc desc, std::vector<std::vector<int>> layers) {
     if (nl[static_cast<size_t>(l)] == 0) fail(kContractViolation, "layer map has an empty layer");
     R.max_layer = std::max(R.max_layer, nl[static_cast<size_t>(l)]);
   }
-  if (R.max_layer > kBigMax) fail(kContractViolation, "layer larger than the inverse kernels support");
   // Entries coupling non-adjacent layers (H and Sigma^r are A's pattern).
   {
     std::vector<std::pair<int, int>> viol;
@@ -1565,7 +1592,7 @@ Plan build_rgf_plan(ProblemDesc desc, std::vector<std::vector<int>> layers) {
   const int64_t nm2 = int64_t(R.max_layer) * R.max_layer;
   const int64_t oT = take(nm2), oM = take(nm2), oPP = take(nm2), oTERM = take(nm2), oX = take(nm2);
   P.big_scratch = cur;
-  if (R.max_layer > kSmemInvMax) take(align8(int64_t(R.max_layer) * kPanel) * 2 + align8((R.max_layer + 3) / 4) + 8);
+  if (R.max_layer > kSmemInvMax) take(big_scratch_elems(R.max_layer));
   P.arena = cur;
   P.a_region = 0;
   for (int l = 0; l < L; ++l) {

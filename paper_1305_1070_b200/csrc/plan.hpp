@@ -124,11 +124,20 @@ struct InvTask {
 };
 
 // Blocks above kSmemInvMax are inverted by the multi-CTA blocked
-// Gauss-Jordan: per 8-column panel one K_PANEL launch (factor the panel, swap
-// rows, stage the pivot rows) and one grouped-GEMM rank-8 update, then one
-// K_PERM launch that undoes the interchanges.  Scratch lives in the arena.
+// Gauss-Jordan, in outer panels of kOuter columns, each factored as kPanel-
+// wide inner panels: per inner panel one K_PANEL launch (factor it with row
+// partial pivoting, apply its interchanges inside the outer panel, stage
+// M_p - I_p and the pivot rows) and one grouped-GEMM rank-kPanel update of the
+// outer panel's columns; per outer panel one K_BIGSWAP launch (its
+// interchanges on every other column, staging of the rank-kOuter operands)
+// and ONE grouped-GEMM rank-kOuter update of the whole block (K = 64: the
+// bulk of the m^3 work runs as compute-bound GEMM); finally one K_PERM launch
+// undoes the interchanges.  Any block size: the panel lives in shared memory
+// up to kPanelSmemMax rows, in arena scratch (L2) beyond.  Scratch lives in
+// the arena.
 constexpr int kPanel = 8;
-constexpr int kBigMax = 1664;  // panel (m x 8 complex) must fit in shared memory
+constexpr int kOuter = 64;
+constexpr int kPanelSmemMax = 1600;  // m x kPanel complex panel in shared memory (200 KB)
 
 struct BigTask {
   int m;
@@ -136,14 +145,21 @@ struct BigTask {
   int cluster;
   int pad;
   int64_t off;       // the block (m x m)
-  int64_t off_mp;    // M_p - I_p (m x kPanel)
-  int64_t off_rs;    // staged pivot rows (kPanel x m)
-  int64_t off_perm;  // m ints
+  int64_t off_mp;    // inner panel M_p - I_p (m x kPanel); the working panel when m > kPanelSmemMax
+  int64_t off_rs;    // inner staged pivot rows (kPanel x m)
+  int64_t off_mp64;  // outer panel M_p - I_p (m x kOuter)
+  int64_t off_rs64;  // outer staged pivot rows (kOuter x m); row buffers of K_PERM
+  int64_t off_perm;  // 3 m ints: perm, and K_PERM's two index maps
   int64_t off_thr;   // (threshold, failed flag)
 };
+// Complex elements of arena scratch one BigTask of size m needs.
+inline int64_t big_scratch_elems(int64_t m) {
+  auto a8 = [](int64_t x) { return (x + 7) & ~int64_t(7); };
+  return a8(m * kPanel) * 2 + a8(m * kOuter) * 2 + a8((3 * m + 3) / 4) + 8;
+}
 
 enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL = 4, K_PERM = 5, K_SKEW = 6,
-                    K_COMBINE = 7, K_SPSI = 8, K_SSCHUR = 9, K_LEAFDIAG = 10 };
+                    K_COMBINE = 7, K_SPSI = 8, K_SSCHUR = 9, K_LEAFDIAG = 10, K_BIGSWAP = 11 };
 
 // Psi_x = -inv_x A_{x,S(x)} for a leaf whose coupling block holds only the
 // energy-independent -H entries (no Schur fill below a leaf; contact and
@@ -207,6 +223,8 @@ struct Op {
   int phase;         // 0 fold, 1 G, 2 seed, 3 N fold, 4 P
   int level;
   int k0;            // K_PANEL: first column of the panel
+  int k1;            // K_PANEL / K_BIGSWAP: first column of the outer panel
+  int inv_update;    // K_GEMM: 1 = a rank-kPanel / rank-kOuter update inside a multi-CTA block inverse
   double cmul;       // executed complex multiply-adds per energy
 };
 
@@ -316,7 +334,14 @@ struct Plan {
   int max_block = 0;
 };
 
-constexpr int kSmemInvMax = 112;  // largest block inverted wholly in shared memory
+constexpr int kSmemInvMax = 112;  // largest block inverted by one CTA (registers / shared memory)
+// Single-CTA inverse kernel variants by block size (kernels.cu
+// launch_inverse, measured with tools/inv_bench.cu): <= 16 and 17..48
+// register-resident Gauss-Jordan, 49..64 and 65..kSmemInvMax shared-memory
+// blocked Gauss-Jordan (one launch per padded size m8 there, so each launch
+// sizes its shared memory for its own blocks).  The plan groups a level's
+// inverse tasks by this class, largest first.
+inline int inv_size_class(int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 48 ? 2 : m <= 64 ? 3 : 4; }
 // CTA tile extents per warp arrangement (see GemmTile::arr).
 constexpr int kArrTM[3] = {32, 16, 64};
 constexpr int kArrTN[3] = {32, 64, 16};

@@ -62,11 +62,12 @@ def workload_ref_problem(w, idx):
     idx = np.atleast_1d(np.asarray(idx))
     p = w.problem
     sr, sl = w.self_energies(idx)
-    ny = w.ny
-    w2 = ny * ny
     n = p.n
     L = np.asarray(p.atomic_groups[0], np.int32)
     R = np.asarray(p.atomic_groups[1], np.int32)
+    ny = len(L)  # contact width (both contacts are equally wide here)
+    assert len(R) == ny
+    w2 = ny * ny
     n_lesser = len(p.sl_rows)
     has_ph = n_lesser > 2 * w2
     ph = phl = None

@@ -194,3 +194,40 @@ def test_density_accumulator_device_view(cuda_ok):
     t.mul_(2.0)  # writes through to the accumulator
     torch.cuda.synchronize()
     assert np.allclose(s.density(), 2 * dens, rtol=1e-15, atol=0)
+
+
+@pytest.mark.parametrize("m", [113, 700, 2048])
+def test_large_block_inverse_any_size(m, cuda_ok):
+    """The multi-CTA blocked Gauss-Jordan (rank-64 outer updates) on one
+    cluster of m dofs, no size cap (inverse, dense.cpp:49-81 has none):
+    diag G^r = diag(A^-1) and diag G^< = diag(A^-1 S A^-H) against numpy, for
+    a random complex-symmetric A with row interchanges at most pivots; two
+    energies (a batch of arenas), a 2x2 dense skew Sigma^< block."""
+    rng = np.random.default_rng(m)
+    B = (rng.standard_normal((m, m)) + 1j * rng.standard_normal((m, m))) / np.sqrt(m)
+    A = B + B.T
+    S = np.zeros((m, m), complex)
+    S[:2, :2] = [[1j, 0.3 + 0.2j], [-0.3 + 0.2j, 0.5j]]  # skew-Hermitian
+    prob, sl = dense_problem(A, S, [-1], [list(range(m))])
+    s = negf.HscGpuSolver(negf.HscPlan(prob))
+    E = np.array([0.0, 0.25])
+    gr, gl = s.solve(E, [1.0, 1.0], None, np.stack([sl, sl]))
+    for q, e in enumerate(E):
+        ginv = np.linalg.inv(A + e * np.eye(m))  # A(E) = E I - H with H = -A
+        assert rel_err(gr[q], np.diag(ginv)) <= 1e-10
+        want = np.einsum("ij,jk,ik->i", ginv, S, ginv.conj())
+        assert rel_err(gl[q], want) <= 1e-10
+
+
+def test_large_block_singular_pivot(cuda_ok):
+    """A rank-deficient 300-dof block: SingularBlock with the pivot index of
+    the reference's partial-pivoting rule |u_kk| <= 1e-13 max|a|."""
+    m = 300
+    rng = np.random.default_rng(3)
+    U = rng.standard_normal((m, 150)) + 1j * rng.standard_normal((m, 150))
+    A = U @ U.T  # complex symmetric, rank 150
+    prob, sl = dense_problem(A, np.zeros((m, m), complex), [-1], [list(range(m))])
+    s = negf.HscGpuSolver(negf.HscPlan(prob))
+    with pytest.raises(negf.SingularBlock) as ei:
+        s.solve([0.0], [1.0], None, None)
+    assert ei.value.pivot_index == 150 and ei.value.energy_index == 0

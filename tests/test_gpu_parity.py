@@ -12,9 +12,18 @@ from tests.helpers import golden_names, load_golden, rel_err
 TOL = 1e-10
 
 
+# Plan form sets (NEGF_PLAN_FORMS): the product default, every rewrite form
+# (incl. the opt-in mirror / Woodbury ones) and none.
+FORM_SETS = {"default": None, "all": "symdiag_g,symdiag_p,sparse,hull,woodbury,mirror_schur,mirror_g,mirror_p",
+             "plain": ""}
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("forms", list(FORM_SETS))
 @pytest.mark.parametrize("name", golden_names())
-def test_golden_hsc_parity(name, cuda_ok):
+def test_golden_hsc_parity(name, forms, cuda_ok, monkeypatch):
+    if FORM_SETS[forms] is not None:
+        monkeypatch.setenv("NEGF_PLAN_FORMS", FORM_SETS[forms])
     rp, prob, hsc, dense = load_golden(name)
     plan = negf.HscPlan(prob)
     solver = negf.HscGpuSolver(plan)

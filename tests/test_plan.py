@@ -153,12 +153,15 @@ def test_gemm_tiles_cover_config2_exactly_once():
     _check_tiles_cover_exactly(negf.HscPlan(devices.config2(n_energies=2).problem))
 
 
-def test_sparse_leaf_paths_are_exercised():
-    """The sparse-leaf ops (K_SPSI 8, K_SSCHUR 9, K_LEAFDIAG 10) replace dense
-    products only where the plan proves them exact; the golden problems the
-    GPU parity tests run must cover each of them and the dense fallback
-    (seeded / fuzzed leaves), and config 2 sends every unseeded leaf down the
-    Woodbury path."""
+def test_sparse_leaf_paths_are_exercised(monkeypatch):
+    """The sparse-leaf ops (K_SPSI 8, K_SSCHUR 9) replace dense products only
+    where the plan proves them exact; the golden problems the GPU parity tests
+    run must cover each of them and the dense fallback (seeded / fuzzed
+    leaves).  The Woodbury leaf diagonals (K_LEAFDIAG 10) are off by default
+    (they lose accuracy at ill-conditioned energies) and, opted
+    in with NEGF_PLAN_FORMS, cover every unseeded leaf of config 2."""
+    from paper_1305_1070_b200 import devices
+
     seen = {8: 0, 9: 0, 10: 0}
     dense_leaf_fallback = False
     for name in golden_names():
@@ -167,12 +170,41 @@ def test_sparse_leaf_paths_are_exercised():
         for k in seen:
             seen[k] += int(o["count"][o["kind"] == k].sum())
         dense_leaf_fallback |= bool((o["kind"] == 8).any() and not (o["kind"] == 10).any())
-    assert all(v > 0 for v in seen.values()), seen
+    assert seen[8] > 0 and seen[9] > 0 and seen[10] == 0, seen
     assert dense_leaf_fallback
-    from paper_1305_1070_b200 import devices
-
+    assert not (negf.HscPlan(devices.config2(n_energies=2).problem).ops()["kind"] == 10).any()
+    monkeypatch.setenv("NEGF_PLAN_FORMS", WOODBURY_FORMS)
     plan = negf.HscPlan(devices.config2(n_energies=2).problem)
     o = plan.ops()
     t = plan.tree()
     leaves = int((np.asarray(t.level) == 1).sum())
     assert o["count"][o["kind"] == 10].tolist() == [leaves - 2, leaves - 2]  # all but the two contact leaves
+
+
+WOODBURY_FORMS = "symdiag_g,symdiag_p,sparse,hull,woodbury"
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_tree_matches_reference_at_baseline_size(cfg, tmp_path):
+    """Bit-exact nested dissection at the BASELINE sizes (2k .. 1M dofs):
+    the plan's tree against the reference's own build_tree + nested_dissection
+    (run.cpp:123-133, partition.cpp:271-326; oracle/_ref ref_driver --solver
+    tree), cluster for cluster: parent, level and the dof list."""
+    from oracle import refio
+    from paper_1305_1070_b200 import devices
+    from tests.helpers import workload_ref_problem
+
+    if not refio.ref_available():
+        pytest.skip("oracle/_ref not built")
+    w = devices.CONFIGS[cfg]()
+    rp, _, _ = workload_ref_problem(w, [0])
+    path = str(tmp_path / "p.bin")
+    refio.write_problem(rp, path)
+    r = refio.run_reference(path, str(tmp_path / "o.bin"), solver="tree")
+    assert r.status == 0, r.message
+    t = negf.HscPlan(w.problem).tree()
+    assert t.num_clusters == len(r.parent)
+    assert np.array_equal(t.parent, r.parent)
+    assert np.array_equal(t.level, r.level)
+    for a, b in zip(t.dofs, r.dofs):
+        assert np.array_equal(a, b)

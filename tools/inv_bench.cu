@@ -1,6 +1,9 @@
-// Micro-benchmark of the batched inverse kernels: inv_bench m blocks energies
+// Micro-benchmark of the batched inverse kernels:
+//   inv_bench m blocks energies [dominant=1]
+// dominant=0: random complex entries (row interchanges at most steps).
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "../paper_1305_1070_b200/csrc/kernels.cu"
@@ -9,12 +12,13 @@ using namespace negfb;
 
 int main(int argc, char** argv) {
   const int m = atoi(argv[1]), nb = atoi(argv[2]), nE = atoi(argv[3]);
+  const double dom = argc > 4 ? atof(argv[4]) : 1.0;
   const int64_t stride = int64_t(m) * m * nb;
   std::vector<double2> h(stride);
   for (int b = 0; b < nb; ++b)
     for (int i = 0; i < m; ++i)
       for (int j = 0; j < m; ++j)
-        h[int64_t(b) * m * m + i * m + j] = make_double2(drand48() - 0.5 + (i == j ? 2.0 * m : 0.0), drand48() - 0.5);
+        h[int64_t(b) * m * m + i * m + j] = make_double2(drand48() - 0.5 + (i == j ? 2.0 * m * dom : 0.0), drand48() - 0.5);
   double2* arena;
   cudaMalloc(&arena, sizeof(double2) * stride * nE);
   for (int e = 0; e < nE; ++e) cudaMemcpy(arena + e * stride, h.data(), sizeof(double2) * stride, cudaMemcpyHostToDevice);
@@ -39,7 +43,14 @@ int main(int argc, char** argv) {
   for (int rep = 0; rep < 4; ++rep) {
     for (int e = 0; e < nE; ++e) cudaMemcpy(arena + e * stride, h.data(), sizeof(double2) * stride, cudaMemcpyHostToDevice);
     cudaEventRecord(e0);
-    launch_inverse(b, dt, t.data(), nb, st, 0, L);
+    const char* shape = getenv("RG_SHAPE");  // force one register-inverse shape
+    dim3 grid(nb, nE);
+    if (!shape) launch_inverse(b, dt, t.data(), nb, st, 0, L);
+    else if (!strcmp(shape, "32x1")) k_inverse_rg<32, 1, 32><<<grid, 32>>>(arena, stride, dt, 0, st);
+    else if (!strcmp(shape, "32x2")) k_inverse_rg<32, 2, 16><<<grid, 64>>>(arena, stride, dt, 0, st);
+    else if (!strcmp(shape, "64x2")) k_inverse_rg<64, 2, 32><<<grid, 128>>>(arena, stride, dt, 0, st);
+    else if (!strcmp(shape, "64x4")) k_inverse_rg<64, 4, 16><<<grid, 256>>>(arena, stride, dt, 0, st);
+    else if (!strcmp(shape, "48x2")) k_inverse_rg<48, 2, 24><<<grid, 96>>>(arena, stride, dt, 0, st);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -61,7 +72,9 @@ int main(int argc, char** argv) {
       res = std::max(res, std::hypot(re, im));
     }
   const double fl = 8.0 * m * double(m) * m * nb * nE;
-  printf("m=%d blocks=%dx%d: %.3f ms  %.2f TF/s  residual %.2e (%s)\n", m, nb, nE, best, fl / best / 1e9, res,
-         cudaGetErrorString(cudaGetLastError()));
+  DevStatus hs;
+  cudaMemcpy(&hs, st, sizeof hs, cudaMemcpyDeviceToHost);
+  printf("m=%d blocks=%dx%d dom=%g: %.3f ms  %.2f TF/s  residual %.2e singular_key %llx (%s)\n", m, nb, nE, dom, best,
+         fl / best / 1e9, res, hs.singular_key, cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

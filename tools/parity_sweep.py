@@ -1,14 +1,14 @@
 """Per-energy parity study (test infrastructure; writes an .npz summary).
 
-GPU (product path, one plan per variant of the exact-arithmetic forms,
-NEGF_PLAN_DISABLE) vs the reference build oracle/_ref over a whole energy grid,
+GPU (product path, one plan per variant of the exact-arithmetic plan forms,
+NEGF_PLAN_FORMS) vs the reference build oracle/_ref over a whole energy grid,
 next to the reference's own floor: the same reference algorithm with a
 different matmul order (NEGF_SHIM_NAIVE=1).  With --dense (n <= 2500,
 oracle.hpp:14) every arm is also compared with the reference's dense oracle
 (dense_gr / dense_gless, oracle.cpp:27-65) as the truth.
 
     python tools/parity_sweep.py --cfg 2 --out gpurun_out/par/c2.npz \
-        --variants "base;mirror_schur,mirror_g,mirror_p"
+        --variants "base;plain;symdiag_g,symdiag_p,sparse,hull,woodbury"
 """
 import argparse
 import os
@@ -33,7 +33,7 @@ def workload(args):
     if args.cfg == 5:
         return devices.config5()
     if args.cfg == 3:
-        return devices.config3(complex_energy=args.complex_energy)
+        return devices.config3(n_cells=args.cells, complex_energy=args.complex_energy)
     return devices.config1()
 
 
@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--cfg", type=int, default=2)
     ap.add_argument("--ny", type=int, default=100)
     ap.add_argument("--nx", type=int, default=400)
+    ap.add_argument("--cells", type=int, default=600, help="config 3: unit cells of the tube")
     ap.add_argument("--complex-energy", action="store_true")
     ap.add_argument("--energies", default="", help="comma list of indices (default: whole grid)")
     ap.add_argument("--variants", default="base")
@@ -109,11 +110,13 @@ def main():
                     res[f"{name}_vs_dense_r"] = per_energy_err(ref[name].gr, ref["dense"].gr)
                     res[f"{name}_vs_dense_l"] = per_energy_err(ref[name].gless, ref["dense"].gless)
     for v in [x for x in args.variants.split(";") if x and x != "none"]:
+        # a variant is the comma list of enabled plan forms (NEGF_PLAN_FORMS);
+        # "base" = the product's default set, "none" = no rewrite form
         tag = v.replace(",", "+")
         if v == "base":
-            os.environ.pop("NEGF_PLAN_DISABLE", None)
+            os.environ.pop("NEGF_PLAN_FORMS", None)
         else:
-            os.environ["NEGF_PLAN_DISABLE"] = v
+            os.environ["NEGF_PLAN_FORMS"] = "" if v == "plain" else v
         plan = negf.HscPlan(w.problem)
         s = negf.HscGpuSolver(plan, max_energy_batch=args.batch or len(idx))
         s.set_residual_check(False)
@@ -132,7 +135,7 @@ def main():
               f"#>1e-10 {int((e > 1e-10).sum())}, median {np.median(e):.1e}, max resid {res[tag + '_resid'].max():.2e}",
               flush=True)
         del s, plan
-    os.environ.pop("NEGF_PLAN_DISABLE", None)
+    os.environ.pop("NEGF_PLAN_FORMS", None)
     os.makedirs(os.path.dirname(os.path.abspath(args.out)), exist_ok=True)
     np.savez(args.out, **res)
     if "naive" in ref:
