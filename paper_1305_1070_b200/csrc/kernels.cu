@@ -296,9 +296,119 @@ __device__ __forceinline__ double2 crcp(double2 a) {
   return make_double2(x / d, -y / d);
 }
 
+// One NB-column panel of the shared-memory blocked Gauss-Jordan, factored by
+// warp 0 with the panel held in registers: lane owns rows lane + 32 i (i <
+// RPL).  Rows are not moved while the panel is factored: each lane tracks the
+// current position of its rows (exactly the row interchanges of partial
+// pivoting, ties to the lowest position), the pivot row reaches every lane by
+// shuffles, and the panel is written back at the final positions -- no
+// shared-memory round trip per pivot.  Same pivots, singular rule and
+// per-element arithmetic as the shared-memory loop.  Returns false (after
+// reporting) on a singular pivot.
+template <int RPL, int NB>
+__device__ __forceinline__ bool panel_regs(double2* A, int ld, int m, int k0, int kb, double thr2, int* perm,
+                                           int* flag, DevStatus* st, int e_global, int fold_pos) {
+  const int lane = threadIdx.x & 31;
+  double2 v[RPL][NB];
+  int pos[RPL];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+    pos[i] = r;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) v[i][c] = (r < m) ? A[r * ld + k0 + c] : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int kk = 0; kk < NB; ++kk) {
+    if (kk >= kb) break;
+    const int k = k0 + kk;
+    double best = -1.0;
+    int bpos = 0x7fffffff, bslot = 0;
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      if (lane + 32 * i < m && pos[i] >= k) {
+        const double x = cnorm(v[i][kk]);
+        if (x > best || (x == best && pos[i] < bpos)) {
+          best = x;
+          bpos = pos[i];
+          bslot = i;
+        }
+      }
+    }
+    const unsigned key = best >= 0.0 ? __float_as_uint(__double2float_ru(best)) : 0u;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+    const unsigned tied = __ballot_sync(0xffffffffu, best >= 0.0 && key == kmax);
+    int wl;
+    if (__popc(tied) <= 1) {
+      wl = tied ? __ffs(tied) - 1 : 0;
+    } else {  // exact order among the lanes whose float images tie
+      double cb = (best >= 0.0 && key == kmax) ? best : -1.0;
+      int cp = (best >= 0.0 && key == kmax) ? bpos : 0x7fffffff, cl = lane;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, cb, o);
+        const int op = __shfl_xor_sync(0xffffffffu, cp, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, cl, o);
+        if (ob > cb || (ob == cb && op < cp)) {
+          cb = ob;
+          cp = op;
+          cl = ol;
+        }
+      }
+      wl = cl;
+    }
+    const double wb = __shfl_sync(0xffffffffu, best, wl);
+    if (!(wb > thr2) && wb == wb) {  // |u_kk| <= 1e-13 max|a| (NaN passes, as the smem loop)
+      if (lane == 0) {
+        *flag = 1;
+        report_singular(st, e_global, fold_pos, k);
+      }
+      return false;
+    }
+    const int p = __shfl_sync(0xffffffffu, bpos, wl);
+    const int ws = __shfl_sync(0xffffffffu, bslot, wl);
+    if (lane == 0) perm[k] = p;
+    double2 pr[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      double2 x = v[0][c];
+#pragma unroll
+      for (int i = 1; i < RPL; ++i)
+        if (ws == i) x = v[i][c];
+      pr[c].x = __shfl_sync(0xffffffffu, x.x, wl);
+      pr[c].y = __shfl_sync(0xffffffffu, x.y, wl);
+    }
+    const double2 piv = pr[kk];
+    const double rd = 1.0 / fma(piv.x, piv.x, piv.y * piv.y);
+    const double2 ip = make_double2(piv.x * rd, -piv.y * rd);
+#pragma unroll
+    for (int c = 0; c < NB; ++c) pr[c] = (c == kk) ? ip : cmul(pr[c], ip);
+    const double2 nip = make_double2(-ip.x, -ip.y);
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) {
+      if (lane == wl && i == ws) {
+#pragma unroll
+        for (int c = 0; c < NB; ++c) v[i][c] = pr[c];
+      } else {
+        const double2 f = v[i][kk];
+#pragma unroll
+        for (int c = 0; c < NB; ++c) v[i][c] = (c == kk) ? cmul(f, nip) : csub(v[i][c], cmul(f, pr[c]));
+      }
+      if (pos[i] == k) pos[i] = p;
+      else if (pos[i] == p) pos[i] = k;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < RPL; ++i)
+    if (lane + 32 * i < m)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) A[pos[i] * ld + k0 + c] = v[i][c];
+  return true;
+}
+
 template <bool kGlobal, int RPL, int NB>
 // blocks <= 32 wide need few registers and little shared memory: 6 CTAs/SM
-__global__ void __launch_bounds__(INV_THREADS, RPL == 1 ? 6 : 4) k_inverse_blocked(double2* arena, int64_t stride,
+__global__ void __launch_bounds__(INV_THREADS, RPL == 1 ? 6 : 3) k_inverse_blocked(double2* arena, int64_t stride,
                                                                  const InvTask* __restrict__ tasks, int e_base,
                                                                  DevStatus* st) {
   extern __shared__ double2 sm[];
@@ -353,7 +463,13 @@ __global__ void __launch_bounds__(INV_THREADS, RPL == 1 ? 6 : 4) k_inverse_block
       }
       __syncthreads();
     }
+#ifndef NEGF_PANEL_SMEM
     if (!kGlobal && warp == 0) {
+      panel_regs<RPL, NB>(A, ld, m, k0, kb, thresh * thresh, perm, flag, st, e_base + blockIdx.y, tk.fold_pos);
+    } else if (false) {
+#else
+    if (!kGlobal && warp == 0) {
+#endif
       // Compact panel loop on warp 0: lane owns rows lane + 32 i (i < RPL);
       // the pivot row is read by broadcast from shared memory and the
       // elimination runs in registers.  Argmax: hardware max-reduction on the

@@ -97,7 +97,8 @@ def analytic_lead_sigma(energy: float, eta: float, t: float, phi: np.ndarray, ep
 def effective_mass_device(name: str, nx: int, ny: int, a_nm: float, m_eff: float, potential: np.ndarray,
                           energies: np.ndarray, eta: float, mu_l: float, mu_r: float, kT: float,
                           phonon_gamma: np.ndarray | None = None, max_leaf: int = 64,
-                          description: str = "", complex_energy: bool = False) -> Workload:
+                          description: str = "", complex_energy: bool = False,
+                          ref_orientation: bool = False) -> Workload:
     t = HBAR2_OVER_2M0 / (m_eff * a_nm * a_nm)
     n = nx * ny
     idx = np.arange(n).reshape(nx, ny)  # dof = x*ny + y
@@ -112,6 +113,8 @@ def effective_mass_device(name: str, nx: int, ny: int, a_nm: float, m_eff: float
     h_cols = np.concatenate(cols).astype(np.int32)
     h_vals = np.concatenate(vals).astype(np.complex128)
     coords = np.stack([np.repeat(np.arange(nx), ny), np.tile(np.arange(ny), nx)], 1).astype(np.float64)
+    if ref_orientation:  # the reference builders' convention: within-layer index first (device.cpp:120-121)
+        coords = coords[:, ::-1].copy()
     left, right = idx[0], idx[-1]
     lr, lc = np.meshgrid(left, left, indexing="ij")
     rr, rc = np.meshgrid(right, right, indexing="ij")
@@ -189,8 +192,12 @@ def config2(n_energies: int = 256, ny: int = 100, complex_energy: bool = False, 
                                  complex_energy=complex_energy)
 
 
-def config4(n_energies: int = 1024, nx: int = 1024, ny: int = 1024, complex_energy: bool = False) -> Workload:
-    """Wide 1024 x 1024 device, sum of 16 Gaussians (configs[3])."""
+def config4(n_energies: int = 1024, nx: int = 1024, ny: int = 1024, complex_energy: bool = False,
+            ref_orientation: bool = False) -> Workload:
+    """Wide 1024 x 1024 device, sum of 16 Gaussians (configs[3]).  With
+    ref_orientation the coordinates follow the reference builders (transverse
+    first): nested dissection then merges a dense contact into the top
+    separator, a 2557-dof root block."""
     r = MT19937_64(3)
     cx = r.uniform01(16) * nx
     cy = r.uniform01(16) * ny
@@ -200,8 +207,9 @@ def config4(n_energies: int = 1024, nx: int = 1024, ny: int = 1024, complex_ener
         v += 0.05 * np.exp(-((X - cx[i]) ** 2 + (Y - cy[i]) ** 2) / (2.0 * 20.0 ** 2))
     e = uniform_grid(0.0, 0.3, n_energies)
     return effective_mass_device(f"cfg4_em_{nx}x{ny}", nx, ny, 0.5, 0.067, v, e, 1e-6, 0.1, 0.0, 0.025,
-                                 description="2D effective mass, 16 Gaussians 0.05 eV width 20a, seed 3",
-                                 complex_energy=complex_energy)
+                                 description="2D effective mass, 16 Gaussians 0.05 eV width 20a, seed 3"
+                                             + (", reference coordinate orientation" if ref_orientation else ""),
+                                 complex_energy=complex_energy, ref_orientation=ref_orientation)
 
 
 def config5(n_energies: int = 2048, nx: int = 512, ny: int = 512) -> Workload:

@@ -184,7 +184,7 @@ def test_sparse_leaf_paths_are_exercised(monkeypatch):
 WOODBURY_FORMS = "symdiag_g,symdiag_p,sparse,hull,woodbury"
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, "4ref"])
 def test_tree_matches_reference_at_baseline_size(cfg, tmp_path):
     """Bit-exact nested dissection at the BASELINE sizes (2k .. 1M dofs):
     the plan's tree against the reference's own build_tree + nested_dissection
@@ -196,7 +196,9 @@ def test_tree_matches_reference_at_baseline_size(cfg, tmp_path):
 
     if not refio.ref_available():
         pytest.skip("oracle/_ref not built")
-    w = devices.CONFIGS[cfg]()
+    # "4ref": config 4 in the reference builders' coordinate orientation (the
+    # 2557-dof root block)
+    w = devices.config4(ref_orientation=True) if cfg == "4ref" else devices.CONFIGS[cfg]()
     rp, _, _ = workload_ref_problem(w, [0])
     path = str(tmp_path / "p.bin")
     refio.write_problem(rp, path)

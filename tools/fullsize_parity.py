@@ -10,7 +10,8 @@ from oracle import refio
 from paper_1305_1070_b200 import devices, negf
 
 cfg = int(sys.argv[1]); idx = np.array([int(x) for x in sys.argv[2].split(",")])
-w = devices.config5() if cfg == 5 else devices.config4() if cfg == 4 else devices.config2()
+ref_or = len(sys.argv) > 3 and sys.argv[3] == "ref"
+w = devices.config5() if cfg == 5 else devices.config4(ref_orientation=ref_or) if cfg == 4 else devices.config2()
 p = w.problem
 sr, sl = w.self_energies(idx)
 ny = w.ny; w2 = ny * ny; n = p.n

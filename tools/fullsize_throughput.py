@@ -19,7 +19,7 @@ from paper_1305_1070_b200 import devices, negf  # noqa: E402
 PEAK = 37.18  # measured DMMA TFLOP/s (profiles/fp64_peak_r01.txt)
 
 cfg = int(sys.argv[1])
-w = devices.config5() if cfg == 5 else devices.config4()
+w = devices.config5() if cfg == 5 else devices.config4(ref_orientation=len(sys.argv) > 2 and sys.argv[2] == "ref")
 t0 = time.time()
 plan = negf.HscPlan(w.problem)
 plan_s = time.time() - t0
@@ -57,6 +57,12 @@ for cname, lo, hi in (("leaves", 1, 1), ("levels 2-4", 2, 4), ("levels >= 5", 5,
     t = float(op_ms[sel].sum())
     if t > 0:
         by_level[f"gemm {cname}"] = round(8.0 * float(ops["cmul"][sel].sum()) * B / (t * 1e-3) / 1e12, 2)
+inv = {}
+for name, sel in (("inverse (single CTA)", ops["kind"] == 0), ("panel", ops["kind"] == 4), ("perm", ops["kind"] == 5),
+                  ("bigswap", ops["kind"] == 11), ("inverse GEMM updates", (ops["kind"] == 1) & (ops["phase"] == 6))):
+    t = float(op_ms[sel].sum())
+    inv[name] = {"ms": round(t, 2), "launches": int(sel.sum()),
+                 "tflops": round(8.0 * float(ops["cmul"][sel].sum()) * B / (t * 1e-3) / 1e12, 2) if t > 0 else None}
 exec_gf = info.exec_flops / 1e9
 out = dict(config=cfg, n_dofs=info.n_dofs, clusters=info.n_clusters, levels=info.levels,
            max_block=info.max_block, arena_mib_per_energy=info.arena_bytes_per_energy / 2**20, batch=B, ms=ms,
@@ -65,5 +71,5 @@ out = dict(config=cfg, n_dofs=info.n_dofs, clusters=info.n_clusters, levels=info
            step_tflops=exec_gf * B / ms, step_frac=exec_gf * B / ms / PEAK,
            gemm_tflops=8.0 * ks["gemm"]["cmul"] / (ks["gemm"]["ms"] * 1e-3) / 1e12,
            kernels_ms={k: round(v["ms"], 1) for k, v in ks.items()}, gemm_tflops_by_level=by_level,
-           plan_s=plan_s, max_real_residual=solver.max_real_residual)
+           plan_s=plan_s, max_real_residual=solver.max_real_residual, inverse_ops=inv)
 print(json.dumps(out))
