@@ -1141,11 +1141,15 @@ __global__ void __launch_bounds__(ROWS * H, (ROWS * H <= 64) ? 8 : (ROWS * H <= 
 template <bool kSmemPanel>
 __global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride, const BigTask* __restrict__ tasks,
                                                   int k0, int o0, int e_base, DevStatus* st) {
-  extern __shared__ double2 pn_smem[];  // m x kPanel panel
+  // Panel rows in shared memory are padded to kPanel + 1 complex (144 B):
+  // thread r's 16-byte accesses to row r then fall on distinct banks (a
+  // 128-byte pitch would put every lane of a phase on the same banks).
+  constexpr int PP = kSmemPanel ? kPanel + 1 : kPanel;
+  extern __shared__ double2 pn_smem[];  // m x PP panel
   __shared__ double red_v[8];
   __shared__ int red_i[8];
   __shared__ double s_thr;
-  __shared__ int s_fail, s_piv;
+  __shared__ int s_fail;
   const BigTask tk = tasks[blockIdx.x];
   const int m = tk.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double2* base = arena + blockIdx.y * stride;
@@ -1174,24 +1178,26 @@ __global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride
   }
   __syncthreads();
   if (s_fail) return;
-  const double thresh = s_thr;
+  const double thr2 = s_thr * s_thr;
   const int kb = min(kPanel, m - k0);
   for (int i = tid; i < m * kPanel; i += 256) {
     const int r = i / kPanel, c = i - r * kPanel;
-    pn[i] = c < kb ? A[int64_t(r) * m + k0 + c] : make_double2(0.0, 0.0);
+    pn[r * PP + c] = c < kb ? A[int64_t(r) * m + k0 + c] : make_double2(0.0, 0.0);
   }
   __syncthreads();
   for (int kk = 0; kk < kb; ++kk) {
     const int k = k0 + kk;
+    // 1. argmax |a_rk|^2 over rows r >= k (lowest row among equals)
     double best = -1.0;
-    int bi = k;
+    int bi = 0x7fffffff;
     for (int r = k + tid; r < m; r += 256) {
-      const double v = cnorm(pn[r * kPanel + kk]);
+      const double v = cnorm(pn[r * PP + kk]);
       if (v > best) {
         best = v;
         bi = r;
       }
     }
+#pragma unroll
     for (int o = 16; o; o >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
@@ -1205,41 +1211,47 @@ __global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride
       red_i[warp] = bi;
     }
     __syncthreads();
-    if (tid == 0) {
-      double b2 = red_v[0];
-      int i2 = red_i[0];
-      for (int w2 = 1; w2 < 8; ++w2)
-        if (red_v[w2] > b2 || (red_v[w2] == b2 && red_i[w2] < i2)) {
-          b2 = red_v[w2];
-          i2 = red_i[w2];
-        }
-      if (sqrt(b2) <= thresh) {
-        s_fail = 1;
-        *thr = make_double2(thresh, 1.0);
+    // 2. every thread combines the warps' candidates (same winner everywhere)
+    double b2 = red_v[0];
+    int p = red_i[0];
+#pragma unroll
+    for (int w2 = 1; w2 < 8; ++w2)
+      if (red_v[w2] > b2 || (red_v[w2] == b2 && red_i[w2] < p)) {
+        b2 = red_v[w2];
+        p = red_i[w2];
+      }
+    if (!(b2 > thr2) && b2 == b2) {  // |u_kk| <= 1e-13 max|a| (uniform)
+      if (tid == 0) {
+        *thr = make_double2(s_thr, 1.0);
         report_singular(st, e_base + blockIdx.y, tk.fold_pos, k);
       }
-      s_piv = i2;
-      perm[k] = i2;
+      return;
+    }
+    const double2 ip = crcp(pn[p * PP + kk]);
+    double2 rowp = make_double2(0.0, 0.0), rowk = make_double2(0.0, 0.0);
+    if (tid < kPanel) {
+      rowp = pn[p * PP + tid];
+      rowk = pn[k * PP + tid];
+    }
+    if (tid == 0) perm[k] = p;
+    __syncthreads();
+    // 3. interchange rows k and p, normalise the pivot row
+    if (tid < kPanel) {
+      pn[k * PP + tid] = (tid == kk) ? ip : cmul(rowp, ip);
+      if (p != k) pn[p * PP + tid] = rowk;
     }
     __syncthreads();
-    if (s_fail) return;
-    const int p = s_piv;
-    if (p != k && tid < kPanel) {
-      const double2 t2 = pn[k * kPanel + tid];
-      pn[k * kPanel + tid] = pn[p * kPanel + tid];
-      pn[p * kPanel + tid] = t2;
-    }
-    __syncthreads();
-    const double2 ip = crcp(pn[k * kPanel + kk]);
-    if (tid < kPanel) pn[k * kPanel + tid] = (tid == kk) ? ip : cmul(pn[k * kPanel + tid], ip);
-    __syncthreads();
+    // 4. eliminate column k from every other row
+    double2 pr[kPanel];
+#pragma unroll
+    for (int c = 0; c < kPanel; ++c) pr[c] = pn[k * PP + c];
     for (int r = tid; r < m; r += 256) {
       if (r == k) continue;
-      const double2 f = pn[r * kPanel + kk];
+      const double2 f = pn[r * PP + kk];
 #pragma unroll
       for (int c = 0; c < kPanel; ++c)
-        pn[r * kPanel + c] = (c == kk) ? make_double2(-(f.x * ip.x - f.y * ip.y), -(f.x * ip.y + f.y * ip.x))
-                                       : csub(pn[r * kPanel + c], cmul(f, pn[k * kPanel + c]));
+        pn[r * PP + c] = (c == kk) ? make_double2(-(f.x * ip.x - f.y * ip.y), -(f.x * ip.y + f.y * ip.x))
+                                   : csub(pn[r * PP + c], cmul(f, pr[c]));
     }
     __syncthreads();
   }
@@ -1247,7 +1259,7 @@ __global__ void __launch_bounds__(256) k_bigpanel(double2* arena, int64_t stride
   double2* mp = base + tk.off_mp;
   for (int i = tid; i < m * kPanel; i += 256) {
     const int r = i / kPanel, c = i - r * kPanel;
-    double2 v = pn[i];
+    double2 v = pn[r * PP + c];
     if (c < kb) A[int64_t(r) * m + k0 + c] = v;
     else v = make_double2(0.0, 0.0);
     if (r == k0 + c) v.x -= 1.0;
@@ -1311,8 +1323,11 @@ __global__ void __launch_bounds__(256) k_bigswap(double2* arena, int64_t stride,
 }
 
 // Undo the row interchanges as column interchanges, last first.  The index
-// maps live in shared memory (8 m bytes), the row buffers in the arena's
-// outer-panel scratch (kOuter x m >= 4 rows).
+// maps live in shared memory (8 m bytes; every CTA of a block derives them --
+// a serial pass over m swaps -- in parallel), the rows are split over
+// gridDim.z CTAs x 4 warps, each warp with its own row buffer in the arena's
+// outer-panel scratch (kOuter x m: kBigPermChunks * 4 <= kOuter rows).
+constexpr int kBigPermChunks = 16;
 __global__ void __launch_bounds__(128) k_bigperm(double2* arena, int64_t stride, const BigTask* __restrict__ tasks) {
   extern __shared__ int pmaps[];  // pos_of[m], cur_at[m]
   const BigTask tk = tasks[blockIdx.x];
@@ -1335,8 +1350,9 @@ __global__ void __launch_bounds__(128) k_bigperm(double2* arena, int64_t stride,
     for (int q = 0; q < m; ++q) pos_of[cur_at[q]] = q;
   }
   __syncthreads();
-  double2* buf = base + tk.off_rs64 + int64_t(warp) * m;
-  for (int r = warp; r < m; r += 4) {
+  const int wid = blockIdx.z * 4 + warp, nw = gridDim.z * 4;
+  double2* buf = base + tk.off_rs64 + int64_t(wid) * m;
+  for (int r = wid; r < m; r += nw) {
     for (int c = lane; c < m; c += 32) buf[c] = A[int64_t(r) * m + c];
     __syncwarp();
     for (int c = lane; c < m; c += 32) A[int64_t(r) * m + pos_of[c]] = buf[c];
@@ -1964,7 +1980,7 @@ void launch_bigpanel(const BatchArgs& b, const BigTask* d_tasks, const BigTask* 
   int mmax = 0;
   for (int i = 0; i < count; ++i) mmax = std::max(mmax, h_tasks[i].m);
   if (mmax <= kPanelSmemMax) {
-    const size_t smem = size_t(mmax) * kPanel * sizeof(double2);
+    const size_t smem = size_t(mmax) * (kPanel + 1) * sizeof(double2);
     static std::atomic<unsigned long long> attr{0};
     if (first_on_device(attr))
       cudaFuncSetAttribute(k_bigpanel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1990,7 +2006,8 @@ void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h
   const size_t smem = size_t(2) * mmax * sizeof(int);
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr)) cudaFuncSetAttribute(k_bigperm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  k_bigperm<<<dim3(count, b.nE), 128, smem, s>>>(b.arena, b.stride, d_tasks);
+  static_assert(kBigPermChunks * 4 <= kOuter, "k_bigperm row buffers live in the outer-panel scratch");
+  k_bigperm<<<dim3(count, b.nE, kBigPermChunks), 128, smem, s>>>(b.arena, b.stride, d_tasks);
   ++launches;
 }
 

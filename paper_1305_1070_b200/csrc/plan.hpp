@@ -137,7 +137,7 @@ struct InvTask {
 // the arena.
 constexpr int kPanel = 8;
 constexpr int kOuter = 64;
-constexpr int kPanelSmemMax = 1600;  // m x kPanel complex panel in shared memory (200 KB)
+constexpr int kPanelSmemMax = 1400;  // m x (kPanel + 1) complex panel in shared memory (<= 197 KB)
 
 struct BigTask {
   int m;

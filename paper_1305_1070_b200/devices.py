@@ -6,18 +6,18 @@ Input generation only (outside the drop-in boundary): each builder returns a
 
 Conventions fixed here (the reference leaves them open):
 * dof = x * Ny + y with x the transport coordinate (layers are columns x),
-  coords = (x, y): the top separator of config 4 is then the 1024-dof column
-  the BASELINE names;
-* A(E) uses the complex energy E + i*eta on the whole diagonal, as the
-  BASELINE configs state ("E + i eta"): it enters through the Sigma^r pattern
-  as -i*eta on every dof (the reference's phonon-diagonal slot, with no
-  Sigma^< counterpart), on top of the eta already inside the lead
-  self-energies.  With eta only in the leads (the reference CLI convention,
-  block.cpp:141-146) the interior Schur complements of the nested-dissection
-  fold are undamped finite-segment resolvents and go numerically singular at
-  many energies; two correct FP64 runs of the reference then disagree at O(1)
-  (config 3) -- see DESIGN.md section 4.  ``complex_energy=False`` restores the
-  reference convention;
+  coords = (x, y) by default: the top separator of config 4 is then the
+  1024-dof column the BASELINE names;
+* A(E) = E I - H - Sigma^r(E) with real E and eta only inside the lead
+  self-energies -- the reference CLI convention (block.cpp:141-146,
+  device.cpp:207) -- for every config by default (``complex_energy=False``).
+  ``complex_energy=True`` adds -i*eta on every dof through the Sigma^r pattern
+  (the reference's phonon-diagonal slot, with no Sigma^< counterpart), i.e.
+  A = (E + i eta) I - H - Sigma, the BASELINE wording ("E + i eta"); at
+  eta = 1e-6 it does not cure the ill-conditioned energies (DESIGN.md §4);
+* ``ref_orientation`` (config 4) puts the within-layer index in coordinate 0
+  as the reference builders do (device.cpp:120-121): nested dissection then
+  merges a dense contact into the top separator (a 2557-dof root);
 * random draws: std::mt19937_64(seed) + uniform01 (synthetic.hpp:18-20), onsite
   potential first in dof order, then any further draws;
 * effective-mass leads: analytic semi-infinite uniform lead,
