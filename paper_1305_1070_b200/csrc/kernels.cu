@@ -2061,7 +2061,8 @@ __global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, 
     }
     __syncthreads();
   }
-  // leaves in gather order; within one leaf its touched rows x columns in parallel
+  // leaves in gather order per target entry; leaves touching disjoint rows x
+  // columns run concurrently (waves, SschurContrib::sync)
   for (int q = 0; q < tk.contrib_count; ++q) {
     const SschurContrib ct = contrib[tk.contrib_begin + q];
     const SpsiTask& lt = spsi[ct.spsi];
@@ -2083,7 +2084,7 @@ __global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, 
       double2* dst = tgt + int64_t(r) * tk.ld + c;
       *dst = cadd(*dst, acc);
     }
-    __syncthreads();
+    if (ct.sync) __syncthreads();  // end of a wave of disjoint leaves
   }
 }
 

@@ -377,11 +377,31 @@ bool form_on(const char* name) {
 
 Plan build_plan(ProblemDesc desc) {
   Plan P;
-  const bool f_mirror_schur = form_on("mirror_schur"), f_mirror_g = form_on("mirror_g"),
-             f_mirror_p = form_on("mirror_p"), f_symdiag_g = form_on("symdiag_g"),
-             f_symdiag_p = form_on("symdiag_p"), f_woodbury = form_on("woodbury"), f_sparse = form_on("sparse"),
-             f_hull = form_on("hull");
   P.desc = std::move(desc);
+  // The symmetric forms need A(E) complex symmetric, as the reference's lean
+  // fold already assumes (it reads only the (descendant, ancestor)
+  // orientation, hsc.cpp:483-490): H symmetric in values, Sigma^r in pattern
+  // (its values are the caller's, per energy).  Otherwise they stay off.
+  bool a_symmetric = true;
+  {
+    std::map<std::pair<int, int>, cplx> hm;
+    for (std::size_t k = 0; k < P.desc.h_rows.size(); ++k) hm[{P.desc.h_rows[k], P.desc.h_cols[k]}] += P.desc.h_vals[k];
+    for (const auto& kv : hm) {
+      auto it = hm.find({kv.first.second, kv.first.first});
+      if (it == hm.end() || it->second != kv.second) {
+        a_symmetric = false;
+        break;
+      }
+    }
+    std::set<std::pair<int, int>> sp;
+    for (std::size_t k = 0; k < P.desc.sr_rows.size(); ++k) sp.insert({P.desc.sr_rows[k], P.desc.sr_cols[k]});
+    for (const auto& e : sp)
+      if (!sp.count({e.second, e.first})) a_symmetric = false;
+  }
+  const bool f_mirror_schur = a_symmetric && form_on("mirror_schur"), f_mirror_g = a_symmetric && form_on("mirror_g"),
+             f_mirror_p = a_symmetric && form_on("mirror_p"), f_symdiag_g = a_symmetric && form_on("symdiag_g"),
+             f_symdiag_p = a_symmetric && form_on("symdiag_p"), f_woodbury = form_on("woodbury"),
+             f_sparse = form_on("sparse"), f_hull = form_on("hull");
   const ProblemDesc& d = P.desc;
   const int n = d.n;
   if (n <= 0) fail(kContractViolation, "problem: no dofs");
@@ -970,6 +990,32 @@ Plan build_plan(ProblemDesc desc) {
         cm += double(cpp[B.msz(jp)] - cpp[0]) * (cpq[B.msz(jq)] - cpq[0]);  // entry pairs
       }
       st.contrib_count = static_cast<int>(P.sschur_contrib.size()) - st.contrib_begin;
+      if (st.contrib_count > 0) {  // waves of row x column-disjoint contributions
+        auto* cb0 = P.sschur_contrib.data() + st.contrib_begin;
+        const int nq = st.contrib_count;
+        std::vector<int> wave(static_cast<std::size_t>(nq), 0);
+        auto overlap = [&](int a, int b, int off_a, int off_b, int na, int nb) {
+          const int* x = P.sschur_rc.data() + cb0[a].rc_begin + off_a;
+          const int* y = P.sschur_rc.data() + cb0[b].rc_begin + off_b;
+          for (int i = 0; i < na; ++i)
+            for (int j = 0; j < nb; ++j)
+              if (x[i] == y[j]) return true;
+          return false;
+        };
+        for (int q2 = 0; q2 < nq; ++q2)
+          for (int q1 = 0; q1 < q2; ++q1)
+            if (overlap(q1, q2, 0, 0, cb0[q1].nr, cb0[q2].nr) &&
+                overlap(q1, q2, cb0[q1].nr, cb0[q2].nr, cb0[q1].nc, cb0[q2].nc))
+              wave[q2] = std::max(wave[q2], wave[q1] + 1);
+        std::vector<int> ord(static_cast<std::size_t>(nq));
+        std::iota(ord.begin(), ord.end(), 0);
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return wave[a] < wave[b]; });
+        std::vector<SschurContrib> sorted;
+        for (int q2 : ord) sorted.push_back(cb0[q2]);
+        for (int q2 = 0; q2 < nq; ++q2)
+          sorted[q2].sync = (q2 + 1 == nq || wave[ord[q2 + 1]] != wave[ord[q2]]) ? 1 : 0;
+        std::copy(sorted.begin(), sorted.end(), cb0);
+      }
       had_sparse.push_back(st.contrib_count > 0);
       if (!st.contrib_count) continue;
       st.mp = J.m;

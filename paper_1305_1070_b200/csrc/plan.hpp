@@ -214,6 +214,12 @@ struct SschurContrib {
   int p_off, q_off;             // column offsets of jp and of jq in A_{i,S}
   int nr, nc;                   // target rows / columns the leaf touches (nonempty columns)
   int rc_begin;                 // nr row then nc column indices in Plan::sschur_rc
+  int sync;                     // 1: last of its wave (a barrier follows).  Contributions are
+                                // ordered by wave: a contribution is in the wave after the
+                                // latest earlier one (gather order) whose rows x columns it
+                                // overlaps, so every target entry still receives its leaves
+                                // in gather order while disjoint leaves run concurrently
+  int pad;
 };
 
 struct Op {

@@ -9,8 +9,8 @@ reference's own algorithm (hsc_fold + hsc_gless, oracle/_ref) drift apart
 there: the maximum, over
   * the same algorithm with another matmul summation order (NEGF_SHIM_NAIVE=1:
     i-k-j loops instead of OpenBLAS ZGEMM), and
-  * three runs on inputs perturbed by one unit in the last place (H and the
-    contact self-energies, relative +-2^-52 per component, seeds 1-3) --
+  * eight runs on inputs perturbed by one unit in the last place (H and the
+    contact self-energies, relative +-2^-52 per component, seeds 1-8) --
     the rounding any FP64 producer of those inputs already carries,
 of max_j |g_j - o_j| / max_j |o_j| against the unperturbed OpenBLAS run, for
 diag G^r and diag G^< separately.  Also stored: the reference's own
@@ -53,7 +53,7 @@ def main() -> None:
         os.environ["NEGF_SHIM_NAIVE"] = "1"
         arms.append(("naive", refio.run_reference(path, os.path.join(tmp, "n.out"), threads=threads)))
         del os.environ["NEGF_SHIM_NAIVE"]
-        for seed in (1, 2, 3):
+        for seed in range(1, 9):
             rng = np.random.default_rng(seed)
             q = workload_ref_problem(w, idx)[0]
             q.h_vals = ulp_perturb(np.asarray(q.h_vals), rng)
