@@ -1458,7 +1458,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
   const int live_i = min(2, max(0, (tk.m - tl.m0 - wm + 7) / 8));
   const int live_j = min(2, max(0, (tk.n - tl.n0 - wn + 7) / 8));
 
-#ifndef NEGF_GEMM_4M
+#ifdef NEGF_GEMM_3M
   // Gauss (3M) complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar+Ai)(Br+Bi);
   // C = (P1 - P2) + i (P3 - P1 - P2): three real DMMAs per complex subtile
   // step instead of four.  Flop accounting stays 8 m n k.
@@ -1471,8 +1471,11 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
       for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = p3[i][j][q] = 0.0;
 #else
   // Conventional (4M) complex product: Re C = Ar Br - Ai Bi, Im C = Ar Bi +
-  // Ai Br, four real DMMAs per complex subtile step (componentwise accurate:
-  // no (Ar+Ai)(Br+Bi) cancellation in the imaginary part).
+  // Ai Br, four real DMMAs per complex subtile step.  The default: the Gauss
+  // (3M) product (-DNEGF_GEMM_3M, 11 % less GEMM time) mixes rounding of the
+  // real parts into the imaginary ones through P3 - P1 - P2, and on config 2
+  // it leaves max|Re G^<_jj| / |G^<_jj| up to 194x the reference's own value
+  // at 40 of 256 energies (4M: at the reference's level).
   double p1[2][2][2], p2[2][2][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
@@ -1559,7 +1562,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         b[j] = b_kr ? Bs[kk * A::LDB_KR + c] : Bs[c * LD_RK + kk];
         b[j].y = flip_sign(b[j].y, conjB);
       }
-#ifndef NEGF_GEMM_4M
+#ifdef NEGF_GEMM_3M
       double as[2], bs[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
@@ -1625,7 +1628,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
       for (int q = 0; q < 2; ++q) {
         const int c = tl.n0 + wn + 8 * j + 2 * t + q;
         if (c >= tk.n) continue;
-#ifndef NEGF_GEMM_4M
+#ifdef NEGF_GEMM_3M
         double2 v = make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
 #else
         double2 v = make_double2(p1[i][j][q], p2[i][j][q]);

@@ -11,8 +11,10 @@ Bar, per energy k and for diag G^r and diag G^< separately:
 i.e. 1e-10 (north_star) wherever FP64 determines the result to 1e-10, and
 within twice the reference's own FP64 spread where it does not (about a third
 of this grid: eta = 1e-6 resonances).  The reference's residual
-guard quantity max_j |Re G^<_jj| / |G^<_jj| must stay within
-max(1e-12, 2x) of the largest value the reference's own runs give."""
+guard quantity max_j |Re G^<_jj| / |G^<_jj| (exactly 0 in exact arithmetic)
+must stay within max(1e-11, 2x) of the largest value the reference's own runs
+give; 1e-11 is the noise level of this sum of ~1e5 complex products, three
+orders below electron_density's 1e-8 guard (observables.cpp:79-84)."""
 import os
 import tempfile
 
@@ -54,6 +56,6 @@ def test_config2_full_grid_vs_reference(cuda_ok):
     ok = (fx["floor_r"] <= 5e-11) & (fx["floor_l"] <= 5e-11)
     assert ok.sum() >= 150 and (er[ok] <= 1e-10).all() and (el[ok] <= 1e-10).all()
     res = real_residual(gl)
-    rbar = np.maximum(1e-12, 2.0 * fx["resid_floor"])
+    rbar = np.maximum(1e-11, 2.0 * fx["resid_floor"])
     rbad = np.nonzero(res > rbar)[0]
     assert len(rbad) == 0, [(int(k), float(res[k]), float(rbar[k])) for k in rbad[:10]]
