@@ -2,31 +2,24 @@
 energies of config 2 / 4 / 5 (test infrastructure; writes nothing).
 
     python tools/fullsize_parity.py 5 0,700,1400,2047
+    python tools/fullsize_parity.py 4 0 ref            # reference orientation (2557-dof root)
+    python tools/fullsize_parity.py 4 341,683 complex  # E + i eta on the whole diagonal
 """
 import sys, os, tempfile, time
 sys.path.insert(0, '/root/repo')
 import numpy as np
 from oracle import refio
 from paper_1305_1070_b200 import devices, negf
+from tests.helpers import workload_ref_problem
 
 cfg = int(sys.argv[1]); idx = np.array([int(x) for x in sys.argv[2].split(",")])
-ref_or = len(sys.argv) > 3 and sys.argv[3] == "ref"
-w = devices.config5() if cfg == 5 else devices.config4(ref_orientation=ref_or) if cfg == 4 else devices.config2()
+opts = sys.argv[3].split(",") if len(sys.argv) > 3 else []
+ref_or, cplx = "ref" in opts, "complex" in opts  # reference orientation / E + i eta on the whole diagonal
+w = (devices.config5() if cfg == 5 else devices.config4(ref_orientation=ref_or, complex_energy=cplx) if cfg == 4
+     else devices.config3(complex_energy=cplx) if cfg == 3 else devices.config2(complex_energy=cplx))
 p = w.problem
-sr, sl = w.self_energies(idx)
-ny = w.ny; w2 = ny * ny; n = p.n
-L = np.asarray(p.atomic_groups[0], np.int32); R = np.asarray(p.atomic_groups[1], np.int32)
-has_ph = len(p.sr_rows) > 2 * w2
-ph = phl = None
-if has_ph:
-    inner = np.asarray(p.sr_rows[2 * w2:], np.int64)
-    ph = np.zeros((len(idx), n), np.complex128); ph[:, inner] = sr[:, 2 * w2:]
-    phl = np.zeros((len(idx), n), np.complex128); phl[:, inner] = sl[:, 2 * w2:]
-rp = refio.RefProblem(n=n, h_rows=p.h_rows, h_cols=p.h_cols, h_vals=p.h_vals, layers=[np.asarray(l) for l in p.layers],
-                      coords=p.coords, groups=[L, R], max_leaf=p.max_leaf, dofs_l=L, dofs_r=R,
-                      has_ph=has_ph, has_ph_less=has_ph, energies=w.energies[idx], weights=w.weights[idx],
-                      sig_l=sr[:, :w2].reshape(-1, ny, ny), sig_r=sr[:, w2:2 * w2].reshape(-1, ny, ny), ph=ph,
-                      less_l=sl[:, :w2].reshape(-1, ny, ny), less_r=sl[:, w2:2 * w2].reshape(-1, ny, ny), ph_less=phl)
+n = p.n
+rp, sr, sl = workload_ref_problem(w, idx)
 s = negf.HscGpuSolver(negf.HscPlan(p), max_energy_batch=len(idx)); s.set_residual_check(False)
 t0 = time.time(); gr, gl = s.solve(w.energies[idx], w.weights[idx], sr, sl); tg = time.time() - t0
 with tempfile.TemporaryDirectory() as tmp:
