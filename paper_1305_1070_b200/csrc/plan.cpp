@@ -610,15 +610,6 @@ Plan build_plan(ProblemDesc desc) {
     if (c == root) ci.off_gd = ci.off_d;  // G_rr = (A_rr folded)^-1 (hsc.cpp:148-150)
     else ci.off_gd = take(ci.full_g ? int64_t(ci.m) * ci.m : int64_t(ci.m));
     if (P.any_seed && c != root) ci.off_pd = take(ci.full_p ? int64_t(ci.m) * ci.m : int64_t(ci.m));
-    // fused-diagonal partials: one per row and 16-column group of each row task
-    if (!ci.full_g && c != root && ci.m > 0) {
-      for (int j : ci.gcols) ci.gpart_np += (B.msz(j) + 15) / 16;
-      if (ci.gpart_np) ci.off_gpart = take(int64_t(ci.m) * ci.gpart_np);
-    }
-    if (P.any_seed && !ci.full_p && c != root && ci.m > 0) {
-      for (int j : ci.pcols) ci.ppart_np += (B.msz(j) + 15) / 16;
-      if (ci.ppart_np) ci.off_ppart = take(int64_t(ci.m) * ci.ppart_np);
-    }
   }
   // Row storage, by liveness.  The multi-CTA inverse scratch lives only in
   // the fold, G rows from the G^r sweep to the seeds (hsc.cpp:229-237), P rows
@@ -880,6 +871,34 @@ Plan build_plan(ProblemDesc desc) {
   if (!f_hull)
     for (int c = 0; c < nc; ++c)
       for (std::size_t q = 0; q < B.I(c).S.size(); ++q) nzr[static_cast<std::size_t>(c)][q] = {0, B.msz(B.I(c).S[q])};
+  // Fused-diagonal row tasks (rows of never-referenced clusters feed only
+  // diag(G_xx) / diag(P_xx) = sum_c Psi[r][c] op(C[r][c])) need only the
+  // output columns where Psi_{x,j} can be nonzero: the hull of its coupling
+  // block.  The other columns are multiplied by exact zeros, so the task is
+  // restricted to the hull (empty hull: no task).  Partials: one per row and
+  // 16-column group of each restricted task.
+  auto out_hull = [&](int x, int j) -> std::array<int, 2> {
+    const int p = find_pos(B.I(x).S, j);
+    return p < 0 ? std::array<int, 2>{0, 0} : nzr[static_cast<std::size_t>(x)][static_cast<std::size_t>(p)];
+  };
+  for (int c = 0; c < nc; ++c) {
+    ClusterInfo& ci = B.I(c);
+    if (!ci.full_g && c != root && ci.m > 0) {
+      for (int j : ci.gcols) {
+        const auto h = out_hull(c, j);
+        if (h[1] > h[0]) ci.gpart_np += (h[1] - h[0] + 15) / 16;
+      }
+      if (ci.gpart_np) ci.off_gpart = take(int64_t(ci.m) * ci.gpart_np);
+    }
+    if (P.any_seed && !ci.full_p && c != root && ci.m > 0) {
+      for (int j : ci.pcols) {
+        const auto h = out_hull(c, j);
+        if (h[1] > h[0]) ci.ppart_np += (h[1] - h[0] + 15) / 16;
+      }
+      if (ci.ppart_np) ci.off_ppart = take(int64_t(ci.m) * ci.ppart_np);
+    }
+  }
+  P.arena = std::max(P.arena, cur);
   // Woodbury diagonals of the sparse, never-referenced, unseeded leaves
   // (LeafDiagTask): per leaf its boundary rows T and, per mode, the gathered
   // upper triangle of M.
@@ -1151,9 +1170,14 @@ Plan build_plan(ProblemDesc desc) {
     for (int x : xs) {
       const ClusterInfo& X = B.I(x);
       if (leaf_wood[static_cast<std::size_t>(x)]) continue;  // K_LEAFDIAG below
-      const bool sym = f_symdiag_g && !X.full_g && X.off_gpart >= 0 && X.off_psi2 >= 0;
+      const bool fused = !X.full_g && x != root;  // rows feed only diag(G_xx): not stored
+      const bool sym = f_symdiag_g && fused && X.off_gpart >= 0 && X.off_psi2 >= 0;
+      int gb = 0;  // partial group of this task
       for (std::size_t jj = 0; jj < X.gcols.size(); ++jj) {
         const int j = X.gcols[jj];
+        const auto oh = fused ? out_hull(x, j) : std::array<int, 2>{0, B.msz(j)};
+        if (oh[0] >= oh[1]) continue;  // Psi_{x,j} == 0: no diagonal contribution
+        const int c0 = oh[0], nw = oh[1] - oh[0];
         const int tb = static_cast<int>(T.size());
         const int jpos = find_pos(X.S, j);
         for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
@@ -1165,28 +1189,28 @@ Plan build_plan(ProblemDesc desc) {
           if (nz[0] >= nz[1]) continue;  // Psi_{x,k} == 0
           const int lo = nz[0], kn = nz[1] - nz[0];
           const int64_t a = (sym && static_cast<int>(kk) < jpos ? X.off_psi2 : X.off_psi) + X.s_col[kk] + lo;
-          if (k == j) B.add_term(T, kn, OP_N, a, X.K, OP_N, B.I(j).off_gd + int64_t(lo) * B.msz(j), B.msz(j), +1);
+          if (k == j)
+            B.add_term(T, kn, OP_N, a, X.K, OP_N, B.I(j).off_gd + int64_t(lo) * B.msz(j) + c0, B.msz(j), +1);
           else if (B.lev(k) < B.lev(j))
             B.add_term(T, kn, OP_N, a, X.K, OP_N,
-                       B.I(k).off_grow + int64_t(lo) * B.I(k).WG + B.col_of(B.I(k).gcols, B.I(k).gcol_off, j),
+                       B.I(k).off_grow + int64_t(lo) * B.I(k).WG + B.col_of(B.I(k).gcols, B.I(k).gcol_off, j) + c0,
                        B.I(k).WG, +1);
           else
             B.add_term(T, kn, OP_N, a, X.K, OP_T,
-                       B.I(j).off_grow + B.col_of(B.I(j).gcols, B.I(j).gcol_off, k) + lo, B.I(j).WG, +1);
+                       B.I(j).off_grow + int64_t(c0) * B.I(j).WG + B.col_of(B.I(j).gcols, B.I(j).gcol_off, k) + lo,
+                       B.I(j).WG, +1);
         }
-        if (!X.full_g && X.off_gpart >= 0) {  // rows feed only diag(G_xx): fused, not stored
-          int gb = 0;
-          for (std::size_t q = 0; q < jj; ++q) gb += (B.msz(X.gcols[q]) + 15) / 16;
-          const int kk = find_pos(X.S, j);
-          if (kk < 0) fail(kInternal, "plan: diagonal-only row outside the fill set");
+        if (fused) {
+          if (X.off_gpart < 0 || jpos < 0) fail(kInternal, "plan: diagonal-only row outside the fill set");
           B.pend_diag.dmode = 1;
           B.pend_diag.nostore = 1;
-          B.pend_diag.dpsi_off = X.off_psi + X.s_col[static_cast<std::size_t>(kk)];
+          B.pend_diag.dpsi_off = X.off_psi + X.s_col[static_cast<std::size_t>(jpos)] + c0;
           B.pend_diag.dpsi_ld = X.K;
           B.pend_diag.dpart_off = X.off_gpart + gb;
           B.pend_diag.dpart_ld = X.gpart_np;
+          gb += (nw + 15) / 16;
         }
-        B.gemm_task(X.m, B.msz(j), X.off_grow + X.gcol_off[jj], X.WG, MODE_SET, 0, 0, tb);
+        B.gemm_task(X.m, nw, X.off_grow + X.gcol_off[jj] + c0, X.WG, MODE_SET, 0, 0, tb);
       }
     }
     B.close();
@@ -1316,13 +1340,18 @@ Plan build_plan(ProblemDesc desc) {
         // w - conj(w) = 2i Im(w): each pair once from 2 Psi, imaginary part kept
         // (dmode 3).  The diagonal blocks' own real parts are rounding noise
         // (G^< is anti-Hermitian), so the whole sum keeps only its imaginary part.
-        const bool psym = f_symdiag_p && !X.full_p && X.off_ppart >= 0 && X.off_psi2 >= 0 && X.ncols.empty() && !X.has_nd;
+        const bool pfused = !X.full_p && x != root;  // rows feed only diag(P_xx): not stored
+        const bool psym = f_symdiag_p && pfused && X.off_ppart >= 0 && X.off_psi2 >= 0 && X.ncols.empty() && !X.has_nd;
+        int gb = 0;  // partial group of this task
         for (std::size_t jj = 0; jj < X.pcols.size(); ++jj) {
           const int j = X.pcols[jj];
+          const auto oh = pfused ? out_hull(x, j) : std::array<int, 2>{0, B.msz(j)};
+          if (oh[0] >= oh[1]) continue;  // Psi_{x,j} == 0: no diagonal contribution
+          const int c0 = oh[0], nw = oh[1] - oh[0];
           const int tb = static_cast<int>(T.size());
           const int np = find_pos(X.ncols, j);
           const int jpos = find_pos(X.S, j);
-          if (np >= 0) B.add_term(T, X.m, OP_N, X.off_d, X.m, OP_N, X.off_nrow + X.ncol_off[np], X.WN, +1);
+          if (np >= 0) B.add_term(T, X.m, OP_N, X.off_d, X.m, OP_N, X.off_nrow + X.ncol_off[np] + c0, X.WN, +1);
           for (std::size_t kk = 0; kk < X.S.size(); ++kk) {
             const int k = X.S[kk];
             if (psym && static_cast<int>(kk) > jpos) continue;
@@ -1330,28 +1359,28 @@ Plan build_plan(ProblemDesc desc) {
             if (nz[0] >= nz[1]) continue;  // Psi_{x,k} == 0
             const int lo = nz[0], kn = nz[1] - nz[0];
             const int64_t a = (psym && static_cast<int>(kk) < jpos ? X.off_psi2 : X.off_psi) + X.s_col[kk] + lo;
-            if (k == j) B.add_term(T, kn, OP_N, a, X.K, OP_N, B.I(j).off_pd + int64_t(lo) * B.msz(j), B.msz(j), +1);
+            if (k == j)
+              B.add_term(T, kn, OP_N, a, X.K, OP_N, B.I(j).off_pd + int64_t(lo) * B.msz(j) + c0, B.msz(j), +1);
             else if (B.lev(k) < B.lev(j))
               B.add_term(T, kn, OP_N, a, X.K, OP_N,
-                         B.I(k).off_prow + int64_t(lo) * B.I(k).WP + B.col_of(B.I(k).pcols, B.I(k).pcol_off, j),
+                         B.I(k).off_prow + int64_t(lo) * B.I(k).WP + B.col_of(B.I(k).pcols, B.I(k).pcol_off, j) + c0,
                          B.I(k).WP, +1);
             else
               B.add_term(T, kn, OP_N, a, X.K, OP_H,
-                         B.I(j).off_prow + B.col_of(B.I(j).pcols, B.I(j).pcol_off, k) + lo, B.I(j).WP, -1);
+                         B.I(j).off_prow + int64_t(c0) * B.I(j).WP + B.col_of(B.I(j).pcols, B.I(j).pcol_off, k) + lo,
+                         B.I(j).WP, -1);
           }
-          if (!X.full_p && X.off_ppart >= 0) {  // rows feed only diag(P_xx): fused, not stored
-            int gb = 0;
-            for (std::size_t q = 0; q < jj; ++q) gb += (B.msz(X.pcols[q]) + 15) / 16;
-            const int kk = find_pos(X.S, j);
-            if (kk < 0) fail(kInternal, "plan: diagonal-only row outside the fill set");
+          if (pfused) {
+            if (X.off_ppart < 0 || jpos < 0) fail(kInternal, "plan: diagonal-only row outside the fill set");
             B.pend_diag.dmode = psym ? 3 : 2;
             B.pend_diag.nostore = 1;
-            B.pend_diag.dpsi_off = X.off_psi + X.s_col[static_cast<std::size_t>(kk)];
+            B.pend_diag.dpsi_off = X.off_psi + X.s_col[static_cast<std::size_t>(jpos)] + c0;
             B.pend_diag.dpsi_ld = X.K;
             B.pend_diag.dpart_off = X.off_ppart + gb;
             B.pend_diag.dpart_ld = X.ppart_np;
+            gb += (nw + 15) / 16;
           }
-          B.gemm_task(X.m, B.msz(j), X.off_prow + X.pcol_off[jj], X.WP, MODE_SET, 0, 0, tb);
+          B.gemm_task(X.m, nw, X.off_prow + X.pcol_off[jj] + c0, X.WP, MODE_SET, 0, 0, tb);
         }
       }
       B.close();
