@@ -103,6 +103,9 @@ struct negf_gpu {
   SkewTask* d_skew_tasks = nullptr;
   SpsiTask* d_spsi = nullptr;
   int* d_spsi_colptr = nullptr;
+  int* d_spsi_wcols = nullptr;
+  MGatherTask* d_mg = nullptr;
+  MGatherBlock* d_mg_blocks = nullptr;
   int* d_spsi_row = nullptr;
   double2* d_spsi_val = nullptr;
   SschurTask* d_sschur = nullptr;
@@ -248,10 +251,11 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
     launch_output_gr(b, P.desc.n, g->d_gr_pos, d_gr, s, L);
     if (hk->gr_ready) ck(cudaEventRecord(hk->gr_ready, s), "event");
   };
-  static const int kind_stat[12] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
+  static const int kind_stat[13] = {NEGF_KSTAT_INVERSE, NEGF_KSTAT_GEMM,    NEGF_KSTAT_DIAG,
                                     NEGF_KSTAT_SCALE,   NEGF_KSTAT_INVERSE, NEGF_KSTAT_INVERSE,
                                     NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,   NEGF_KSTAT_SCALE,
-                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_DIAG,    NEGF_KSTAT_INVERSE};
+                                    NEGF_KSTAT_SCALE,   NEGF_KSTAT_DIAG,    NEGF_KSTAT_INVERSE,
+                                    NEGF_KSTAT_DIAG};
   // K_SPSI / K_SSCHUR: sparse, with the scalings; K_LEAFDIAG: diagonals;
   // K_BIGSWAP: part of the multi-CTA inverse
   for (size_t oi = 0; oi < P.ops.size(); ++oi) {
@@ -285,7 +289,11 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         launch_combine(b, g->d_comb_tasks, P.comb_tasks.data(), op.begin, op.count, s, L);
         break;
       case K_SPSI:
-        launch_spsi(b, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row, g->d_spsi_val, op.begin, op.count, s, L);
+        launch_spsi(b, g->d_spsi, g->d_spsi_colptr, g->d_spsi_row, g->d_spsi_val, g->d_spsi_wcols, op.begin, op.count,
+                    s, L);
+        break;
+      case K_MGATHER:
+        launch_mgather(b, g->d_mg, g->d_mg_blocks, op.begin, op.count, s, L);
         break;
       case K_LEAFDIAG:
         launch_leafdiag(b, g->d_ld, P.ld_tasks.data(), g->d_ld_rows, g->d_ld_optr, P.ld_optr.data(),
@@ -589,6 +597,9 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     g->d_skew_tasks = dev_upload(P.skew_tasks, o);
     g->d_spsi = dev_upload(P.spsi_tasks, o);
     g->d_spsi_colptr = dev_upload(P.spsi_colptr, o);
+    g->d_spsi_wcols = dev_upload(P.spsi_wcols, o);
+    g->d_mg = dev_upload(P.mg_tasks, o);
+    g->d_mg_blocks = dev_upload(P.mg_blocks, o);
     g->d_spsi_row = dev_upload(P.spsi_row, o);
     g->d_spsi_val = reinterpret_cast<double2*>(dev_upload(P.spsi_val, o));
     g->d_sschur = dev_upload(P.sschur_tasks, o);

@@ -2020,11 +2020,22 @@ void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h
 // (coalesced stores; inv_x is re-read from L1).
 __global__ void __launch_bounds__(256) k_spsi(double2* arena, int64_t stride, const SpsiTask* __restrict__ tasks,
                                               const int* __restrict__ colptr, const int* __restrict__ rows,
-                                              const double2* __restrict__ vals, int begin) {
+                                              const double2* __restrict__ vals, const int* __restrict__ wcols,
+                                              int begin) {
   const SpsiTask tk = tasks[begin + blockIdx.x];
   double2* base = arena + int64_t(blockIdx.y) * stride;
   const double2* inv = base + tk.off_inv;
   const int* cp = colptr + tk.col_begin;
+  if (tk.h > 0) {  // compact leaf: only the hull columns, Psi_H (m x h)
+    const int* wc = wcols + tk.wcol_begin;
+    for (int idx = threadIdx.x; idx < tk.m * tk.h; idx += blockDim.x) {
+      const int r = idx / tk.h, c = wc[idx - r * tk.h];
+      double2 acc = make_double2(0.0, 0.0);
+      for (int e = cp[c]; e < cp[c + 1]; ++e) acc = cadd(acc, cmul(inv[int64_t(r) * tk.m + rows[e]], vals[e]));
+      base[tk.off_psi + idx] = make_double2(-acc.x, -acc.y);
+    }
+    return;
+  }
   const int total = tk.m * tk.K;
   for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
     const int r = idx / tk.K, c = idx - r * tk.K;
@@ -2037,9 +2048,40 @@ __global__ void __launch_bounds__(256) k_spsi(double2* arena, int64_t stride, co
 }
 
 void launch_spsi(const BatchArgs& b, const SpsiTask* d_tasks, const int* d_colptr, const int* d_rows,
-                 const double2* d_vals, int begin, int count, cudaStream_t s, int64_t& launches) {
+                 const double2* d_vals, const int* d_wcols, int begin, int count, cudaStream_t s, int64_t& launches) {
   if (count <= 0) return;
-  k_spsi<<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, d_colptr, d_rows, d_vals, begin);
+  k_spsi<<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, d_colptr, d_rows, d_vals, d_wcols, begin);
+  ++launches;
+}
+
+// M of a compact leaf (MGatherTask): per block, coef * [conj] src[a rs + c cs]
+// into M[dst_row + a][dst_col + c] (coef 0: zeros).  One CTA per (leaf,
+// energy); consecutive threads on consecutive M columns.
+__global__ void __launch_bounds__(256) k_mgather(double2* arena, int64_t stride, const MGatherTask* __restrict__ tasks,
+                                                 const MGatherBlock* __restrict__ blocks, int begin) {
+  const MGatherTask tk = tasks[begin + blockIdx.x];
+  double2* base = arena + int64_t(blockIdx.y) * stride;
+  double2* M = base + tk.dst;
+  for (int q = 0; q < tk.block_count; ++q) {
+    const MGatherBlock bl = blocks[tk.block_begin + q];
+    for (int idx = threadIdx.x; idx < bl.rows * bl.cols; idx += blockDim.x) {
+      const int a = idx / bl.cols, c = idx - a * bl.cols;
+      double2 v = make_double2(0.0, 0.0);
+      if (bl.coef != 0.0) {
+        v = base[bl.src + a * bl.rs + c * bl.cs];
+        if (bl.conj) v.y = -v.y;
+        v.x *= bl.coef;
+        v.y *= bl.coef;
+      }
+      M[int64_t(bl.dst_row + a) * tk.h + bl.dst_col + c] = v;
+    }
+  }
+}
+
+void launch_mgather(const BatchArgs& b, const MGatherTask* d_tasks, const MGatherBlock* d_blocks, int begin, int count,
+                    cudaStream_t s, int64_t& launches) {
+  if (count <= 0) return;
+  k_mgather<<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, d_blocks, begin);
   ++launches;
 }
 

@@ -42,7 +42,9 @@ void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_
                  const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
                  cudaStream_t s, int64_t& launches);
 void launch_spsi(const BatchArgs& b, const SpsiTask* d_tasks, const int* d_colptr, const int* d_rows,
-                 const double2* d_vals, int begin, int count, cudaStream_t s, int64_t& launches);
+                 const double2* d_vals, const int* d_wcols, int begin, int count, cudaStream_t s, int64_t& launches);
+void launch_mgather(const BatchArgs& b, const MGatherTask* d_tasks, const MGatherBlock* d_blocks, int begin, int count,
+                    cudaStream_t s, int64_t& launches);
 void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurContrib* d_contrib,
                    const SpsiTask* d_spsi, const int* d_colptr, const int* d_rows, const double2* d_vals,
                    const int* d_rc, int begin, int count, cudaStream_t s, int64_t& launches);

@@ -88,6 +88,7 @@ struct Builder {
       case K_SPSI: cur.begin = static_cast<int>(P.spsi_tasks.size()); break;
       case K_SSCHUR: cur.begin = static_cast<int>(P.sschur_tasks.size()); break;
       case K_LEAFDIAG: cur.begin = static_cast<int>(P.ld_tasks.size()); break;
+      case K_MGATHER: cur.begin = static_cast<int>(P.mg_tasks.size()); break;
       default: cur.begin = static_cast<int>(P.scale_tasks.size()); break;
     }
   }
@@ -105,6 +106,7 @@ struct Builder {
       case K_SPSI: cur.count = static_cast<int>(P.spsi_tasks.size()) - cur.begin; break;
       case K_SSCHUR: cur.count = static_cast<int>(P.sschur_tasks.size()) - cur.begin; break;
       case K_LEAFDIAG: cur.count = static_cast<int>(P.ld_tasks.size()) - cur.begin; break;
+      case K_MGATHER: cur.count = static_cast<int>(P.mg_tasks.size()) - cur.begin; break;
       default: cur.count = static_cast<int>(P.scale_tasks.size()) - cur.begin; break;
     }
     if (cur.kind == K_GEMM && cur.count > 1) {
@@ -361,7 +363,9 @@ namespace {
 // Exact-arithmetic rewrite forms of the plan.  On by default:
 // symdiag_g / symdiag_p (each off-diagonal block pair of a diagonal-only
 // quadratic form once, from 2 Psi), sparse (stencil-entry leaf Psi / Schur
-// contributions), hull (structural zero columns skipped).  Off by default,
+// contributions), hull (structural zero columns skipped), compact (the
+// diagonal-only rows of sparse leaves as one gathered Psi_H M Psi_H^T form per
+// leaf, MGatherTask; hull only, so exact zeros are all it skips).  Off by default,
 // because they measurably lose accuracy against the dense truth at
 // ill-conditioned energies (profiles/parity_forms_r02.txt):
 // mirror_schur / mirror_g / mirror_p (upper triangle of a symmetric /
@@ -370,7 +374,7 @@ namespace {
 // replaces the set for A/B experiments.
 bool form_on(const char* name) {
   const char* e = std::getenv("NEGF_PLAN_FORMS");
-  const std::string s = std::string(",") + (e ? e : "symdiag_g,symdiag_p,sparse,hull") + ",";
+  const std::string s = std::string(",") + (e ? e : "symdiag_g,symdiag_p,sparse,hull,compact") + ",";
   return s.find(std::string(",") + name + ",") != std::string::npos;
 }
 }  // namespace
@@ -401,7 +405,7 @@ Plan build_plan(ProblemDesc desc) {
   const bool f_mirror_schur = a_symmetric && form_on("mirror_schur"), f_mirror_g = a_symmetric && form_on("mirror_g"),
              f_mirror_p = a_symmetric && form_on("mirror_p"), f_symdiag_g = a_symmetric && form_on("symdiag_g"),
              f_symdiag_p = a_symmetric && form_on("symdiag_p"), f_woodbury = form_on("woodbury"),
-             f_sparse = form_on("sparse"), f_hull = form_on("hull");
+             f_sparse = form_on("sparse"), f_hull = form_on("hull"), f_compact = form_on("compact");
   const ProblemDesc& d = P.desc;
   const int n = d.n;
   if (n <= 0) fail(kContractViolation, "problem: no dofs");
@@ -881,8 +885,39 @@ Plan build_plan(ProblemDesc desc) {
     const int p = find_pos(B.I(x).S, j);
     return p < 0 ? std::array<int, 2>{0, 0} : nzr[static_cast<std::size_t>(x)][static_cast<std::size_t>(p)];
   };
+  auto same_set = [](std::vector<int> x, std::vector<int> y) {
+    std::sort(x.begin(), x.end());
+    std::sort(y.begin(), y.end());
+    return x == y;
+  };
   for (int c = 0; c < nc; ++c) {
     ClusterInfo& ci = B.I(c);
+    const bool wood = f_woodbury && leaf_sparse[static_cast<std::size_t>(c)] && !ci.full_g && !ci.full_p &&
+                      !ci.seeded && !ci.has_nd && ci.ncols.empty() && ci.m > 0;
+    if (f_compact && f_hull && leaf_sparse[static_cast<std::size_t>(c)] && !wood && c != root && ci.m > 0 && ci.K > 0 &&
+        !ci.full_g && !ci.seeded && !ci.has_nd && ci.ncols.empty() && same_set(ci.gcols, ci.S) &&
+        (!P.any_seed || (!ci.full_p && same_set(ci.pcols, ci.S)))) {
+      int h = 0;
+      ci.hoff.assign(ci.S.size(), 0);
+      for (std::size_t q = 0; q < ci.S.size(); ++q) {
+        ci.hoff[q] = h;
+        const auto& r = nzr[static_cast<std::size_t>(c)][q];
+        if (r[1] > r[0]) h += r[1] - r[0];
+      }
+      if (h > 0) {
+        ci.compact = true;
+        ci.hc = h;
+        ci.gpart_np = (h + 15) / 16;
+        ci.off_gpart = take(int64_t(ci.m) * ci.gpart_np);
+        if (P.any_seed) {
+          ci.ppart_np = ci.gpart_np;
+          ci.off_ppart = take(int64_t(ci.m) * ci.ppart_np);
+        }
+        ci.off_psic = take(int64_t(ci.m) * h);
+        ci.off_mg = take(int64_t(h) * h);
+        continue;
+      }
+    }
     if (!ci.full_g && c != root && ci.m > 0) {
       for (int j : ci.gcols) {
         const auto h = out_hull(c, j);
@@ -1142,6 +1177,16 @@ Plan build_plan(ProblemDesc desc) {
         st.off_inv = I.off_d;
         st.off_psi = I.off_psi;
         st.off_psi2 = leaf_wood[static_cast<std::size_t>(x)] ? -1 : I.off_psi2;  // 2 Psi: the row forms only
+        if (I.compact) {  // only the hull columns, compacted (Psi_H); no 2 Psi
+          st.h = I.hc;
+          st.wcol_begin = static_cast<int>(P.spsi_wcols.size());
+          st.off_psi = I.off_psic;
+          st.off_psi2 = -1;
+          for (std::size_t q = 0; q < I.S.size(); ++q) {
+            const auto& r = nzr[static_cast<std::size_t>(x)][q];
+            for (int a = r[0]; a < r[1]; ++a) P.spsi_wcols.push_back(static_cast<int>(I.s_col[q]) + a);
+          }
+        }
         for (int c = 0; c < I.K; ++c) {
           P.spsi_colptr.push_back(static_cast<int>(P.spsi_row.size()));
           for (const auto& e : cols[static_cast<std::size_t>(c)]) {
@@ -1150,7 +1195,15 @@ Plan build_plan(ProblemDesc desc) {
           }
         }
         P.spsi_colptr.push_back(static_cast<int>(P.spsi_row.size()));
-        if (!closed) B.cur.cmul += double(I.m) * (P.spsi_colptr.back() - P.spsi_colptr[static_cast<std::size_t>(st.col_begin)]);
+        if (!closed && I.compact) {
+          for (int q = 0; q < I.hc; ++q) {
+            const int c = P.spsi_wcols[static_cast<std::size_t>(st.wcol_begin + q)];
+            B.cur.cmul += double(I.m) * (P.spsi_colptr[static_cast<std::size_t>(st.col_begin + c + 1)] -
+                                         P.spsi_colptr[static_cast<std::size_t>(st.col_begin + c)]);
+          }
+        } else if (!closed) {
+          B.cur.cmul += double(I.m) * (P.spsi_colptr.back() - P.spsi_colptr[static_cast<std::size_t>(st.col_begin)]);
+        }
         spsi_of[static_cast<std::size_t>(x)] = static_cast<int>(P.spsi_tasks.size());
         P.spsi_tasks.push_back(st);
       }
@@ -1163,13 +1216,103 @@ Plan build_plan(ProblemDesc desc) {
   P.exec_inv_cmul = 0;
   for (int c = 0; c < nc; ++c) P.exec_inv_cmul += double(B.msz(c)) * B.msz(c) * B.msz(c);
 
+  // M of a compact leaf (MGatherTask): the G_SS (mode 0) / P_SS (mode 1)
+  // blocks on the hull columns H, exactly the B operands of the row tasks it
+  // replaces -- block pair (k, j) at (hoff[k], hoff[j]).  Every pair is
+  // gathered (the reference's own sum, hsc.cpp:210-227 / 275-303): in this one
+  // product the symmetric forms would only turn half of M into zeros.
+  auto emit_mgather = [&](int x, int mode) {
+    const ClusterInfo& X = B.I(x);
+    const bool sym = false;
+    MGatherTask mt{};
+    mt.h = X.hc;
+    mt.dst = X.off_mg;
+    mt.block_begin = static_cast<int>(P.mg_blocks.size());
+    for (std::size_t qa = 0; qa < X.S.size(); ++qa) {
+      const auto ra = nzr[static_cast<std::size_t>(x)][qa];
+      if (ra[0] >= ra[1]) continue;
+      for (std::size_t qc = 0; qc < X.S.size(); ++qc) {
+        const auto rc = nzr[static_cast<std::size_t>(x)][qc];
+        if (rc[0] >= rc[1]) continue;
+        MGatherBlock mb{};
+        mb.dst_row = X.hoff[qa];
+        mb.dst_col = X.hoff[qc];
+        mb.rows = ra[1] - ra[0];
+        mb.cols = rc[1] - rc[0];
+        if (sym && qa > qc) {
+          mb.coef = 0.0;
+        } else {
+          const int k = X.S[qa], j = X.S[qc];
+          const double two = (sym && qa < qc) ? 2.0 : 1.0;
+          const ClusterInfo& Kc = B.I(k);
+          const ClusterInfo& Jc = B.I(j);
+          if (k == j) {
+            mb.src = (mode == 0 ? Jc.off_gd : Jc.off_pd) + int64_t(ra[0]) * B.msz(j) + rc[0];
+            mb.rs = B.msz(j);
+            mb.cs = 1;
+            mb.coef = two;
+          } else if (B.lev(k) < B.lev(j)) {
+            if (mode == 0) {
+              mb.src = Kc.off_grow + int64_t(ra[0]) * Kc.WG + B.col_of(Kc.gcols, Kc.gcol_off, j) + rc[0];
+              mb.rs = Kc.WG;
+            } else {
+              mb.src = Kc.off_prow + int64_t(ra[0]) * Kc.WP + B.col_of(Kc.pcols, Kc.pcol_off, j) + rc[0];
+              mb.rs = Kc.WP;
+            }
+            mb.cs = 1;
+            mb.coef = two;
+          } else {  // G_{k,j} = G_{j,k}^T;  P_{k,j} = -P_{j,k}^H
+            if (mode == 0) {
+              mb.src = Jc.off_grow + int64_t(rc[0]) * Jc.WG + B.col_of(Jc.gcols, Jc.gcol_off, k) + ra[0];
+              mb.cs = Jc.WG;
+              mb.coef = two;
+            } else {
+              mb.src = Jc.off_prow + int64_t(rc[0]) * Jc.WP + B.col_of(Jc.pcols, Jc.pcol_off, k) + ra[0];
+              mb.cs = Jc.WP;
+              mb.coef = -two;
+              mb.conj = 1;
+            }
+            mb.rs = 1;
+          }
+        }
+        P.mg_blocks.push_back(mb);  // a copy: no flops charged
+      }
+    }
+    mt.block_count = static_cast<int>(P.mg_blocks.size()) - mt.block_begin;
+    P.mg_tasks.push_back(mt);
+  };
+  // The single GEMM task of a compact leaf: Psi_H (m x h) M (h x h), only
+  // the fused diagonal kept (dmode 1: G, 2 / 3: P).
+  auto emit_compact_rows = [&](int x, int mode) {
+    const ClusterInfo& X = B.I(x);
+    const int tb = static_cast<int>(T.size());
+    B.add_term(T, X.hc, OP_N, X.off_psic, X.hc, OP_N, X.off_mg, X.hc, +1);
+    // P: diag(P_xx) of an anti-Hermitian P is imaginary; with the symdiag_p
+    // form the sum keeps only its imaginary part (dmode 3), as the row tasks do
+    B.pend_diag.dmode = mode == 0 ? 1 : (f_symdiag_p ? 3 : 2);
+    B.pend_diag.nostore = 1;
+    B.pend_diag.dpsi_off = X.off_psic;
+    B.pend_diag.dpsi_ld = X.hc;
+    B.pend_diag.dpart_off = mode == 0 ? X.off_gpart : X.off_ppart;
+    B.pend_diag.dpart_ld = mode == 0 ? X.gpart_np : X.ppart_np;
+    B.gemm_task(X.m, X.hc, X.off_mg, X.hc, MODE_SET, 0, 0, tb);
+  };
+
   // G^r extraction top-down (hsc.cpp:171-227).
   for (int l = t.levels() - 1; l >= 1; --l) {
     const auto& xs = by_level[l];
+    B.open(K_MGATHER, 1, l);
+    for (int x : xs)
+      if (B.I(x).compact) emit_mgather(x, 0);
+    B.close();
     B.open(K_GEMM, 1, l);
     for (int x : xs) {
       const ClusterInfo& X = B.I(x);
       if (leaf_wood[static_cast<std::size_t>(x)]) continue;  // K_LEAFDIAG below
+      if (X.compact) {
+        emit_compact_rows(x, 0);
+        continue;
+      }
       const bool fused = !X.full_g && x != root;  // rows feed only diag(G_xx): not stored
       const bool sym = f_symdiag_g && fused && X.off_gpart >= 0 && X.off_psi2 >= 0;
       int gb = 0;  // partial group of this task
@@ -1330,10 +1473,18 @@ Plan build_plan(ProblemDesc desc) {
     B.close();
     for (int l = t.levels() - 1; l >= 1; --l) {
       const auto& xs = by_level[l];
+      B.open(K_MGATHER, 4, l);
+      for (int x : xs)
+        if (B.I(x).compact) emit_mgather(x, 1);
+      B.close();
       B.open(K_GEMM, 4, l);
       for (int x : xs) {
         const ClusterInfo& X = B.I(x);
         if (leaf_wood[static_cast<std::size_t>(x)]) continue;  // K_LEAFDIAG below
+        if (X.compact) {
+          emit_compact_rows(x, 1);
+          continue;
+        }
         // Symmetric form of a diagonal-only, unseeded P row set:
         // diag(P_xx) = diag(Psi P_SS Psi^H) with P_SS anti-Hermitian (P_{j,k} =
         // -P_{k,j}^H, hsc.cpp:204-206), so the (k, j) and (j, k) block pairs sum to

@@ -159,7 +159,29 @@ inline int64_t big_scratch_elems(int64_t m) {
 }
 
 enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL = 4, K_PERM = 5, K_SKEW = 6,
-                    K_COMBINE = 7, K_SPSI = 8, K_SSCHUR = 9, K_LEAFDIAG = 10, K_BIGSWAP = 11 };
+                    K_COMBINE = 7, K_SPSI = 8, K_SSCHUR = 9, K_LEAFDIAG = 10, K_BIGSWAP = 11, K_MGATHER = 12 };
+
+// Compact leaves (sparse, never referenced, unseeded): their G / P rows feed
+// only diag(G_xx) / diag(P_xx) = sum_{a,c} Psi[r][a] M[a][c] Psi[r][c] over the
+// hull columns H of Psi_x (concatenated over S(x)), with M the G_SS / P_SS
+// blocks restricted to H x H (block pairs of the symmetric forms doubled, the
+// skipped ones zero).  K_MGATHER builds M per (leaf, energy); one grouped-GEMM
+// task per leaf then forms Psi_H M with the fused-diagonal epilogue.
+struct MGatherBlock {
+  int dst_row, dst_col;   // block origin in M (h x h, row-major)
+  int rows, cols;
+  int conj;               // 1: conjugate the source
+  int pad;
+  double coef;            // 0: zero block (no source)
+  int64_t src;            // source element (0, 0)
+  int64_t rs, cs;         // source strides per M row / column
+};
+struct MGatherTask {
+  int h;
+  int block_begin, block_count;
+  int pad;
+  int64_t dst;            // M (h x h)
+};
 
 // Psi_x = -inv_x A_{x,S(x)} for a leaf whose coupling block holds only the
 // energy-independent -H entries (no Schur fill below a leaf; contact and
@@ -169,6 +191,8 @@ enum OpKind : int { K_INVERSE = 0, K_GEMM = 1, K_DIAG = 2, K_SCALE = 3, K_PANEL 
 struct SpsiTask {
   int m, K;
   int col_begin;      // K + 1 entries of Plan::spsi_colptr from here
+  int h;              // > 0: compact Psi_H (m x h, the hull columns of Plan::spsi_wcols from
+  int wcol_begin;     //      wcol_begin) is written instead of the full m x K Psi
   int pad;
   int64_t off_inv;    // inv_x (m x m, row-major; the D block after inversion)
   int64_t off_psi;    // Psi_x (m x K)
@@ -266,6 +290,11 @@ struct ClusterInfo {
   int64_t off_gpart = -1, off_ppart = -1;  // fused-diagonal partials (m x NP)
   int64_t off_psi2 = -1;                   // 2 Psi (symmetric fused G diagonal)
   int gpart_np = 0, ppart_np = 0;
+  // compact leaf (see MGatherTask): hull width h, offsets of S's hull blocks in H
+  bool compact = false;
+  int hc = 0;
+  std::vector<int> hoff;
+  int64_t off_psic = -1, off_mg = -1;  // Psi_H (m x h), M (h x h)
 };
 
 // Region [off, off + rows*pitch) with `cols` leading elements per row.
@@ -317,6 +346,9 @@ struct Plan {
   std::vector<CombineTask> comb_tasks;   // RGF path only
   std::vector<SpsiTask> spsi_tasks;      // sparse leaf Psi (K_SPSI)
   std::vector<int> spsi_colptr;          // per task: K + 1 offsets into spsi_row / spsi_val
+  std::vector<int> spsi_wcols;           // compact leaves: written Psi columns (S space), H order
+  std::vector<MGatherTask> mg_tasks;     // K_MGATHER
+  std::vector<MGatherBlock> mg_blocks;
   std::vector<int> spsi_row;             // local row t of the entry
   std::vector<cplx> spsi_val;            // A_{x,S}[t][c] (= -H)
   std::vector<SschurTask> sschur_tasks;  // sparse leaf Schur contributions (K_SSCHUR)

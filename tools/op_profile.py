@@ -4,7 +4,7 @@
     python tools/op_profile.py run [reps]      # GPU: per-op ms / TF/s, grouped and top ops
 
 Kinds: 0 inverse, 1 gemm, 2 diag, 3 scale, 4 bigpanel, 5 bigperm, 6 skew, 7 combine,
-8 spsi, 9 sschur, 10 leafdiag, 11 bigswap.  Phases: 0 fold, 1 G, 2 seed, 3 N fold, 4 P, 6 big inverse.
+8 spsi, 9 sschur, 10 leafdiag, 11 bigswap, 12 mgather.  Phases: 0 fold, 1 G, 2 seed, 3 N fold, 4 P, 6 big inverse.
 """
 import collections
 import sys
@@ -14,7 +14,7 @@ import numpy as np  # noqa: E402
 
 NE = 256
 KIND = {0: "inverse", 1: "gemm", 2: "diag", 3: "scale", 4: "bigpanel", 5: "bigperm", 6: "skew", 7: "combine",
-        8: "spsi", 9: "sschur", 10: "leafdiag", 11: "bigswap"}
+        8: "spsi", 9: "sschur", 10: "leafdiag", 11: "bigswap", 12: "mgather"}
 PEAK = 37.18
 
 
