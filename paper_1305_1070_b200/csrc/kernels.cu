@@ -1583,6 +1583,27 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
       double nai[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) nai[i] = flip_sign(a[i].y, int(0x80000000));
+      if (live_i == 2 && live_j == 2) {
+        // all four subtiles live: the first product of every accumulator,
+        // then the second, so 8 independent DMMAs separate the dependent
+        // ones (the asm statements keep their order; same per-accumulator
+        // summation order as below)
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+            dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+          }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
+            dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
+          }
+        return;
+      }
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         if (i >= live_i) break;
