@@ -110,3 +110,32 @@ def test_full_size_properties(cfg, cuda_ok):
     d = s.density()
     contrib = w.weights[idx][:, None] * gl.imag / (2 * np.pi)
     assert (np.abs(d - contrib.sum(0)) <= 1e-12 * np.abs(contrib).sum(0) + 1e-300).all()
+
+
+@pytest.mark.slow
+def test_config5_full_size_vs_reference(cuda_ok):
+    """Config 5 at full size (512 x 512, 262k dofs, phonon self-energy on every
+    dof: a damped, well-conditioned problem) against the reference's own solver
+    (oracle/_ref: solve_all -> hsc_fold + hsc_gless) at two energies of its
+    grid: 1e-10 relative on diag G^r and diag G^< (north_star)."""
+    import os
+    import tempfile
+
+    from oracle import refio
+    from tests.helpers import per_energy_err, workload_ref_problem
+
+    if not refio.ref_available():
+        pytest.skip("oracle/_ref not built")
+    w = devices.config5()
+    idx = np.array([0, len(w.energies) - 1])
+    rp, sr, sl = workload_ref_problem(w, idx)
+    s = negf.HscGpuSolver(negf.HscPlan(w.problem), max_energy_batch=len(idx))
+    s.set_residual_check(False)
+    gr, gl = s.solve(w.energies[idx], w.weights[idx], sr, sl)
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "p.bin")
+        refio.write_problem(rp, path)
+        ref = refio.run_reference(path, os.path.join(tmp, "o.bin"), threads=len(idx))
+    assert ref.status == 0, ref.message
+    assert (per_energy_err(gr, ref.gr) <= TOL).all(), per_energy_err(gr, ref.gr)
+    assert (per_energy_err(gl, ref.gless) <= TOL).all(), per_energy_err(gl, ref.gless)
