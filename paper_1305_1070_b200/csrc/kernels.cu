@@ -2110,9 +2110,18 @@ void launch_mgather(const BatchArgs& b, const MGatherTask* d_tasks, const MGathe
 // T[r][c] (+)= sum over its leaves i (in gather order) of
 // (Psi_i^T A_i)[p_off + r][q_off + c] = -sum inv_i[t][t'] a(t', p_off + r) a(t, q_off + c)
 // over the stencil entries of the two columns of the leaf's A_{i,S} (Psi_i
-// itself is not needed).  One CTA per (target, energy), consecutive threads on
-// consecutive columns of a target row.
-__global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, const SschurTask* __restrict__ tasks,
+// itself is not needed).  One CTA per (target, energy), two schedules
+// (SschurTask::entry, chosen by the plan from the touched area):
+//  * entry: one thread per target entry walks the target's leaves in their
+//    stored order and skips those whose column pair at (r, c) is empty -- no
+//    barrier (small targets, densely touched: the low separator levels);
+//  * per leaf over its touched rows x columns, leaves touching disjoint rows
+//    x columns concurrently (waves, SschurContrib::sync) -- large targets with
+//    small touched areas.
+// Contributions are stored in waves, which keeps gather order for every
+// entry, so both schedules give every entry the same sums in the same order
+// as the reference's right-looking update.
+__global__ void __launch_bounds__(128) k_sschur(double2* arena, int64_t stride, const SschurTask* __restrict__ tasks,
                                                 const SschurContrib* __restrict__ contrib,
                                                 const SpsiTask* __restrict__ spsi, const int* __restrict__ colptr,
                                                 const int* __restrict__ rows, const double2* __restrict__ vals,
@@ -2120,6 +2129,38 @@ __global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, 
   const SschurTask tk = tasks[begin + blockIdx.x];
   double2* base = arena + int64_t(blockIdx.y) * stride;
   double2* tgt = base + tk.off;
+  auto leaf_term = [&](const SpsiTask& lt, const int* cb, int p0, int p1, int q0, int q1) {
+    const double2* inv = base + lt.off_inv;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int e2 = q0; e2 < q1; ++e2) {
+      const double2* irow = inv + int64_t(rows[e2]) * lt.m;
+      double2 z = make_double2(0.0, 0.0);
+      for (int e1 = p0; e1 < p1; ++e1) z = cadd(z, cmul(irow[rows[e1]], vals[e1]));
+      acc = csub(acc, cmul(z, vals[e2]));
+    }
+    (void)cb;
+    return acc;
+  };
+  if (tk.entry) {
+    for (int idx = threadIdx.x; idx < tk.mp * tk.mq; idx += blockDim.x) {
+      const int r = idx / tk.mq, c = idx - r * tk.mq;
+      double2* dst = tgt + int64_t(r) * tk.ld + c;
+      double2 sum = tk.mode == MODE_ADD ? *dst : make_double2(0.0, 0.0);  // a pure fill block starts from zero
+      bool touched = false;
+      for (int q = 0; q < tk.contrib_count; ++q) {
+        const SschurContrib& ct = contrib[tk.contrib_begin + q];
+        const SpsiTask& lt = spsi[ct.spsi];
+        const int* cb = colptr + lt.col_begin;
+        const int p0 = cb[ct.p_off + r], p1 = cb[ct.p_off + r + 1];
+        const int q0 = cb[ct.q_off + c], q1 = cb[ct.q_off + c + 1];
+        if (p0 == p1 || q0 == q1) continue;
+        sum = cadd(sum, leaf_term(lt, cb, p0, p1, q0, q1));
+        touched = true;
+      }
+      if (touched || tk.mode != MODE_ADD) *dst = sum;
+    }
+    return;
+  }
   if (tk.mode != MODE_ADD) {  // a pure fill block starts from zero
     for (int idx = threadIdx.x; idx < tk.mp * tk.mq; idx += blockDim.x) {
       const int r = idx / tk.mq, c = idx - r * tk.mq;
@@ -2127,28 +2168,18 @@ __global__ void __launch_bounds__(256) k_sschur(double2* arena, int64_t stride, 
     }
     __syncthreads();
   }
-  // leaves in gather order per target entry; leaves touching disjoint rows x
-  // columns run concurrently (waves, SschurContrib::sync)
   for (int q = 0; q < tk.contrib_count; ++q) {
     const SschurContrib ct = contrib[tk.contrib_begin + q];
     const SpsiTask& lt = spsi[ct.spsi];
     const int* R = rc + ct.rc_begin;
     const int* Cc = R + ct.nr;
-    const double2* inv = base + lt.off_inv;
     const int* cb = colptr + lt.col_begin;
     for (int idx = threadIdx.x; idx < ct.nr * ct.nc; idx += blockDim.x) {
       const int r = R[idx / ct.nc], c = Cc[idx % ct.nc];
       const int* cp = cb + ct.p_off + r;
       const int* cq = cb + ct.q_off + c;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int e2 = cq[0]; e2 < cq[1]; ++e2) {
-        const double2* irow = inv + int64_t(rows[e2]) * lt.m;
-        double2 z = make_double2(0.0, 0.0);
-        for (int e1 = cp[0]; e1 < cp[1]; ++e1) z = cadd(z, cmul(irow[rows[e1]], vals[e1]));
-        acc = csub(acc, cmul(z, vals[e2]));
-      }
       double2* dst = tgt + int64_t(r) * tk.ld + c;
-      *dst = cadd(*dst, acc);
+      *dst = cadd(*dst, leaf_term(lt, cb, cp[0], cp[1], cq[0], cq[1]));
     }
     if (ct.sync) __syncthreads();  // end of a wave of disjoint leaves
   }
@@ -2158,7 +2189,7 @@ void launch_sschur(const BatchArgs& b, const SschurTask* d_tasks, const SschurCo
                    const SpsiTask* d_spsi, const int* d_colptr, const int* d_rows, const double2* d_vals,
                    const int* d_rc, int begin, int count, cudaStream_t s, int64_t& launches) {
   if (count <= 0) return;
-  k_sschur<<<dim3(count, b.nE), 256, 0, s>>>(b.arena, b.stride, d_tasks, d_contrib, d_spsi, d_colptr, d_rows,
+  k_sschur<<<dim3(count, b.nE), 128, 0, s>>>(b.arena, b.stride, d_tasks, d_contrib, d_spsi, d_colptr, d_rows,
                                               d_vals, d_rc, begin);
   ++launches;
 }

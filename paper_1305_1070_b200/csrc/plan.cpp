@@ -1074,6 +1074,14 @@ Plan build_plan(ProblemDesc desc) {
       if (!st.contrib_count) continue;
       st.mp = J.m;
       st.mq = B.msz(jq);
+      {
+        int64_t touched = 0;
+        for (int q2 = 0; q2 < st.contrib_count; ++q2) {
+          const SschurContrib& c2 = P.sschur_contrib[static_cast<std::size_t>(st.contrib_begin + q2)];
+          touched += int64_t(c2.nr) * c2.nc;
+        }
+        st.entry = int64_t(st.mp) * st.mq <= 2 * touched ? 1 : 0;
+      }
       if (jp == jq) {
         st.ld = J.m;
         st.mode = MODE_ADD;

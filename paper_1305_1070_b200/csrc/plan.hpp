@@ -206,6 +206,10 @@ struct SpsiTask {
 struct SschurTask {
   int mp, mq, ld, mode;         // mode: MODE_ADD or MODE_SET
   int contrib_begin, contrib_count;
+  int entry;                    // 1: one thread per target entry over all leaves (small, densely
+                                //    touched targets); 0: per leaf over its touched rows x columns,
+                                //    waves of disjoint leaves between barriers (large targets)
+  int pad;
   int64_t off;                  // target block
 };
 // diag(G_xx) / diag(P_xx) of a never-referenced, unseeded sparse leaf by the

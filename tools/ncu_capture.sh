@@ -1,19 +1,29 @@
 # ncu evidence for one config-2 batch (256 energies): launch list + --set full
-# captures of the kernels DESIGN.md §3 lists.  Run on the GPU box after the
-# bench itself has exited 0 without ncu.  Outputs under gpurun_out/ncu/.
+# captures of the kernels DESIGN.md §3 lists, summarised on the box
+# (tools/ncu_summary.py; raw CSV pages kept, large reports dropped so the
+# merge-back stays small).  Run after the bench itself exited 0 without ncu.
 set -x
 mkdir -p gpurun_out/ncu
 B="python tools/launch_map.py batch 1"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu/launches.csv $B > gpurun_out/ncu/launches.log 2>&1
+python tools/launch_map.py ops gpurun_out/ncu/ops.json
+python tools/launch_map.py map gpurun_out/ncu/launches.csv gpurun_out/ncu/ops.json > gpurun_out/ncu/launch_map.txt 2>&1
 F="ncu --set full --clock-control none --import-source on"
-$F -k regex:k_gemm --launch-skip 26 -c 1 -o gpurun_out/ncu/gemm_lv9_fold $B > /dev/null 2>&1
-$F -k regex:k_gemm --launch-skip 101 -c 1 -o gpurun_out/ncu/gemm_lv2_grows $B > /dev/null 2>&1
-$F -k regex:k_gemm --launch-skip 103 -c 1 -o gpurun_out/ncu/gemm_lv1_compact $B > /dev/null 2>&1
-$F -k regex:k_inverse_blocked -c 1 -o gpurun_out/ncu/inverse_blocked $B > /dev/null 2>&1
-$F -k regex:k_inverse_rg -c 2 -o gpurun_out/ncu/inverse_rg $B > /dev/null 2>&1
-$F -k regex:k_inverse_la -c 1 -o gpurun_out/ncu/inverse_la $B > /dev/null 2>&1
-$F -k regex:k_bigpanel -c 1 -o gpurun_out/ncu/bigpanel $B > /dev/null 2>&1
-$F -k regex:k_sschur -c 1 -o gpurun_out/ncu/sschur $B > /dev/null 2>&1
-$F -k regex:k_spsi -c 1 -o gpurun_out/ncu/spsi $B > /dev/null 2>&1
-$F -k regex:k_mgather -c 1 -o gpurun_out/ncu/mgather $B > /dev/null 2>&1
-ls -la gpurun_out/ncu
+cap() {  # name, ncu filter args...
+  local name=$1; shift
+  $F "$@" -o /tmp/ncu_$name $B > /dev/null 2>&1
+  ncu -i /tmp/ncu_$name.ncu-rep --page raw --csv > gpurun_out/ncu/$name.raw.csv 2>/dev/null
+  python tools/ncu_summary.py /tmp/ncu_$name.ncu-rep > gpurun_out/ncu/$name.summary.txt 2>&1
+}
+cap gemm_lv9_fold -k regex:k_gemm --launch-skip 26 -c 1
+cap gemm_lv2_grows -k regex:k_gemm --launch-skip 101 -c 1
+cap gemm_lv1_compact -k regex:k_gemm --launch-skip 103 -c 1
+cap inverse_blocked -k regex:k_inverse_blocked -c 1
+cap inverse_rg -k regex:k_inverse_rg -c 2
+cap inverse_la -k regex:k_inverse_la -c 1
+cap bigpanel -k regex:k_bigpanel -c 1
+cap sschur -k regex:k_sschur -c 1
+cap spsi -k regex:k_spsi -c 1
+cap mgather -k regex:k_mgather -c 1
+cp /tmp/ncu_gemm_lv9_fold.ncu-rep gpurun_out/ncu/
+du -sh gpurun_out/ncu; ls -la gpurun_out/ncu
