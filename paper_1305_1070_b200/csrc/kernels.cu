@@ -1447,6 +1447,70 @@ __device__ __forceinline__ double flip_sign(double v, int mask) {
   return __hiloint2double(__double2hiint(v) ^ mask, __double2loint(v));
 }
 
+// Epilogue of one warp's 16 x 16 output block at (r0, c0) of task tk: lane
+// owns C[r][c], C[r][c+1] of each 8x8 subtile (val(i, j, q)).  Fused diagonal
+// (GemmTask::dmode): row sums of Psi[r][c] op(C[r][c]), one partial per row
+// and 16-column group.  mir: the block lies strictly above the diagonal of a
+// symmetric task (also writes the transpose).
+template <class Val>
+__device__ __forceinline__ void gemm_epilogue(double2* base, const GemmTask& tk, int r0, int c0, bool mir,
+                                              const Val& val) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double2 rs[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + 8 * i + g;
+    if (r >= tk.m) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = c0 + 8 * j + 2 * t + q;
+        if (c >= tk.n) continue;
+        double2 v = val(i, j, q);
+        if (mir) {  // strictly-upper tile of a symmetric task: the (c, r) entry too
+          double2* d2 = base + tk.c_off + int64_t(c) * tk.ldc + r;
+          if (tk.mirror == 2) *d2 = make_double2(-v.x, v.y);  // anti-Hermitian: -conj
+          else if (tk.mode == MODE_ADD) *d2 = cadd(*d2, v);
+          else if (tk.mode == MODE_INIT) *d2 = cadd(base[tk.init_off + int64_t(c) * tk.ld_init + r], v);
+          else *d2 = v;
+        }
+        double2* dst = base + tk.c_off + int64_t(r) * tk.ldc + c;
+        if (tk.mode == MODE_ADD) v = cadd(*dst, v);
+        else if (tk.mode == MODE_INIT) v = cadd(base[tk.init_off + int64_t(r) * tk.ld_init + c], v);
+        if (!tk.nostore) *dst = v;
+        if (tk.c2_off >= 0) base[tk.c2_off + int64_t(r) * tk.ldc + c] = make_double2(2.0 * v.x, 2.0 * v.y);
+        if (tk.dmode) {
+          const double2 psi = base[tk.dpsi_off + int64_t(r) * tk.dpsi_ld + c];
+          if (tk.dmode >= 2) v.y = -v.y;
+          rs[i] = cadd(rs[i], cmul(psi, v));
+        }
+      }
+    }
+  }
+  if (tk.dmode) {  // task-uniform: reduce over the 4 lanes of a row, one partial per (row, 16-column group)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      rs[i].x += __shfl_xor_sync(0xffffffffu, rs[i].x, 1);
+      rs[i].y += __shfl_xor_sync(0xffffffffu, rs[i].y, 1);
+      rs[i].x += __shfl_xor_sync(0xffffffffu, rs[i].x, 2);
+      rs[i].y += __shfl_xor_sync(0xffffffffu, rs[i].y, 2);
+    }
+    if (t == 0 && c0 < tk.n) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = r0 + 8 * i + g;
+        if (r >= tk.m) continue;
+        // dmode 3: the anti-Hermitian form, imaginary part only (plan.cpp)
+        const double2 s = tk.dmode == 3 ? make_double2(0.0, -rs[i].y)
+                          : tk.dmode == 2 ? make_double2(-rs[i].x, -rs[i].y) : rs[i];
+        base[tk.dpart_off + int64_t(r) * tk.dpart_ld + c0 / 16] = s;
+      }
+    }
+  }
+}
+
 template <int WR, int WC>
 __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, const GemmTerm* __restrict__ terms,
                                           const GemmTile& tl, double2* smem) {
@@ -1635,66 +1699,14 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
   }
   cp_async_wait<0>();
 
-  // Epilogue: lane owns C[r][c], C[r][c+1] of each 8x8 subtile.  Fused
-  // diagonal (GemmTask::dmode): row sums of Psi[r][c] op(C[r][c]).
-  double2 rs[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
   const bool mir = tk.mirror && tl.n0 > tl.m0;  // aligned 32x32 tiles: every entry has c > r
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int r = tl.m0 + wm + 8 * i + g;
-    if (r >= tk.m) continue;
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int c = tl.n0 + wn + 8 * j + 2 * t + q;
-        if (c >= tk.n) continue;
+  gemm_epilogue(base, tk, tl.m0 + wm, tl.n0 + wn, mir, [&](int i, int j, int q) {
 #ifdef NEGF_GEMM_3M
-        double2 v = make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
+    return make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
 #else
-        double2 v = make_double2(p1[i][j][q], p2[i][j][q]);
+    return make_double2(p1[i][j][q], p2[i][j][q]);
 #endif
-        if (mir) {  // strictly-upper tile of a symmetric task: the (c, r) entry too
-          double2* d2 = base + tk.c_off + int64_t(c) * tk.ldc + r;
-          if (tk.mirror == 2) *d2 = make_double2(-v.x, v.y);  // anti-Hermitian: -conj
-          else if (tk.mode == MODE_ADD) *d2 = cadd(*d2, v);
-          else if (tk.mode == MODE_INIT) *d2 = cadd(base[tk.init_off + int64_t(c) * tk.ld_init + r], v);
-          else *d2 = v;
-        }
-        double2* dst = base + tk.c_off + int64_t(r) * tk.ldc + c;
-        if (tk.mode == MODE_ADD) v = cadd(*dst, v);
-        else if (tk.mode == MODE_INIT) v = cadd(base[tk.init_off + int64_t(r) * tk.ld_init + c], v);
-        if (!tk.nostore) *dst = v;
-        if (tk.c2_off >= 0) base[tk.c2_off + int64_t(r) * tk.ldc + c] = make_double2(2.0 * v.x, 2.0 * v.y);
-        if (tk.dmode) {
-          const double2 psi = base[tk.dpsi_off + int64_t(r) * tk.dpsi_ld + c];
-          if (tk.dmode >= 2) v.y = -v.y;
-          rs[i] = cadd(rs[i], cmul(psi, v));
-        }
-      }
-    }
-  }
-  if (tk.dmode) {  // task-uniform: reduce over the 4 lanes of a row, one partial per (row, 16-column group)
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      rs[i].x += __shfl_xor_sync(0xffffffffu, rs[i].x, 1);
-      rs[i].y += __shfl_xor_sync(0xffffffffu, rs[i].y, 1);
-      rs[i].x += __shfl_xor_sync(0xffffffffu, rs[i].x, 2);
-      rs[i].y += __shfl_xor_sync(0xffffffffu, rs[i].y, 2);
-    }
-    const int c0 = tl.n0 + wn;
-    if (t == 0 && c0 < tk.n) {
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int r = tl.m0 + wm + 8 * i + g;
-        if (r >= tk.m) continue;
-        // dmode 3: the anti-Hermitian form, imaginary part only (plan.cpp)
-        const double2 s = tk.dmode == 3 ? make_double2(0.0, -rs[i].y)
-                          : tk.dmode == 2 ? make_double2(-rs[i].x, -rs[i].y) : rs[i];
-        base[tk.dpart_off + int64_t(r) * tk.dpart_ld + c0 / 16] = s;
-      }
-    }
-  }
+  });
 }
 
 // ---------------------------------------------------------------------------
@@ -2317,6 +2329,157 @@ __global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride,
     __syncthreads();
   }
 }
+// Warp tiles (GemmTile::arr == 3, small tasks): one warp per 16 x 16 output
+// block, fragments loaded straight from global memory (L2 / HBM) into
+// registers -- no shared-memory staging, no CTA barrier -- so many
+// independent warps keep their loads in flight.  The DMMA sequence per
+// accumulator (terms in order, 4-deep k-steps, zero-padded) is that of
+// gemm_item, so the results are bit-identical to the CTA tiles.
+__global__ void __launch_bounds__(256, 2) k_gemm_warp(double2* arena, int64_t stride, int nE,
+                                                      const GemmTask* __restrict__ tasks,
+                                                      const GemmTerm* __restrict__ terms,
+                                                      const GemmTile* __restrict__ tiles, int tile_begin,
+                                                      int64_t items) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wpb = blockDim.x >> 5;
+  const int64_t nw = int64_t(gridDim.x) * wpb;
+  for (int64_t w = int64_t(blockIdx.x) * wpb + (threadIdx.x >> 5); w < items; w += nw) {
+    const int64_t ti = w / nE;
+    const int e = static_cast<int>(w - ti * nE);
+    const GemmTile tl = tiles[tile_begin + ti];
+    const GemmTask tk = tasks[tl.task];
+    double2* base = arena + int64_t(e) * stride;
+    const int live_i = min(2, max(0, (tk.m - tl.m0 + 7) / 8));
+    const int live_j = min(2, max(0, (tk.n - tl.n0 + 7) / 8));
+#ifdef NEGF_GEMM_3M
+    double p1[2][2][2], p2[2][2][2], p3[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = p3[i][j][q] = 0.0;
+#else
+    double p1[2][2][2], p2[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = 0.0;
+#endif
+    const int ra0 = tl.m0 + g, ra1 = tl.m0 + 8 + g;  // A rows of this lane
+    const int cb0 = tl.n0 + g, cb1 = tl.n0 + 8 + g;  // B columns of this lane
+    for (int q = tk.term_begin; q < tk.term_begin + tk.term_count; ++q) {
+      const GemmTerm tm = terms[q];
+      if (tm.k <= 0) continue;
+      const int negA = tm.sign < 0 ? int(0x80000000) : 0;
+      const int conjB = (tm.b_op == OP_C || tm.b_op == OP_H) ? int(0x80000000) : 0;
+      const bool a_rk = (tm.a_op == OP_N);
+      const bool b_kr = (tm.b_op == OP_N || tm.b_op == OP_C);
+      const double2* A = base + tm.a_off;
+      const double2* Bm = base + tm.b_off;
+      // element (row, k) of op(A) and (k, col) of op(B) at this lane
+      const int64_t as_r = a_rk ? tm.lda : 1, as_k = a_rk ? 1 : tm.lda;
+      const int64_t bs_k = b_kr ? tm.ldb : 1, bs_c = b_kr ? 1 : tm.ldb;
+      const bool va0 = ra0 < tk.m, va1 = ra1 < tk.m, vb0 = cb0 < tk.n, vb1 = cb1 < tk.n;
+#pragma unroll 2
+      for (int k0 = 0; k0 < tm.k; k0 += 4) {
+        const int kk = k0 + t;
+        const bool vk = kk < tm.k;
+        double2 a[2], b[2];
+        const double2 z = make_double2(0.0, 0.0);
+        a[0] = (va0 && vk) ? A[ra0 * as_r + kk * as_k] : z;
+        a[1] = (va1 && vk) ? A[ra1 * as_r + kk * as_k] : z;
+        b[0] = (vb0 && vk) ? Bm[kk * bs_k + cb0 * bs_c] : z;
+        b[1] = (vb1 && vk) ? Bm[kk * bs_k + cb1 * bs_c] : z;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          a[i].x = flip_sign(a[i].x, negA);
+          a[i].y = flip_sign(a[i].y, negA);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) b[j].y = flip_sign(b[j].y, conjB);
+#ifdef NEGF_GEMM_3M
+        double as[2], bs[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (i >= live_i) break;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (j >= live_j) break;
+            dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+            dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].y);
+            dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
+          }
+        }
+#else
+        double nai[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) nai[i] = flip_sign(a[i].y, int(0x80000000));
+        if (live_i == 2 && live_j == 2) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+              dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+            }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
+              dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
+            }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            if (i >= live_i) break;
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              if (j >= live_j) break;
+              dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+              dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
+              dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+              dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
+            }
+          }
+        }
+#endif
+      }
+    }
+    gemm_epilogue(base, tk, tl.m0, tl.n0, false, [&](int i, int j, int q) {
+#ifdef NEGF_GEMM_3M
+      return make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
+#else
+      return make_double2(p1[i][j][q], p2[i][j][q]);
+#endif
+    });
+  }
+}
+
+static void launch_gemm_warp(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
+                             const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
+  static int slots_of[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& slots = slots_of[dev & 63];
+  if (!slots) {
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_warp, 256, 0);
+    slots = std::max(1, sms * std::max(1, per_sm));
+  }
+  const int64_t items = int64_t(tile_count) * b.nE;
+  const int grid = static_cast<int>(std::min<int64_t>((items + 7) / 8, slots));
+  k_gemm_warp<<<grid, 256, 0, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
+}
+
 template <int WR, int WC>
 static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                             const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
@@ -2348,6 +2511,7 @@ void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_
     while (j < end && h_tiles[j].arr == arr) ++j;
     if (arr == 1) launch_gemm_arr<1, 4>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
     else if (arr == 2) launch_gemm_arr<4, 1>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
+    else if (arr == 3) launch_gemm_warp(b, d_tasks, d_terms, d_tiles, i, j - i, s);
     else launch_gemm_arr<2, 2>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
     ++launches;
     i = j;

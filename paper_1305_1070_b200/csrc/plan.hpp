@@ -92,7 +92,7 @@ struct GemmTerm {
 struct GemmTile {
   int task;
   int m0, n0;
-  int arr;  // warp arrangement of the CTA: 0 = 2x2 (32x32), 1 = 1x4 (16x64), 2 = 4x1 (64x16)
+  int arr;  // warp arrangement of the CTA: 0 = 2x2 (32x32), 1 = 1x4 (16x64), 2 = 4x1 (64x16), 3 = one warp (16x16)
 };
 
 // Diagonal-only output: out[a] = [init[a*init_stride]] + sum_t sign_t
@@ -385,8 +385,9 @@ constexpr int kSmemInvMax = 112;  // largest block inverted by one CTA (register
 // inverse tasks by this class, largest first.
 inline int inv_size_class(int m) { return m <= 16 ? 0 : m <= 32 ? 1 : m <= 48 ? 2 : m <= 64 ? 3 : 4; }
 // CTA tile extents per warp arrangement (see GemmTile::arr).
-constexpr int kArrTM[3] = {32, 16, 64};
-constexpr int kArrTN[3] = {32, 64, 16};
+// arr 3: warp tiles (16 x 16 per warp, fragments from global memory) for small tasks
+constexpr int kArrTM[4] = {32, 16, 64, 16};
+constexpr int kArrTN[4] = {32, 64, 16, 16};
 
 // Cover an m x n output block with CTA tiles (appended to `out`).  The
 // candidates are the three uniform grids and a 32x32 core with its bottom /
@@ -394,7 +395,7 @@ constexpr int kArrTN[3] = {32, 64, 16};
 // cheapest under the measured tile cost model (a fixed part per tile-chunk
 // plus a part proportional to the live 8x8 DMMA subtiles; tools/gemm_bench)
 // wins.
-void tile_task(int task, int m, int n, std::vector<GemmTile>& out);
+void tile_task(int task, int m, int n, int ksum, std::vector<GemmTile>& out);
 // Upper-triangular 32x32 tiles of a symmetric m x m task (GemmTask::mirror);
 // returns the number of output entries the tiles compute.
 int64_t tile_task_sym(int task, int m, std::vector<GemmTile>& out);

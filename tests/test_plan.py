@@ -125,8 +125,8 @@ def test_gpu_handle_fails_loudly_without_device():
 def _check_tiles_cover_exactly(plan):
     tk = plan.gemm_tasks()
     tl = plan.gemm_tiles()
-    tm = np.array([32, 16, 64])
-    tn = np.array([32, 64, 16])
+    tm = np.array([32, 16, 64, 16])  # arr 3: warp tiles (one warp per 16 x 16 block)
+    tn = np.array([32, 64, 16, 16])
     cover = [np.zeros((int(m), int(n)), np.int32) for m, n in zip(tk["m"], tk["n"])]
     for t, m0, n0, a, mir in zip(tl["task"], tl["m0"], tl["n0"], tl["arr"], tl["mirrored"]):
         c = cover[t]
@@ -140,7 +140,7 @@ def _check_tiles_cover_exactly(plan):
 
 @pytest.mark.parametrize("name", golden_names())
 def test_gemm_tiles_cover_every_task_exactly_once(name):
-    """Mixed 32x32 / 16x64 / 64x16 tiling: every output entry of every grouped
+    """Mixed 32x32 / 16x64 / 64x16 / warp 16x16 tiling: every output entry of every grouped
     GEMM task is computed by exactly one CTA tile (accumulating tasks would
     double-add otherwise)."""
     _, prob, _, _ = load_golden(name)

@@ -50,7 +50,7 @@ int main(int argc, char** argv) {
     tk.term_count = static_cast<int>(terms.size()) - tb;
     tasks.push_back(tk);
     if (ARR == 3) {
-      tile_task(t, M, N, tiles[0]);  // the plan's mixed tiling
+      tile_task(t, M, N, 1 << 30, tiles[0]);  // the plan's mixed tiling (never warp tiles)
     } else {
       for (int m0 = 0; m0 < M; m0 += kArrTM[ARR])
         for (int n0 = 0; n0 < N; n0 += kArrTN[ARR]) tiles[0].push_back(GemmTile{t, m0, n0, ARR});

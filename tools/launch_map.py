@@ -23,7 +23,7 @@ def op_list(path):
     w = devices.config2(n_energies=2)
     plan = negf.HscPlan(w.problem)
     ops, tl, tk = plan.ops(), plan.gemm_tiles(), plan.gemm_tasks()
-    tms, tns = np.array([32, 16, 64]), np.array([32, 64, 16])
+    tms, tns = np.array([32, 16, 64, 16]), np.array([32, 64, 16, 16])
     rows = []
     for i in range(len(ops["kind"])):
         k, b, c = int(ops["kind"][i]), int(ops["begin"][i]), int(ops["count"][i])

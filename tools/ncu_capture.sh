@@ -9,15 +9,20 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python tools/launch_map.py ops gpurun_out/ncu/ops.json
 python tools/launch_map.py map gpurun_out/ncu/launches.csv gpurun_out/ncu/ops.json > gpurun_out/ncu/launch_map.txt 2>&1
 F="ncu --set full --clock-control none --import-source on"
+# k_gemm launch index of (phase, level, arrangement) in plan order
+gidx() { python -c "
+import json; g=[o for o in json.load(open('gpurun_out/ncu/ops.json')) if o['kind']==1]
+print([i for i,o in enumerate(g) if (o['phase'],o['level'],o['arr'])==($1,$2,$3)][0])"; }
 cap() {  # name, ncu filter args...
   local name=$1; shift
   $F "$@" -o /tmp/ncu_$name $B > /dev/null 2>&1
   ncu -i /tmp/ncu_$name.ncu-rep --page raw --csv > gpurun_out/ncu/$name.raw.csv 2>/dev/null
   python tools/ncu_summary.py /tmp/ncu_$name.ncu-rep > gpurun_out/ncu/$name.summary.txt 2>&1
 }
-cap gemm_lv9_fold -k regex:k_gemm --launch-skip 26 -c 1
-cap gemm_lv2_grows -k regex:k_gemm --launch-skip 101 -c 1
-cap gemm_lv1_compact -k regex:k_gemm --launch-skip 103 -c 1
+cap gemm_lv9_fold -k regex:k_gemm --launch-skip $(gidx 0 9 0) -c 1
+cap gemm_lv2_grows_warp -k regex:k_gemm --launch-skip $(gidx 1 2 3) -c 1
+cap gemm_lv5_grows -k regex:k_gemm --launch-skip $(gidx 1 5 0) -c 1
+cap gemm_lv1_compact -k regex:k_gemm --launch-skip $(gidx 1 1 0) -c 1
 cap inverse_blocked -k regex:k_inverse_blocked -c 1
 cap inverse_rg -k regex:k_inverse_rg -c 2
 cap inverse_la -k regex:k_inverse_la -c 1
