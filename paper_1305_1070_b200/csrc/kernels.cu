@@ -2335,7 +2335,14 @@ __global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride,
 // independent warps keep their loads in flight.  The DMMA sequence per
 // accumulator (terms in order, 4-deep k-steps, zero-padded) is that of
 // gemm_item, so the results are bit-identical to the CTA tiles.
-__global__ void __launch_bounds__(256, 2) k_gemm_warp(double2* arena, int64_t stride, int nE,
+#ifndef NEGF_WARP_MINB
+#define NEGF_WARP_MINB 3
+#endif
+#ifndef NEGF_WARP_UNROLL
+#define NEGF_WARP_UNROLL 1
+#endif
+constexpr int kWarpUnroll = NEGF_WARP_UNROLL;
+__global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* arena, int64_t stride, int nE,
                                                       const GemmTask* __restrict__ tasks,
                                                       const GemmTerm* __restrict__ terms,
                                                       const GemmTile* __restrict__ tiles, int tile_begin,
@@ -2383,7 +2390,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_warp(double2* arena, int64_t st
       const int64_t as_r = a_rk ? tm.lda : 1, as_k = a_rk ? 1 : tm.lda;
       const int64_t bs_k = b_kr ? tm.ldb : 1, bs_c = b_kr ? 1 : tm.ldb;
       const bool va0 = ra0 < tk.m, va1 = ra1 < tk.m, vb0 = cb0 < tk.n, vb1 = cb1 < tk.n;
-#pragma unroll 2
+#pragma unroll kWarpUnroll
       for (int k0 = 0; k0 < tm.k; k0 += 4) {
         const int kk = k0 + t;
         const bool vk = kk < tm.k;

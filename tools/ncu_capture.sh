@@ -8,13 +8,14 @@ B="python tools/launch_map.py batch 1"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu/launches.csv $B > gpurun_out/ncu/launches.log 2>&1
 python tools/launch_map.py ops gpurun_out/ncu/ops.json
 python tools/launch_map.py map gpurun_out/ncu/launches.csv gpurun_out/ncu/ops.json > gpurun_out/ncu/launch_map.txt 2>&1
-F="ncu --set full --clock-control none --import-source on"
+F="ncu -f --set full --clock-control none --import-source on"
 # k_gemm launch index of (phase, level, arrangement) in plan order
 gidx() { python -c "
 import json; g=[o for o in json.load(open('gpurun_out/ncu/ops.json')) if o['kind']==1]
 print([i for i,o in enumerate(g) if (o['phase'],o['level'],o['arr'])==($1,$2,$3)][0])"; }
 cap() {  # name, ncu filter args...
   local name=$1; shift
+  rm -f /tmp/ncu_$name.ncu-rep
   $F "$@" -o /tmp/ncu_$name $B > /dev/null 2>&1
   ncu -i /tmp/ncu_$name.ncu-rep --page raw --csv > gpurun_out/ncu/$name.raw.csv 2>/dev/null
   python tools/ncu_summary.py /tmp/ncu_$name.ncu-rep > gpurun_out/ncu/$name.summary.txt 2>&1
