@@ -1032,6 +1032,36 @@ Plan build_plan(ProblemDesc desc) {
     leaf_wood[static_cast<std::size_t>(c)] = f_woodbury && leaf_sparse[static_cast<std::size_t>(c)] && !I.full_g && !I.full_p &&
                                              !I.seeded && !I.has_nd && I.ncols.empty() && I.m > 0 && I.m < 65536;
   }
+  // A sparse leaf's coupling block A_{x,S} is read only through its stencil
+  // entries (the plan's CSC: K_SPSI, K_SSCHUR, K_LEAFDIAG, the hulls above),
+  // never from the arena: its Arow region is neither zeroed nor scattered
+  // per energy.
+  {
+    std::vector<std::pair<int64_t, int64_t>> skip;  // [begin, end) arena ranges
+    for (int c = 0; c < nc; ++c) {
+      const ClusterInfo& I = B.I(c);
+      if (leaf_sparse[static_cast<std::size_t>(c)] && I.K > 0 && I.m > 0)
+        skip.push_back({I.off_arow, I.off_arow + int64_t(I.m) * I.K});
+    }
+    std::sort(skip.begin(), skip.end());
+    auto skipped = [&](int64_t pos) {
+      auto it = std::upper_bound(skip.begin(), skip.end(), std::make_pair(pos, std::numeric_limits<int64_t>::max()));
+      return it != skip.begin() && pos < std::prev(it)->second;
+    };
+    std::vector<InitRegion> iz;
+    for (const InitRegion& r : P.init_zero)
+      if (!skipped(r.off)) iz.push_back(r);
+    P.init_zero.swap(iz);
+    std::vector<int64_t> hp;
+    std::vector<cplx> hv;
+    for (std::size_t q = 0; q < P.h_pos.size(); ++q)
+      if (!skipped(P.h_pos[q])) {
+        hp.push_back(P.h_pos[q]);
+        hv.push_back(P.h_val[q]);
+      }
+    P.h_pos.swap(hp);
+    P.h_val.swap(hv);
+  }
   // Leaf -> SpsiTask index (leaves' Psi tasks are emitted at level 1, before
   // any gather that reads them).
   std::vector<int> spsi_of(static_cast<std::size_t>(nc), -1);
