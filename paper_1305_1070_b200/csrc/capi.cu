@@ -122,6 +122,7 @@ struct negf_gpu {
   double* d_density = nullptr;
   double* d_skew = nullptr;
   DevStatus* d_status = nullptr;
+  unsigned long long* d_gemm_ctr = nullptr;  // persistent-GEMM work counters (BatchArgs::gemm_ctr)
   void* comm = nullptr;
   int nranks = 1;
   double* d_gather = nullptr;  // nranks x n partial densities (ordered reduction)
@@ -228,7 +229,7 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
                const double2* d_sr, const double2* d_sl, double2* d_gr, double2* d_gl,
                const BatchHooks* hk = nullptr) {
   const Plan& P = *g->plan;
-  BatchArgs b{g->arena, P.arena, nE, e_base};
+  BatchArgs b{g->arena, P.arena, nE, e_base, g->d_gemm_ctr};
   cudaStream_t s = g->stream;
   int64_t& L = g->launches;
   {
@@ -633,6 +634,8 @@ int negf_gpu_create(const negf_plan* hp, int device, int max_energy_batch, negf_
     g->d_density = dev_alloc<double>(n, o);
     g->d_skew = dev_alloc<double>(2 * std::max<size_t>(1, P.seeded_ids.size()) * cap, o);
     g->d_status = dev_alloc<DevStatus>(1, o);
+    g->d_gemm_ctr = dev_alloc<unsigned long long>(2, o);
+    ck(cudaMemsetAsync(g->d_gemm_ctr, 0, 2 * sizeof(unsigned long long), g->stream), "memset");
     ck(cudaMemsetAsync(g->d_density, 0, sizeof(double) * n, g->stream), "memset");
     reset_status(g.get());
     ck(cudaStreamSynchronize(g->stream), "sync");

@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 
 namespace negfb {
 
@@ -1440,7 +1441,19 @@ struct OperandLoader {
   }
 };
 
-constexpr int kTermCache = 48;  // term descriptors staged in shared memory per item
+constexpr int kTermCache = 48;
+// Energy groups of the item order (measured on config 2, dynamic scheduling):
+// the CTA tiles run best with all energies in one group (energy fastest: the
+// copies of a tile run side by side, LPT over tiles; 70.7 vs 72.8 ms per batch
+// for groups of 4), the warp tiles of the small separators with one energy per
+// group (24.8 vs 25.4 ms).
+#ifndef NEGF_GEMM_EG_CTA
+#define NEGF_GEMM_EG_CTA (1 << 30)
+#endif
+#ifndef NEGF_GEMM_EG_WARP
+#define NEGF_GEMM_EG_WARP 1
+#endif
+constexpr int kGemmEgCta = NEGF_GEMM_EG_CTA, kGemmEgWarp = NEGF_GEMM_EG_WARP;  // term descriptors staged in shared memory per item
 
 // Sign flip on the integer pipe (keeps the FP64 pipes free).
 __device__ __forceinline__ double flip_sign(double v, int mask) {
@@ -2298,19 +2311,54 @@ void launch_leafdiag(const BatchArgs& b, const LeafDiagTask* d_tasks, const Leaf
   ++launches;
 }
 
-// Persistent launch: CTAs stride over (tile, energy) items, energy fastest;
-// one launch per warp arrangement of an op (a task may mix arrangements,
-// plan.cpp tile_task); tiles pre-sorted by decreasing cost in the plan.
+// Item w of a launch -> (tile, energy).  Energies go in groups of `eg`:
+// all tiles of a group's energies are issued before the next group, energy
+// fastest inside the group.  Small groups keep the operand panels that
+// neighbouring tiles of one energy share in L2 (config 2, all k_gemm launches
+// of a batch: 331 GB of DRAM traffic with eg = nE and a static stride, 195 GB
+// with groups of 4 and the atomic counter below, against 298 GB algorithmic);
+// eg = nE runs the 256 copies of a tile side by side.  Defaults: measured.
+__device__ __forceinline__ void gemm_item_index(int64_t w, int nE, int64_t ntiles, int eg, int64_t& ti, int& e) {
+  const int64_t per = ntiles * eg;
+  const int64_t grp = w / per;
+  const int64_t r = w - grp * per;
+  const int e0 = static_cast<int>(grp) * eg;
+  const int egc = min(eg, nE - e0);
+  ti = r / egc;
+  e = e0 + static_cast<int>(r - ti * egc);
+}
+
+// Persistent launch over (tile, energy) items in the grouped order above; one
+// launch per warp arrangement of an op (a task may mix arrangements, plan.cpp
+// tile_task); tiles pre-sorted by decreasing cost in the plan.  Items are
+// handed out by an atomic counter (ctr[0]; ctr == nullptr: static stride):
+// with a static stride each CTA's sequence is fixed, CTAs drift apart by whole
+// tile times after the first wave, and tiles that share an operand panel
+// (neighbours in the item order) no longer run together -- the panel has left
+// L2 before its second reader arrives.  The last CTA to finish resets the
+// counters for the next launch on the stream.
+__device__ __forceinline__ void gemm_ctr_done(unsigned long long* ctr, unsigned long long workers) {
+  if (atomicAdd(ctr + 1, 1ull) == workers - 1) {
+    ctr[0] = 0;
+    ctr[1] = 0;
+  }
+}
+
 template <int WR, int WC>
 __global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride, int nE,
                                                      const GemmTask* __restrict__ tasks,
                                                      const GemmTerm* __restrict__ terms,
                                                      const GemmTile* __restrict__ tiles, int tile_begin,
-                                                     int64_t items) {
+                                                     int64_t items, int eg, unsigned long long* ctr) {
   extern __shared__ double2 gsm[];
-  for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
-    const int64_t ti = w / nE;
-    const int e = static_cast<int>(w - ti * nE);
+  __shared__ int64_t s_next[2];  // double-buffered: slot it & 1 is written in iteration it
+  const int64_t ntiles = items / nE;
+  int64_t w = blockIdx.x;
+  for (int it = 0; w < items; ++it) {
+    if (ctr && threadIdx.x == 0) s_next[it & 1] = int64_t(gridDim.x) + int64_t(atomicAdd(ctr, 1ull));
+    int64_t ti;
+    int e;
+    gemm_item_index(w, nE, ntiles, eg, ti, e);
     const GemmTile tl = tiles[tile_begin + ti];
     const GemmTask tk = tasks[tl.task];
     // Stage the task's term descriptors in shared memory (read every chunk).
@@ -2327,7 +2375,9 @@ __global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride,
     }
     gemm_item<WR, WC>(arena + e * stride, tk, tp, tl, gsm);
     __syncthreads();
+    w = ctr ? s_next[it & 1] : w + gridDim.x;
   }
+  if (ctr && threadIdx.x == 0) gemm_ctr_done(ctr, gridDim.x);
 }
 // Warp tiles (GemmTile::arr == 3, small tasks): one warp per 16 x 16 output
 // block, fragments loaded straight from global memory (L2 / HBM) into
@@ -2346,13 +2396,23 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
                                                       const GemmTask* __restrict__ tasks,
                                                       const GemmTerm* __restrict__ terms,
                                                       const GemmTile* __restrict__ tiles, int tile_begin,
-                                                      int64_t items) {
+                                                      int64_t items, int eg, unsigned long long* ctr) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wpb = blockDim.x >> 5;
   const int64_t nw = int64_t(gridDim.x) * wpb;
-  for (int64_t w = int64_t(blockIdx.x) * wpb + (threadIdx.x >> 5); w < items; w += nw) {
-    const int64_t ti = w / nE;
-    const int e = static_cast<int>(w - ti * nE);
+  const int64_t ntiles = items / nE;
+  // items per warp: static stride or the launch's atomic counter (k_gemm)
+  for (int64_t w = int64_t(blockIdx.x) * wpb + (threadIdx.x >> 5), wn = 0; w < items; w = wn) {
+    if (ctr) {
+      unsigned long long x = 0;
+      if (lane == 0) x = atomicAdd(ctr, 1ull);
+      wn = nw + int64_t(__shfl_sync(0xffffffffu, x, 0));
+    } else {
+      wn = w + nw;
+    }
+    int64_t ti;
+    int e;
+    gemm_item_index(w, nE, ntiles, eg, ti, e);
     const GemmTile tl = tiles[tile_begin + ti];
     const GemmTask tk = tasks[tl.task];
     double2* base = arena + int64_t(e) * stride;
@@ -2468,6 +2528,25 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
 #endif
     });
   }
+  if (ctr && lane == 0) gemm_ctr_done(ctr, static_cast<unsigned long long>(nw));
+}
+
+// Energies per item group (gemm_item_index); NEGF_GEMM_EG overrides (A/B).
+static int gemm_energy_group(int nE, bool warp) {
+  static const int env = [] {
+    const char* e = std::getenv("NEGF_GEMM_EG");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int eg = env > 0 ? env : (warp ? kGemmEgWarp : kGemmEgCta);
+  return std::max(1, std::min(eg, nE));
+}
+// Dynamic item scheduling (atomic counter) unless NEGF_GEMM_DYN=0 (A/B).
+static unsigned long long* gemm_counter(const BatchArgs& b) {
+  static const bool dyn = [] {
+    const char* e = std::getenv("NEGF_GEMM_DYN");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return dyn ? b.gemm_ctr : nullptr;
 }
 
 static void launch_gemm_warp(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
@@ -2484,7 +2563,8 @@ static void launch_gemm_warp(const BatchArgs& b, const GemmTask* d_tasks, const 
   }
   const int64_t items = int64_t(tile_count) * b.nE;
   const int grid = static_cast<int>(std::min<int64_t>((items + 7) / 8, slots));
-  k_gemm_warp<<<grid, 256, 0, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
+  k_gemm_warp<<<grid, 256, 0, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items,
+                                   gemm_energy_group(b.nE, true), gemm_counter(b));
 }
 
 template <int WR, int WC>
@@ -2504,7 +2584,8 @@ static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const G
   }
   const int64_t items = int64_t(tile_count) * b.nE;
   const int grid = static_cast<int>(std::min<int64_t>(items, slots));
-  k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items);
+  k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items,
+                                         gemm_energy_group(b.nE, false), gemm_counter(b));
 }
 void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                  const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,

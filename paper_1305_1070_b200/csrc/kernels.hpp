@@ -21,6 +21,10 @@ struct BatchArgs {
   int64_t stride;     // complex elements per energy arena
   int nE;
   int e_base;         // global index of energy 0 of this batch
+  // Work counters of the persistent GEMM launches: {next item, finished CTAs},
+  // zero between launches (the last CTA of a launch resets them; launches on
+  // the solver stream are ordered).
+  unsigned long long* gemm_ctr;
 };
 
 void launch_assemble(const BatchArgs& b, const Plan& p, const int64_t* d_h_pos, const double2* d_h_val,

@@ -305,6 +305,7 @@ struct negf_lead {
   int* d_conv = nullptr;
   int* d_counters = nullptr;  // [pending, lowest_open]
   DevStatus* d_status = nullptr;
+  unsigned long long* d_gemm_ctr = nullptr;  // BatchArgs::gemm_ctr
   double* d_energies = nullptr;
   double2* d_out = nullptr;
   int64_t launches = 0;
@@ -349,7 +350,7 @@ int lead_batch(negf_lead* l, int nE, int e_base, const double* d_E, double2* d_o
   cudaStream_t s = l->stream;
   LeadOffs off;
   for (int k = 0; k < LB_COUNT; ++k) off.o[k] = L.off[k];
-  BatchArgs b{l->arena, L.P.arena, nE, e_base};
+  BatchArgs b{l->arena, L.P.arena, nE, e_base, l->d_gemm_ctr};
   const DevStatus clean{~0ull, ~0ull, ~0ull, 0ull};
   ck(cudaMemcpyAsync(l->d_status, &clean, sizeof clean, cudaMemcpyHostToDevice, s), "status reset");
   ck(cudaMemsetAsync(l->d_conv, 0xFF, sizeof(int) * nE, s), "conv reset");
@@ -505,6 +506,8 @@ int negf_lead_create(int device, int w, const double* h00, const double* h01, do
     l->d_conv = dev_alloc<int>(static_cast<size_t>(cap), l->owned);
     l->d_counters = dev_alloc<int>(2, l->owned);
     l->d_status = dev_alloc<DevStatus>(1, l->owned);
+    l->d_gemm_ctr = dev_alloc<unsigned long long>(2, l->owned);
+    ck(cudaMemset(l->d_gemm_ctr, 0, 2 * sizeof(unsigned long long)), "memset");
     l->d_energies = dev_alloc<double>(static_cast<size_t>(cap), l->owned);
     l->d_out = dev_alloc<double2>(static_cast<size_t>(cap) * w * w, l->owned);
   } catch (const CudaFail& f) {

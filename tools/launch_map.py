@@ -3,6 +3,10 @@
     python tools/launch_map.py ops  out.json          # plan op list (GEMM rows per warp arrangement)
     python tools/launch_map.py batch [repeats]        # one 256-point batch (run under ncu)
     python tools/launch_map.py map launches.csv ops.json   # per (phase, level) GEMM time and TF/s
+    python tools/launch_map.py traffic dram.csv ops.json   # k_gemm DRAM bytes vs algorithmic bytes
+
+traffic: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:k_gemm
+         --clock-control none --csv --log-file dram.csv python tools/launch_map.py batch
 
 ncu: ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file L.csv \\
          python tools/launch_map.py batch
@@ -37,7 +41,11 @@ def op_list(path):
             t = tl["task"][sel]
             lm = np.minimum(tms[a], tk["m"][t] - tl["m0"][sel])
             ln = np.minimum(tns[a], tk["n"][t] - tl["n0"][sel])
-            rows.append(dict(base, arr=int(a), tiles=int(len(sel)), flops=float((8.0 * lm * ln * tk["k"][t]).sum())))
+            ut = np.unique(t)  # algorithmic bytes: every operand read once, C read + written once
+            ab = float((16.0 * (tk["m"][ut] * tk["k"][ut] + tk["k"][ut] * tk["n"][ut]
+                                + 2.0 * tk["m"][ut] * tk["n"][ut])).sum())
+            rows.append(dict(base, arr=int(a), tiles=int(len(sel)), flops=float((8.0 * lm * ln * tk["k"][t]).sum()),
+                             alg_bytes=ab))
     json.dump(rows, open(path, "w"))
 
 
@@ -84,11 +92,42 @@ def map_launches(csv_path, ops_path):
         print(f"  {k[-44:]:44s} {n:4d} {t:9.2f} ms {100 * t / tot:5.1f} %")
 
 
+def traffic(csv_path, ops_path):
+    """Per k_gemm launch: DRAM bytes (ncu) against the algorithmic bytes of its
+    tasks (operands and C once per energy; a task split over two arrangement
+    launches counts in both)."""
+    lines = [ln for ln in open(csv_path) if ln.startswith('"')]
+    rows = list(csv.reader(lines))
+    h, rows = rows[0], rows[1:]
+    i_id, i_m, i_v = h.index("ID"), h.index("Metric Name"), h.index("Metric Value")
+    per = collections.defaultdict(dict)
+    for r in rows:
+        per[int(r[i_id])][r[i_m]] = float(r[i_v].replace(",", ""))
+    ls = [per[k] for k in sorted(per)]
+    g = [o for o in json.load(open(ops_path)) if o["kind"] == 1]
+    assert len(ls) == len(g), (len(ls), len(g))
+    tot_d = tot_a = tot_t = 0.0
+    out = []
+    for m, o in zip(ls, g):
+        d = m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]
+        t = m["gpu__time_duration.sum"] * 1e-9
+        a = o["alg_bytes"] * NE
+        tot_d, tot_a, tot_t = tot_d + d, tot_a + a, tot_t + t
+        out.append((t, d, a, o))
+    print(f"# k_gemm: {len(out)} launches {tot_t * 1e3:.2f} ms, DRAM {tot_d / 1e9:.2f} GB, algorithmic "
+          f"{tot_a / 1e9:.2f} GB ({tot_d / tot_a:.2f}x)")
+    print("# top launches: ms, DRAM GB, algorithmic GB, ratio, phase, level, arr")
+    for t, d, a, o in sorted(out, key=lambda x: -x[0])[:12]:
+        print(f"  {t * 1e3:7.3f} {d / 1e9:7.2f} {a / 1e9:7.2f} {d / a:6.2f}  ph {o['phase']} lv {o['level']} arr {o['arr']}")
+
+
 if __name__ == "__main__":
     cmd = sys.argv[1]
     if cmd == "ops":
         op_list(sys.argv[2])
     elif cmd == "batch":
         batch(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+    elif cmd == "traffic":
+        traffic(sys.argv[2], sys.argv[3])
     else:
         map_launches(sys.argv[2], sys.argv[3])
