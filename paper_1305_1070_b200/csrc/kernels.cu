@@ -1128,6 +1128,190 @@ __global__ void __launch_bounds__(ROWS * H, (ROWS * H <= 64) ? 8 : (ROWS * H <= 
 }
 
 // ---------------------------------------------------------------------------
+// Shifting-window register Gauss-Jordan (m <= ROWS, m <= H * S).  Same
+// elimination as k_inverse_rg (row partial pivoting by position tracking, the
+// same pivot sequence and singular rule), but the m live columns of [A | I]
+// are kept as a window that moves one column to the right per pivot step:
+// the pivot column is always window column 0 and the new inverse column
+// enters at the right end.  Every step is then the same code on the same
+// registers (w[j-1] = w[j] - fs * prow[j-1]), so the pivot loop is NOT
+// unrolled: a few hundred instructions instead of the ~100 KB of straight-line
+// code k_inverse_rg needs for static register indices (its top stall is
+// instruction fetch).  Thread t owns row r = t / H and the window columns
+// h S .. h S + S - 1 (h = t % H); one shuffle per step brings the next
+// chunk's first column.  Rows are scaled late: a pivoted row stays
+// unnormalised (the update is linear in the row, the multiplier of a step is
+// fs = f / pivot as in an LU factorisation) and is multiplied by its own
+// 1 / pivot when the block is written back.
+// ---------------------------------------------------------------------------
+template <int NW>
+__device__ __forceinline__ void sw_barrier() {
+  if constexpr (NW == 1) __syncwarp();
+  else __syncthreads();
+}
+
+template <int ROWS, int H, int S, int MINB>
+__global__ void __launch_bounds__(ROWS * H, MINB)
+    k_inverse_sw(double2* arena, int64_t stride, const InvTask* __restrict__ tasks, int e_base, DevStatus* st) {
+  constexpr int NT = ROWS * H, NW = NT / 32, MW = H * S;
+  constexpr int PS = S | 1, PW = H * PS;  // odd chunk pitch: the H chunk reads of one LDS.128 hit distinct banks
+  static_assert(NT % 32 == 0 && (H & (H - 1)) == 0 && H <= 32, "bad window inverse shape");
+  __shared__ double2 prow[2][PW];
+  __shared__ InvCand cand[2][NW];
+  __shared__ double red[NW];
+  __shared__ int pos_of[ROWS];  // physical pivot row of step c = original column of the inverse column made there
+  const InvTask tk = tasks[blockIdx.x];
+  const int m = tk.m;
+  double2* g = arena + int64_t(blockIdx.y) * stride + tk.off;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, h = t & (H - 1), r = t / H;
+  const bool live = r < m;
+  double2 w[S];
+  double mx = 0.0;
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const int c = h * S + j;
+    w[j] = (live && c < m) ? g[int64_t(r) * m + c] : make_double2(0.0, 0.0);
+    mx = fmax(mx, cnorm(w[j]));  // max |a|^2: the singular rule compares squared moduli
+  }
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) red[warp] = mx;
+  sw_barrier<NW>();
+  mx = 0.0;
+#pragma unroll
+  for (int q = 0; q < NW; ++q) mx = fmax(mx, red[q]);
+  const double thr2 = 1e-26 * mx;  // (1e-13 max|a|)^2
+  int pos = r;  // current position of this physical row
+  double2 myip = make_double2(1.0, 0.0);
+  const double2* pw = &prow[0][h * PS];
+#pragma unroll 1
+  for (int k = 0; k < m; ++k) {
+    const int par = k & 1;
+    // window column 0 of my row (held by the row's h == 0 thread), and the
+    // first column of the next chunk (thread h + 1 of the row)
+    double2 f, nx;
+    f.x = __shfl_sync(0xffffffffu, w[0].x, lane & ~(H - 1));
+    f.y = __shfl_sync(0xffffffffu, w[0].y, lane & ~(H - 1));
+    if constexpr (H > 1) {
+      nx.x = __shfl_down_sync(0xffffffffu, w[0].x, 1);
+      nx.y = __shfl_down_sync(0xffffffffu, w[0].y, 1);
+    }
+    // warp argmax over the rows not yet pivoted (pos >= k): largest |a_rk|,
+    // lowest position among equals
+    double best = (live && h == 0 && pos >= k) ? cnorm(f) : -1.0;
+    int bpos = (best >= 0.0) ? pos : 0x7fffffff;
+    const unsigned key = best >= 0.0 ? __float_as_uint(__double2float_ru(best)) : 0u;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
+    const unsigned tied = __ballot_sync(0xffffffffu, key == kmax && best >= 0.0);
+    int wl;  // lane holding the warp's winner
+    if (__popc(tied) <= 1) {
+      wl = tied ? __ffs(tied) - 1 : 0;
+    } else {  // exact order among the lanes whose float images tie
+      double cb = (key == kmax) ? best : -1.0;
+      int cp = (key == kmax) ? bpos : 0x7fffffff, cl = lane;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, cb, o);
+        const int op = __shfl_xor_sync(0xffffffffu, cp, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, cl, o);
+        if (ob > cb || (ob == cb && op < cp)) {
+          cb = ob;
+          cp = op;
+          cl = ol;
+        }
+      }
+      wl = cl;
+    }
+    InvCand win;
+    if constexpr (NW == 1) {
+      win.v = __shfl_sync(0xffffffffu, best, wl);
+      win.pos = __shfl_sync(0xffffffffu, bpos, wl);
+      win.row = __shfl_sync(0xffffffffu, r, wl);
+      win.val.x = __shfl_sync(0xffffffffu, f.x, wl);
+      win.val.y = __shfl_sync(0xffffffffu, f.y, wl);
+    } else {
+      if (lane == wl) cand[par][warp] = InvCand{best, bpos, r, f};
+      __syncthreads();
+      win = cand[par][0];
+#pragma unroll
+      for (int q = 1; q < NW; ++q) {
+        const InvCand o = cand[par][q];
+        if (o.v > win.v || (o.v == win.v && o.pos < win.pos)) win = o;
+      }
+    }
+    if (!(win.v > thr2)) {  // |u_kk| <= 1e-13 max|a| (uniform across the CTA)
+      if (win.v == win.v) {
+        if (t == 0) report_singular(st, e_base + blockIdx.y, tk.fold_pos, k);
+        return;
+      }
+    }
+    const int p = win.pos;
+    if (t == 0) pos_of[k] = win.row;
+    const double rd = 1.0 / fma(win.val.x, win.val.x, win.val.y * win.val.y);
+    const double2 ip = make_double2(win.val.x * rd, -win.val.y * rd);
+    const bool pivot_row = r == win.row;
+    // the incoming column at the right end: the next chunk's first column,
+    // or (last chunk) the unit column of the pivot row
+    double2 last = make_double2(pivot_row ? 1.0 : 0.0, 0.0);
+    if constexpr (H > 1) {
+      if (h != H - 1) last = nx;
+    }
+#ifdef NEGF_SW_NORMALISED  // A/B: pivot row normalised at its own step (k_inverse_rg's arithmetic)
+    if (pivot_row) {
+      double2* d = &prow[par][h * PS];
+#pragma unroll
+      for (int j = 1; j < S; ++j) d[j - 1] = cmul(w[j], ip);
+      d[S - 1] = cmul(last, ip);
+    }
+    sw_barrier<NW>();
+    const double2 fs = pivot_row ? make_double2(0.0, 0.0) : f;
+    const double2* pr = pw + par * PW;
+    if (pivot_row) {
+#pragma unroll
+      for (int j = 1; j < S; ++j) w[j] = pr[j - 1];
+      last = pr[S - 1];
+    }
+#else
+    if (pivot_row) {
+      double2* d = &prow[par][h * PS];
+#pragma unroll
+      for (int j = 1; j < S; ++j) d[j - 1] = w[j];
+      d[S - 1] = last;
+      myip = ip;
+    }
+    sw_barrier<NW>();
+    const double2 fs = pivot_row ? make_double2(0.0, 0.0) : cmul(f, ip);
+    const double2* pr = pw + par * PW;
+#endif
+#pragma unroll
+    for (int j = 1; j < S; ++j) {
+      const double2 q = pr[j - 1];
+      w[j - 1].x = fma(-fs.x, q.x, fma(fs.y, q.y, w[j].x));
+      w[j - 1].y = fma(-fs.x, q.y, fma(-fs.y, q.x, w[j].y));
+    }
+    {
+      const double2 q = pr[S - 1];
+      w[S - 1].x = fma(-fs.x, q.x, fma(fs.y, q.y, last.x));
+      w[S - 1].y = fma(-fs.x, q.y, fma(-fs.y, q.x, last.y));
+    }
+    if (pos == k) pos = p;
+    else if (pos == p) pos = k;
+  }
+  // No row was moved: the elimination turned A into the permutation with a 1
+  // at (pivot row of step k, k), so row k of the inverse is the physical
+  // pivot row of step k (final position pos = k) and the column made at step
+  // c is the original column pos_of[c].
+  __syncthreads();
+  if (live) {
+    const int shift = MW - m;  // the inverse column of step j sits at window column shift + j
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const int c = h * S + j - shift;
+      if (c >= 0) g[int64_t(pos) * m + pos_of[c]] = cmul(w[j], myip);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Multi-CTA blocked Gauss-Jordan for large blocks (m > kSmemInvMax), see
 // plan.hpp: per kPanel-column inner panel, k_bigpanel (one CTA per block and
 // energy) factors the panel with row partial pivoting (in shared memory, or
@@ -1971,18 +2155,42 @@ void launch_combine(const BatchArgs& b, const CombineTask* d_tasks, const Combin
   ++launches;
 }
 
+// Shifting-window variant of a block size (classes 1-3 of inv_size_class):
+// the narrowest window H * S >= m, in steps of 4 columns (a step's cost goes
+// with rows x window width; measured with tools/inv_bench, profiles/
+// inverse_experiments_r02.txt).  0: none (m <= 16 or m > 64).
+static int sw_window(int m) {
+  if (m <= 16 || m > 64) return 0;
+  if (m <= 32) return std::max(20, (m + 3) & ~3);
+  if (m <= 48) return std::max(36, (m + 3) & ~3);
+  return (m + 3) & ~3;
+}
+
+template <int ROWS, int H, int S, int MINB>
+static void launch_sw(dim3 grid, const BatchArgs& b, const InvTask* dt, DevStatus* st, cudaStream_t s) {
+  k_inverse_sw<ROWS, H, S, MINB><<<grid, ROWS * H, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
+}
+
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
                     DevStatus* st, cudaStream_t s, int64_t& launches) {
   // Tasks of a level are pre-sorted by size class (inv_size_class, shared
-  // with plan.cpp), so each variant below covers one contiguous range.
+  // with plan.cpp) and by size within a class, so each variant below covers
+  // one contiguous range.
   int i = 0;
   while (i < count) {
     const int c = inv_size_class(h_tasks[i].m);
+#ifdef NEGF_INV_LEGACY
+    const int win = 0;
+#else
+    const int win = sw_window(h_tasks[i].m);
+#endif
     int j = i;
     int mmax = 0;
-    // the shared-memory variants: one launch per padded size
+    // the register variants: one launch per window width; the shared-memory
+    // variants: one launch per padded size
     while (j < count && inv_size_class(h_tasks[j].m) == c &&
-           (c < 3 || ((h_tasks[j].m + 7) & ~7) == ((h_tasks[i].m + 7) & ~7))) {
+           (win ? sw_window(h_tasks[j].m) == win
+                : (c < 3 || ((h_tasks[j].m + 7) & ~7) == ((h_tasks[i].m + 7) & ~7)))) {
       mmax = std::max(mmax, h_tasks[j].m);
       ++j;
     }
@@ -1996,27 +2204,35 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
       cudaFuncSetAttribute(k_inverse_blocked<false, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       cudaFuncSetAttribute(k_inverse_la<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     }
-#ifdef NEGF_INV_LEGACY
-    // round-1 kernels (A/B builds): shared-memory blocked Gauss-Jordan from 17 up
-    if (c == 1 || c == 2) {
-      if (mmax <= 32)
-        k_inverse_blocked<false, 1, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
-      else
-        k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
-      ++launches;
-      i = j;
-      continue;
-    }
-#endif
-    switch (c) {
-      case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
-      case 1: k_inverse_rg<32, 2, 16><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
-      case 2: k_inverse_rg<48, 2, 24><<<grid, 96, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
-      case 3:  // 49..64: 8-column panel on one warp + DMMA rank-8 updates
-        k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
-        break;
-      default:  // 65..kSmemInvMax: the same with look-ahead (panel p+1 overlaps update p)
-        k_inverse_la<4><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
+    switch (win) {
+      // 17..32: one row per lane, one warp per block
+      case 20: launch_sw<32, 1, 20, 10>(grid, b, dt, st, s); break;
+      case 24: launch_sw<32, 1, 24, 10>(grid, b, dt, st, s); break;
+      case 28: launch_sw<32, 1, 28, 10>(grid, b, dt, st, s); break;
+      case 32: launch_sw<32, 1, 32, 10>(grid, b, dt, st, s); break;
+      // 33..48: two lanes per row, three warps
+      case 36: launch_sw<48, 2, 18, 4>(grid, b, dt, st, s); break;
+      case 40: launch_sw<48, 2, 20, 4>(grid, b, dt, st, s); break;
+      case 44: launch_sw<48, 2, 22, 4>(grid, b, dt, st, s); break;
+      case 48: launch_sw<48, 2, 24, 4>(grid, b, dt, st, s); break;
+      // 49..64: two lanes per row, four warps
+      case 52: launch_sw<64, 2, 26, 3>(grid, b, dt, st, s); break;
+      case 56: launch_sw<64, 2, 28, 3>(grid, b, dt, st, s); break;
+      case 60: launch_sw<64, 2, 30, 3>(grid, b, dt, st, s); break;
+      case 64: launch_sw<64, 2, 32, 3>(grid, b, dt, st, s); break;
+      default:
+        switch (c) {
+          case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
+          // classes 1-3 here only with -DNEGF_INV_LEGACY (A/B builds): the
+          // unrolled register kernel and the shared-memory blocked kernel
+          case 1: k_inverse_rg<32, 2, 16><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
+          case 2: k_inverse_rg<48, 2, 24><<<grid, 96, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
+          case 3:  // 8-column panel on one warp + DMMA rank-8 updates
+            k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
+            break;
+          default:  // 65..kSmemInvMax: the same with look-ahead (panel p+1 overlaps update p)
+            k_inverse_la<4><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
+        }
     }
     ++launches;
     i = j;
