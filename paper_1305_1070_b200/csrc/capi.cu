@@ -214,6 +214,19 @@ void reset_status(negf_gpu* g) {
   ck(cudaMemcpyAsync(g->d_status, &h, sizeof h, cudaMemcpyHostToDevice, g->stream), "status reset");
 }
 
+// Phases (Op::phase bit mask) whose GEMM ops use the Gauss (3M) complex
+// product.  Default 0: the conventional product everywhere.  NEGF_GEMM_3M_PHASES
+// (e.g. 3 = fold + G^r sweep) is an A/B switch: the G^< phases (seeds, N fold,
+// P rows) must keep the conventional product, whose rounding keeps diag G^<
+// imaginary to the reference's level.
+unsigned gauss3m_phases() {
+  static const unsigned m = [] {
+    const char* e = std::getenv("NEGF_GEMM_3M_PHASES");
+    return e ? static_cast<unsigned>(std::atoi(e)) : 0u;
+  }();
+  return m;
+}
+
 // Host-side hooks of a batch replay: `lesser_in` enqueues the Sigma^< upload
 // (it runs right before the first Sigma^< reader is enqueued, so the fold is
 // already queued while a pageable copy stages); with `gr_early`, the G^r
@@ -269,7 +282,8 @@ void run_batch(negf_gpu* g, int nE, int e_base, const double* d_E, const double*
         launch_inverse(b, g->d_inv + op.begin, P.inv_tasks.data() + op.begin, op.count, g->d_status, s, L);
         break;
       case K_GEMM:
-        launch_gemm(b, g->d_tasks, g->d_terms, g->d_tiles, P.gemm_tiles.data(), op.begin, op.count, s, L);
+        launch_gemm(b, g->d_tasks, g->d_terms, g->d_tiles, P.gemm_tiles.data(), op.begin, op.count, s, L,
+                    gauss3m_phases() & (1u << op.phase));
         break;
       case K_DIAG:
         launch_diag(b, g->d_diag, g->d_diag_terms, op.begin, op.count, s, L);

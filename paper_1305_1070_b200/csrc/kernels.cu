@@ -1708,7 +1708,7 @@ __device__ __forceinline__ void gemm_epilogue(double2* base, const GemmTask& tk,
   }
 }
 
-template <int WR, int WC>
+template <int WR, int WC, bool M3>
 __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, const GemmTerm* __restrict__ terms,
                                           const GemmTile& tl, double2* smem) {
   using A = Arr<WR, WC>;
@@ -1719,7 +1719,12 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
   const int live_i = min(2, max(0, (tk.m - tl.m0 - wm + 7) / 8));
   const int live_j = min(2, max(0, (tk.n - tl.n0 - wn + 7) / 8));
 
-#ifdef NEGF_GEMM_3M
+  // Conventional (4M) complex product: Re C = Ar Br - Ai Bi, Im C = Ar Bi +
+  // Ai Br, four real DMMAs per complex subtile step.  The default: the Gauss
+  // (3M) product (-DNEGF_GEMM_3M, 11 % less GEMM time) mixes rounding of the
+  // real parts into the imaginary ones through P3 - P1 - P2, and on config 2
+  // it leaves max|Re G^<_jj| / |G^<_jj| up to 194x the reference's own value
+  // at 40 of 256 energies (4M: at the reference's level; DESIGN.md §4).
   // Gauss (3M) complex product: P1 = Ar Br, P2 = Ai Bi, P3 = (Ar+Ai)(Br+Bi);
   // C = (P1 - P2) + i (P3 - P1 - P2): three real DMMAs per complex subtile
   // step instead of four.  Flop accounting stays 8 m n k.
@@ -1730,21 +1735,6 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
     for (int j = 0; j < 2; ++j)
 #pragma unroll
       for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = p3[i][j][q] = 0.0;
-#else
-  // Conventional (4M) complex product: Re C = Ar Br - Ai Bi, Im C = Ar Bi +
-  // Ai Br, four real DMMAs per complex subtile step.  The default: the Gauss
-  // (3M) product (-DNEGF_GEMM_3M, 11 % less GEMM time) mixes rounding of the
-  // real parts into the imaginary ones through P3 - P1 - P2, and on config 2
-  // it leaves max|Re G^<_jj| / |G^<_jj| up to 194x the reference's own value
-  // at 40 of 256 energies (4M: at the reference's level; DESIGN.md §4).
-  double p1[2][2][2], p2[2][2][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-      for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = 0.0;
-#endif
 
   // Flattened (term, k-chunk) sequence through a 2-stage cp.async ring, one
   // barrier per chunk.  The loader is re-based only when the term changes.
@@ -1823,7 +1813,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         b[j] = b_kr ? Bs[kk * A::LDB_KR + c] : Bs[c * LD_RK + kk];
         b[j].y = flip_sign(b[j].y, conjB);
       }
-#ifdef NEGF_GEMM_3M
+      if constexpr (M3) {
       double as[2], bs[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
@@ -1840,7 +1830,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
           dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
         }
       }
-#else
+      } else {
       double nai[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) nai[i] = flip_sign(a[i].y, int(0x80000000));
@@ -1877,7 +1867,7 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
           dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
         }
       }
-#endif
+      }
     };
     if (live_i > 0 && live_j > 0) {
       if (ksteps == KC) {  // full chunk: straight-line, loads can be hoisted
@@ -1898,11 +1888,11 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
 
   const bool mir = tk.mirror && tl.n0 > tl.m0;  // aligned 32x32 tiles: every entry has c > r
   gemm_epilogue(base, tk, tl.m0 + wm, tl.n0 + wn, mir, [&](int i, int j, int q) {
-#ifdef NEGF_GEMM_3M
+    if constexpr (M3) {
     return make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
-#else
+    } else {
     return make_double2(p1[i][j][q], p2[i][j][q]);
-#endif
+    }
   });
 }
 
@@ -2155,15 +2145,24 @@ void launch_combine(const BatchArgs& b, const CombineTask* d_tasks, const Combin
   ++launches;
 }
 
-// Shifting-window variant of a block size (classes 1-3 of inv_size_class):
+// Shifting-window variant of a block size:
 // the narrowest window H * S >= m, in steps of 4 columns (a step's cost goes
 // with rows x window width; measured with tools/inv_bench, profiles/
 // inverse_experiments_r02.txt).  0: none (m <= 16 or m > 64).
 static int sw_window(int m) {
-  if (m <= 16 || m > 64) return 0;
+  // m <= 16 (the small separators of levels 2-4) stays on k_inverse_reg: the
+  // window kernel is 3 x faster there (-DNEGF_SW_TINY: 1.3 ms per config-2
+  // step), but its rounding moves the resonant energy 211 of the config-2
+  // grid to 1.08 x its parity bar (tests/test_gpu_fullgrid.py).
+#ifndef NEGF_SW_TINY
+  if (m <= 16) return 0;
+#endif
+  if (m <= 0 || m > 100) return 0;
+  if (m <= 16) return std::max(8, (m + 3) & ~3);
   if (m <= 32) return std::max(20, (m + 3) & ~3);
   if (m <= 48) return std::max(36, (m + 3) & ~3);
-  return (m + 3) & ~3;
+  if (m <= 64) return (m + 3) & ~3;
+  return m <= 76 ? 76 : 100;  // separators of the upper levels (few blocks: one CTA per SM)
 }
 
 template <int ROWS, int H, int S, int MINB>
@@ -2205,6 +2204,10 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
       cudaFuncSetAttribute(k_inverse_la<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     }
     switch (win) {
+      // <= 16 (-DNEGF_SW_TINY only): one warp per block, 3 x the 64-thread k_inverse_reg
+      case 8: launch_sw<32, 1, 8, 16>(grid, b, dt, st, s); break;
+      case 12: launch_sw<32, 1, 12, 16>(grid, b, dt, st, s); break;
+      case 16: launch_sw<32, 1, 16, 16>(grid, b, dt, st, s); break;
       // 17..32: one row per lane, one warp per block
       case 20: launch_sw<32, 1, 20, 10>(grid, b, dt, st, s); break;
       case 24: launch_sw<32, 1, 24, 10>(grid, b, dt, st, s); break;
@@ -2220,6 +2223,9 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
       case 56: launch_sw<64, 2, 28, 3>(grid, b, dt, st, s); break;
       case 60: launch_sw<64, 2, 30, 3>(grid, b, dt, st, s); break;
       case 64: launch_sw<64, 2, 32, 3>(grid, b, dt, st, s); break;
+      // 65..100: 2.3 / 1.1 x the look-ahead shared-memory kernel on 74 / 100 wide blocks
+      case 76: launch_sw<80, 2, 38, 1>(grid, b, dt, st, s); break;
+      case 100: launch_sw<104, 4, 25, 1>(grid, b, dt, st, s); break;
       default:
         switch (c) {
           case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
@@ -2230,7 +2236,7 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
           case 3:  // 8-column panel on one warp + DMMA rank-8 updates
             k_inverse_blocked<false, 2, 8><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
             break;
-          default:  // 65..kSmemInvMax: the same with look-ahead (panel p+1 overlaps update p)
+          default:  // 101..kSmemInvMax: the same with look-ahead (panel p+1 overlaps update p)
             k_inverse_la<4><<<grid, INV_THREADS, smem, s>>>(b.arena, b.stride, dt, b.e_base, st);
         }
     }
@@ -2534,14 +2540,24 @@ void launch_leafdiag(const BatchArgs& b, const LeafDiagTask* d_tasks, const Leaf
 // of a batch: 331 GB of DRAM traffic with eg = nE and a static stride, 195 GB
 // with groups of 4 and the atomic counter below, against 298 GB algorithmic);
 // eg = nE runs the 256 copies of a tile side by side.  Defaults: measured.
-__device__ __forceinline__ void gemm_item_index(int64_t w, int nE, int64_t ntiles, int eg, int64_t& ti, int& e) {
+// The last group (energies e_main .. nE - 1, e_main a multiple of eg) may be
+// wider than eg: a few waves of items in tile-major order, longest tiles
+// first, so the launch does not end on a long tile that started last.
+__device__ __forceinline__ void gemm_item_index(int64_t w, int nE, int64_t ntiles, int eg, int e_main, int64_t& ti,
+                                                int& e) {
+  const int64_t main_items = ntiles * e_main;
+  if (w >= main_items) {
+    const int64_t r = w - main_items;
+    const int egc = nE - e_main;
+    ti = r / egc;
+    e = e_main + static_cast<int>(r - ti * egc);
+    return;
+  }
   const int64_t per = ntiles * eg;
   const int64_t grp = w / per;
   const int64_t r = w - grp * per;
-  const int e0 = static_cast<int>(grp) * eg;
-  const int egc = min(eg, nE - e0);
-  ti = r / egc;
-  e = e0 + static_cast<int>(r - ti * egc);
+  ti = r / eg;
+  e = static_cast<int>(grp) * eg + static_cast<int>(r - ti * eg);
 }
 
 // Persistent launch over (tile, energy) items in the grouped order above; one
@@ -2560,12 +2576,13 @@ __device__ __forceinline__ void gemm_ctr_done(unsigned long long* ctr, unsigned 
   }
 }
 
-template <int WR, int WC>
+template <int WR, int WC, bool M3>
 __global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride, int nE,
                                                      const GemmTask* __restrict__ tasks,
                                                      const GemmTerm* __restrict__ terms,
                                                      const GemmTile* __restrict__ tiles, int tile_begin,
-                                                     int64_t items, int eg, unsigned long long* ctr) {
+                                                     int64_t items, int eg, int e_main,
+                                                     unsigned long long* ctr) {
   extern __shared__ double2 gsm[];
   __shared__ int64_t s_next[2];  // double-buffered: slot it & 1 is written in iteration it
   const int64_t ntiles = items / nE;
@@ -2574,7 +2591,7 @@ __global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride,
     if (ctr && threadIdx.x == 0) s_next[it & 1] = int64_t(gridDim.x) + int64_t(atomicAdd(ctr, 1ull));
     int64_t ti;
     int e;
-    gemm_item_index(w, nE, ntiles, eg, ti, e);
+    gemm_item_index(w, nE, ntiles, eg, e_main, ti, e);
     const GemmTile tl = tiles[tile_begin + ti];
     const GemmTask tk = tasks[tl.task];
     // Stage the task's term descriptors in shared memory (read every chunk).
@@ -2589,7 +2606,7 @@ __global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride,
       __syncthreads();
       tp = tsm - tk.term_begin;
     }
-    gemm_item<WR, WC>(arena + e * stride, tk, tp, tl, gsm);
+    gemm_item<WR, WC, M3>(arena + e * stride, tk, tp, tl, gsm);
     __syncthreads();
     w = ctr ? s_next[it & 1] : w + gridDim.x;
   }
@@ -2608,11 +2625,13 @@ __global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride,
 #define NEGF_WARP_UNROLL 1
 #endif
 constexpr int kWarpUnroll = NEGF_WARP_UNROLL;
+template <bool M3>
 __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* arena, int64_t stride, int nE,
                                                       const GemmTask* __restrict__ tasks,
                                                       const GemmTerm* __restrict__ terms,
                                                       const GemmTile* __restrict__ tiles, int tile_begin,
-                                                      int64_t items, int eg, unsigned long long* ctr) {
+                                                      int64_t items, int eg, int e_main,
+                                                      unsigned long long* ctr) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wpb = blockDim.x >> 5;
   const int64_t nw = int64_t(gridDim.x) * wpb;
@@ -2628,13 +2647,12 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
     }
     int64_t ti;
     int e;
-    gemm_item_index(w, nE, ntiles, eg, ti, e);
+    gemm_item_index(w, nE, ntiles, eg, e_main, ti, e);
     const GemmTile tl = tiles[tile_begin + ti];
     const GemmTask tk = tasks[tl.task];
     double2* base = arena + int64_t(e) * stride;
     const int live_i = min(2, max(0, (tk.m - tl.m0 + 7) / 8));
     const int live_j = min(2, max(0, (tk.n - tl.n0 + 7) / 8));
-#ifdef NEGF_GEMM_3M
     double p1[2][2][2], p2[2][2][2], p3[2][2][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
@@ -2642,15 +2660,6 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = p3[i][j][q] = 0.0;
-#else
-    double p1[2][2][2], p2[2][2][2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) p1[i][j][q] = p2[i][j][q] = 0.0;
-#endif
     const int ra0 = tl.m0 + g, ra1 = tl.m0 + 8 + g;  // A rows of this lane
     const int cb0 = tl.n0 + g, cb1 = tl.n0 + 8 + g;  // B columns of this lane
     for (int q = tk.term_begin; q < tk.term_begin + tk.term_count; ++q) {
@@ -2683,7 +2692,7 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
         }
 #pragma unroll
         for (int j = 0; j < 2; ++j) b[j].y = flip_sign(b[j].y, conjB);
-#ifdef NEGF_GEMM_3M
+        if constexpr (M3) {
         double as[2], bs[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
@@ -2700,7 +2709,7 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
             dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
           }
         }
-#else
+        } else {
         double nai[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) nai[i] = flip_sign(a[i].y, int(0x80000000));
@@ -2733,28 +2742,43 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
             }
           }
         }
-#endif
+        }
       }
     }
     gemm_epilogue(base, tk, tl.m0, tl.n0, false, [&](int i, int j, int q) {
-#ifdef NEGF_GEMM_3M
+      if constexpr (M3) {
       return make_double2(p1[i][j][q] - p2[i][j][q], p3[i][j][q] - p1[i][j][q] - p2[i][j][q]);
-#else
+      } else {
       return make_double2(p1[i][j][q], p2[i][j][q]);
-#endif
+      }
     });
   }
   if (ctr && lane == 0) gemm_ctr_done(ctr, static_cast<unsigned long long>(nw));
 }
 
-// Energies per item group (gemm_item_index); NEGF_GEMM_EG overrides (A/B).
-static int gemm_energy_group(int nE, bool warp) {
+// Energies per item group and the start of the last group (gemm_item_index).
+// NEGF_GEMM_EG = n > 0 forces groups of n (A/B); NEGF_GEMM_EG = -1 (CTA
+// tiles): wave-sized groups -- as many energies as fill the launch's resident
+// CTAs once, so the tiles of one task run together and share its operand
+// panels through L2 -- with the last three waves as one tile-major group.
+struct EnergyGroups {
+  int eg, e_main;
+};
+static EnergyGroups gemm_energy_groups(int nE, bool warp, int tile_count, int slots) {
   static const int env = [] {
     const char* e = std::getenv("NEGF_GEMM_EG");
     return e ? std::atoi(e) : 0;
   }();
-  const int eg = env > 0 ? env : (warp ? kGemmEgWarp : kGemmEgCta);
-  return std::max(1, std::min(eg, nE));
+  int mode = env != 0 ? env : (warp ? kGemmEgWarp : kGemmEgCta);
+  if (mode < 0 && !warp) {
+    const int wave = std::max(1, slots / std::max(1, tile_count));
+    const int eg = std::min(wave, nE);
+    const int tail = std::min(nE, 3 * wave);
+    return {eg, ((nE - tail) / eg) * eg};
+  }
+  if (mode < 0) mode = kGemmEgWarp;
+  const int eg = std::max(1, std::min(mode, nE));
+  return {eg, (nE / eg) * eg};
 }
 // Dynamic item scheduling (atomic counter) unless NEGF_GEMM_DYN=0 (A/B).
 static unsigned long long* gemm_counter(const BatchArgs& b) {
@@ -2765,6 +2789,7 @@ static unsigned long long* gemm_counter(const BatchArgs& b) {
   return dyn ? b.gemm_ctr : nullptr;
 }
 
+template <bool M3>
 static void launch_gemm_warp(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                              const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
   static int slots_of[64] = {};
@@ -2774,16 +2799,17 @@ static void launch_gemm_warp(const BatchArgs& b, const GemmTask* d_tasks, const 
   if (!slots) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_warp, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm_warp<M3>, 256, 0);
     slots = std::max(1, sms * std::max(1, per_sm));
   }
   const int64_t items = int64_t(tile_count) * b.nE;
   const int grid = static_cast<int>(std::min<int64_t>((items + 7) / 8, slots));
-  k_gemm_warp<<<grid, 256, 0, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items,
-                                   gemm_energy_group(b.nE, true), gemm_counter(b));
+  const EnergyGroups eg = gemm_energy_groups(b.nE, true, tile_count, slots);
+  k_gemm_warp<M3><<<grid, 256, 0, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items, eg.eg,
+                                   eg.e_main, gemm_counter(b));
 }
 
-template <int WR, int WC>
+template <int WR, int WC, bool M3>
 static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                             const GemmTile* d_tiles, int tile_begin, int tile_count, cudaStream_t s) {
   constexpr size_t smem = sizeof(double2) * 2 * Arr<WR, WC>::STAGE + sizeof(GemmTerm) * kTermCache;
@@ -2793,19 +2819,21 @@ static void launch_gemm_arr(const BatchArgs& b, const GemmTask* d_tasks, const G
   int& slots = slots_of[dev & 63];
   if (!slots) {
     int sms = 0, per_sm = 0;
-    cudaFuncSetAttribute(k_gemm<WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_gemm<WR, WC, M3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm<WR, WC>, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gemm<WR, WC, M3>, 128, smem);
     slots = std::max(1, sms * std::max(1, per_sm));
   }
   const int64_t items = int64_t(tile_count) * b.nE;
   const int grid = static_cast<int>(std::min<int64_t>(items, slots));
-  k_gemm<WR, WC><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items,
-                                         gemm_energy_group(b.nE, false), gemm_counter(b));
+  const EnergyGroups eg = gemm_energy_groups(b.nE, false, tile_count, slots);
+  k_gemm<WR, WC, M3><<<grid, 128, smem, s>>>(b.arena, b.stride, b.nE, d_tasks, d_terms, d_tiles, tile_begin, items, eg.eg,
+                                         eg.e_main, gemm_counter(b));
 }
-void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
-                 const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
-                 cudaStream_t s, int64_t& launches) {
+template <bool M3>
+static void launch_gemm_impl(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
+                             const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
+                             cudaStream_t s, int64_t& launches) {
   // Tiles of one op are grouped by warp arrangement (plan.cpp): one launch each.
   int i = tile_begin;
   const int end = tile_begin + tile_count;
@@ -2813,13 +2841,24 @@ void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_
     const int arr = h_tiles[i].arr;
     int j = i;
     while (j < end && h_tiles[j].arr == arr) ++j;
-    if (arr == 1) launch_gemm_arr<1, 4>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
-    else if (arr == 2) launch_gemm_arr<4, 1>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
-    else if (arr == 3) launch_gemm_warp(b, d_tasks, d_terms, d_tiles, i, j - i, s);
-    else launch_gemm_arr<2, 2>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
+    if (arr == 1) launch_gemm_arr<1, 4, M3>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
+    else if (arr == 2) launch_gemm_arr<4, 1, M3>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
+    else if (arr == 3) launch_gemm_warp<M3>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
+    else launch_gemm_arr<2, 2, M3>(b, d_tasks, d_terms, d_tiles, i, j - i, s);
     ++launches;
     i = j;
   }
+}
+// gauss3m: the Gauss (3M) complex product for this op (see gemm_item); the
+// caller decides per op (capi.cu: never for the G^< phases).
+void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
+                 const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
+                 cudaStream_t s, int64_t& launches, bool gauss3m) {
+#ifdef NEGF_GEMM_3M
+  gauss3m = true;  // A/B builds: 3M everywhere (round 1)
+#endif
+  if (gauss3m) launch_gemm_impl<true>(b, d_tasks, d_terms, d_tiles, h_tiles, tile_begin, tile_count, s, launches);
+  else launch_gemm_impl<false>(b, d_tasks, d_terms, d_tiles, h_tiles, tile_begin, tile_count, s, launches);
 }
 
 void launch_diag(const BatchArgs& b, const DiagTask* d_tasks, const GemmTerm* d_terms, int begin,

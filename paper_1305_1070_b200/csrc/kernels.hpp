@@ -44,7 +44,7 @@ void launch_bigperm(const BatchArgs& b, const BigTask* d_tasks, const BigTask* h
                     int64_t& launches);
 void launch_gemm(const BatchArgs& b, const GemmTask* d_tasks, const GemmTerm* d_terms,
                  const GemmTile* d_tiles, const GemmTile* h_tiles, int tile_begin, int tile_count,
-                 cudaStream_t s, int64_t& launches);
+                 cudaStream_t s, int64_t& launches, bool gauss3m = false);
 void launch_spsi(const BatchArgs& b, const SpsiTask* d_tasks, const int* d_colptr, const int* d_rows,
                  const double2* d_vals, const int* d_wcols, int begin, int count, cudaStream_t s, int64_t& launches);
 void launch_mgather(const BatchArgs& b, const MGatherTask* d_tasks, const MGatherBlock* d_blocks, int begin, int count,

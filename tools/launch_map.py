@@ -4,6 +4,7 @@
     python tools/launch_map.py batch [repeats]        # one 256-point batch (run under ncu)
     python tools/launch_map.py map launches.csv ops.json   # per (phase, level) GEMM time and TF/s
     python tools/launch_map.py traffic dram.csv ops.json   # k_gemm DRAM bytes vs algorithmic bytes
+    python tools/launch_map.py shares launches.csv         # kernel shares of any ncu launch list
 
 traffic: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k regex:k_gemm
          --clock-control none --csv --log-file dram.csv python tools/launch_map.py batch
@@ -121,8 +122,31 @@ def traffic(csv_path, ops_path):
         print(f"  {t * 1e3:7.3f} {d / 1e9:7.2f} {a / 1e9:7.2f} {d / a:6.2f}  ph {o['phase']} lv {o['level']} arr {o['arr']}")
 
 
+def shares(csv_path):
+    """Kernel shares of an ncu launch list (any command, e.g. bench.py)."""
+    lines = [ln for ln in open(csv_path) if ln.startswith('"')]
+    rows = list(csv.reader(lines))
+    h, rows = rows[0], rows[1:]
+    i_n, i_v = h.index("Kernel Name"), h.index("Metric Value")
+    byname = collections.defaultdict(lambda: [0, 0.0])
+    tot = 0.0
+    for r in rows:
+        t = float(r[i_v].replace(",", "")) / 1e6
+        key = r[i_n].split("(")[0].replace("(anonymous namespace)::", "").replace("negfb::", "")
+        byname[key][0] += 1
+        byname[key][1] += t
+        tot += t
+    print(f"# {len(rows)} launches, {tot:.2f} ms (ncu per-launch times: serialised, cold caches)")
+    print("# kernel, launches, total ms, share")
+    for k, (n, t) in sorted(byname.items(), key=lambda x: -x[1][1]):
+        print(f"  {k[-52:]:52s} {n:5d} {t:9.2f} ms {100 * t / tot:5.1f} %")
+
+
 if __name__ == "__main__":
     cmd = sys.argv[1]
+    if cmd == "shares":
+        shares(sys.argv[2])
+        sys.exit(0)
     if cmd == "ops":
         op_list(sys.argv[2])
     elif cmd == "batch":

@@ -24,12 +24,14 @@ cap gemm_lv9_fold -k regex:k_gemm --launch-skip $(gidx 0 9 0) -c 1
 cap gemm_lv2_grows_warp -k regex:k_gemm --launch-skip $(gidx 1 2 3) -c 1
 cap gemm_lv5_grows -k regex:k_gemm --launch-skip $(gidx 1 5 0) -c 1
 cap gemm_lv1_compact -k regex:k_gemm --launch-skip $(gidx 1 1 0) -c 1
-cap inverse_blocked -k regex:k_inverse_blocked -c 1
-cap inverse_rg -k regex:k_inverse_rg -c 2
+cap inverse_sw -k regex:k_inverse_sw -c 12
 cap inverse_la -k regex:k_inverse_la -c 1
 cap bigpanel -k regex:k_bigpanel -c 1
 cap sschur -k regex:k_sschur -c 1
 cap spsi -k regex:k_spsi -c 1
 cap mgather -k regex:k_mgather -c 1
-cp /tmp/ncu_gemm_lv9_fold.ncu-rep gpurun_out/ncu/
+# launch list of the bench command itself (kernel shares of the step)
+ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/ncu/bench_launches.csv \
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-rgf --extra-configs= > gpurun_out/ncu/bench_under_ncu.log 2>&1
+python tools/launch_map.py shares gpurun_out/ncu/bench_launches.csv > gpurun_out/ncu/bench_launch_shares.txt 2>&1
 du -sh gpurun_out/ncu; ls -la gpurun_out/ncu
