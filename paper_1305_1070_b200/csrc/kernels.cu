@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1150,13 +1151,51 @@ __device__ __forceinline__ void sw_barrier() {
   else __syncthreads();
 }
 
-template <int ROWS, int H, int S, int MINB>
+// Value type of the window kernel: double2, or double for blocks that are real
+// at every energy (InvTask::real).  The real operations are the complex ones
+// with the zero imaginary parts dropped, so both give the same bits.
+__device__ __forceinline__ double sw_norm(double2 a) { return cnorm(a); }
+__device__ __forceinline__ double sw_norm(double a) { return a * a; }
+__device__ __forceinline__ double2 sw_mul(double2 a, double2 b) { return cmul(a, b); }
+__device__ __forceinline__ double sw_mul(double a, double b) { return a * b; }
+__device__ __forceinline__ double2 sw_shfl(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ double sw_shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+__device__ __forceinline__ double2 sw_shfl_down1(double2 v) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ double sw_shfl_down1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+// w - fs * q
+__device__ __forceinline__ double2 sw_fnma(double2 fs, double2 q, double2 w) {
+  return make_double2(fma(-fs.x, q.x, fma(fs.y, q.y, w.x)), fma(-fs.x, q.y, fma(-fs.y, q.x, w.y)));
+}
+__device__ __forceinline__ double sw_fnma(double fs, double q, double w) { return fma(-fs, q, w); }
+__device__ __forceinline__ void sw_set(double2& v, double re) { v = make_double2(re, 0.0); }
+__device__ __forceinline__ void sw_set(double& v, double re) { v = re; }
+__device__ __forceinline__ void sw_load(double2& v, const double2* p) { v = *p; }
+__device__ __forceinline__ void sw_load(double& v, const double2* p) { v = p->x; }
+__device__ __forceinline__ double2 sw_c(double2 v) { return v; }
+__device__ __forceinline__ double2 sw_c(double v) { return make_double2(v, 0.0); }
+// 1 / pivot from the candidate record (val = the pivot, v = |pivot|^2)
+__device__ __forceinline__ void sw_recip(double2& ip, double2 val) {
+  const double rd = 1.0 / fma(val.x, val.x, val.y * val.y);
+  ip = make_double2(val.x * rd, -val.y * rd);
+}
+__device__ __forceinline__ void sw_recip(double& ip, double2 val) {
+  const double rd = 1.0 / (val.x * val.x);
+  ip = val.x * rd;
+}
+
+template <int ROWS, int H, int S, int MINB, bool REAL>
 __global__ void __launch_bounds__(ROWS * H, MINB)
     k_inverse_sw(double2* arena, int64_t stride, const InvTask* __restrict__ tasks, int e_base, DevStatus* st) {
+  using V = std::conditional_t<REAL, double, double2>;
   constexpr int NT = ROWS * H, NW = NT / 32, MW = H * S;
-  constexpr int PS = S | 1, PW = H * PS;  // odd chunk pitch: the H chunk reads of one LDS.128 hit distinct banks
+  // odd chunk pitch: the H chunk reads of one shared load hit distinct banks
+  constexpr int PS = S | 1, PW = H * PS;
   static_assert(NT % 32 == 0 && (H & (H - 1)) == 0 && H <= 32, "bad window inverse shape");
-  __shared__ double2 prow[2][PW];
+  __shared__ V prow[2][PW];
   __shared__ InvCand cand[2][NW];
   __shared__ double red[NW];
   __shared__ int pos_of[ROWS];  // physical pivot row of step c = original column of the inverse column made there
@@ -1165,13 +1204,14 @@ __global__ void __launch_bounds__(ROWS * H, MINB)
   double2* g = arena + int64_t(blockIdx.y) * stride + tk.off;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, h = t & (H - 1), r = t / H;
   const bool live = r < m;
-  double2 w[S];
+  V w[S];
   double mx = 0.0;
 #pragma unroll
   for (int j = 0; j < S; ++j) {
     const int c = h * S + j;
-    w[j] = (live && c < m) ? g[int64_t(r) * m + c] : make_double2(0.0, 0.0);
-    mx = fmax(mx, cnorm(w[j]));  // max |a|^2: the singular rule compares squared moduli
+    sw_set(w[j], 0.0);
+    if (live && c < m) sw_load(w[j], g + int64_t(r) * m + c);
+    mx = fmax(mx, sw_norm(w[j]));  // max |a|^2: the singular rule compares squared moduli
   }
   for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) red[warp] = mx;
@@ -1181,23 +1221,21 @@ __global__ void __launch_bounds__(ROWS * H, MINB)
   for (int q = 0; q < NW; ++q) mx = fmax(mx, red[q]);
   const double thr2 = 1e-26 * mx;  // (1e-13 max|a|)^2
   int pos = r;  // current position of this physical row
-  double2 myip = make_double2(1.0, 0.0);
-  const double2* pw = &prow[0][h * PS];
+  V myip;
+  sw_set(myip, 1.0);
+  const V* pw = &prow[0][h * PS];
 #pragma unroll 1
   for (int k = 0; k < m; ++k) {
     const int par = k & 1;
     // window column 0 of my row (held by the row's h == 0 thread), and the
     // first column of the next chunk (thread h + 1 of the row)
-    double2 f, nx;
-    f.x = __shfl_sync(0xffffffffu, w[0].x, lane & ~(H - 1));
-    f.y = __shfl_sync(0xffffffffu, w[0].y, lane & ~(H - 1));
-    if constexpr (H > 1) {
-      nx.x = __shfl_down_sync(0xffffffffu, w[0].x, 1);
-      nx.y = __shfl_down_sync(0xffffffffu, w[0].y, 1);
-    }
+    const V f = sw_shfl(w[0], lane & ~(H - 1));
+    V nx;
+    sw_set(nx, 0.0);
+    if constexpr (H > 1) nx = sw_shfl_down1(w[0]);
     // warp argmax over the rows not yet pivoted (pos >= k): largest |a_rk|,
     // lowest position among equals
-    double best = (live && h == 0 && pos >= k) ? cnorm(f) : -1.0;
+    double best = (live && h == 0 && pos >= k) ? sw_norm(f) : -1.0;
     int bpos = (best >= 0.0) ? pos : 0x7fffffff;
     const unsigned key = best >= 0.0 ? __float_as_uint(__double2float_ru(best)) : 0u;
     const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
@@ -1223,13 +1261,14 @@ __global__ void __launch_bounds__(ROWS * H, MINB)
     }
     InvCand win;
     if constexpr (NW == 1) {
+      const double2 fc = sw_c(f);
       win.v = __shfl_sync(0xffffffffu, best, wl);
       win.pos = __shfl_sync(0xffffffffu, bpos, wl);
       win.row = __shfl_sync(0xffffffffu, r, wl);
-      win.val.x = __shfl_sync(0xffffffffu, f.x, wl);
-      win.val.y = __shfl_sync(0xffffffffu, f.y, wl);
+      win.val.x = __shfl_sync(0xffffffffu, fc.x, wl);
+      win.val.y = REAL ? 0.0 : __shfl_sync(0xffffffffu, fc.y, wl);
     } else {
-      if (lane == wl) cand[par][warp] = InvCand{best, bpos, r, f};
+      if (lane == wl) cand[par][warp] = InvCand{best, bpos, r, sw_c(f)};
       __syncthreads();
       win = cand[par][0];
 #pragma unroll
@@ -1246,25 +1285,28 @@ __global__ void __launch_bounds__(ROWS * H, MINB)
     }
     const int p = win.pos;
     if (t == 0) pos_of[k] = win.row;
-    const double rd = 1.0 / fma(win.val.x, win.val.x, win.val.y * win.val.y);
-    const double2 ip = make_double2(win.val.x * rd, -win.val.y * rd);
+    V ip;
+    sw_recip(ip, win.val);
     const bool pivot_row = r == win.row;
     // the incoming column at the right end: the next chunk's first column,
     // or (last chunk) the unit column of the pivot row
-    double2 last = make_double2(pivot_row ? 1.0 : 0.0, 0.0);
+    V last;
+    sw_set(last, pivot_row ? 1.0 : 0.0);
     if constexpr (H > 1) {
       if (h != H - 1) last = nx;
     }
+    V fs;
 #ifdef NEGF_SW_NORMALISED  // A/B: pivot row normalised at its own step (k_inverse_rg's arithmetic)
     if (pivot_row) {
-      double2* d = &prow[par][h * PS];
+      V* d = &prow[par][h * PS];
 #pragma unroll
-      for (int j = 1; j < S; ++j) d[j - 1] = cmul(w[j], ip);
-      d[S - 1] = cmul(last, ip);
+      for (int j = 1; j < S; ++j) d[j - 1] = sw_mul(w[j], ip);
+      d[S - 1] = sw_mul(last, ip);
     }
     sw_barrier<NW>();
-    const double2 fs = pivot_row ? make_double2(0.0, 0.0) : f;
-    const double2* pr = pw + par * PW;
+    fs = f;
+    if (pivot_row) sw_set(fs, 0.0);
+    const V* pr = pw + par * PW;
     if (pivot_row) {
 #pragma unroll
       for (int j = 1; j < S; ++j) w[j] = pr[j - 1];
@@ -1272,27 +1314,20 @@ __global__ void __launch_bounds__(ROWS * H, MINB)
     }
 #else
     if (pivot_row) {
-      double2* d = &prow[par][h * PS];
+      V* d = &prow[par][h * PS];
 #pragma unroll
       for (int j = 1; j < S; ++j) d[j - 1] = w[j];
       d[S - 1] = last;
       myip = ip;
     }
     sw_barrier<NW>();
-    const double2 fs = pivot_row ? make_double2(0.0, 0.0) : cmul(f, ip);
-    const double2* pr = pw + par * PW;
+    fs = sw_mul(f, ip);
+    if (pivot_row) sw_set(fs, 0.0);
+    const V* pr = pw + par * PW;
 #endif
 #pragma unroll
-    for (int j = 1; j < S; ++j) {
-      const double2 q = pr[j - 1];
-      w[j - 1].x = fma(-fs.x, q.x, fma(fs.y, q.y, w[j].x));
-      w[j - 1].y = fma(-fs.x, q.y, fma(-fs.y, q.x, w[j].y));
-    }
-    {
-      const double2 q = pr[S - 1];
-      w[S - 1].x = fma(-fs.x, q.x, fma(fs.y, q.y, last.x));
-      w[S - 1].y = fma(-fs.x, q.y, fma(-fs.y, q.x, last.y));
-    }
+    for (int j = 1; j < S; ++j) w[j - 1] = sw_fnma(fs, pr[j - 1], w[j]);
+    w[S - 1] = sw_fnma(fs, pr[S - 1], last);
     if (pos == k) pos = p;
     else if (pos == p) pos = k;
   }
@@ -1306,7 +1341,7 @@ __global__ void __launch_bounds__(ROWS * H, MINB)
 #pragma unroll
     for (int j = 0; j < S; ++j) {
       const int c = h * S + j - shift;
-      if (c >= 0) g[int64_t(pos) * m + pos_of[c]] = cmul(w[j], myip);
+      if (c >= 0) g[int64_t(pos) * m + pos_of[c]] = sw_c(sw_mul(w[j], myip));
     }
   }
 }
@@ -1796,8 +1831,15 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
     const bool a_rk = (tm.a_op == OP_N);
     const bool b_kr = (tm.b_op == OP_N || tm.b_op == OP_C);
     const int ksteps = min(KC, tm.k - ck0);
-    // One k4-step of the 2x2 subtile block (3M products).
-    auto kstep = [&](int s) {
+    // One k4-step of the 2x2 subtile block.  RE (GemmTerm::real): bit 0 = the
+    // A operand is real (exact zero imaginary parts, e.g. Psi of a cluster the
+    // self-energies never reach), bit 1 = B is real: the products with a zero
+    // factor are skipped -- they add exact zeros, so the sums are unchanged.
+    auto kstep = [&](int s, auto re_c) {
+      constexpr int RE = decltype(re_c)::value;
+      constexpr bool a_re = (RE & 1) != 0, b_re = (RE & 2) != 0;
+      (void)a_re;
+      (void)b_re;
       const int kk = 4 * s + t;
       double2 a[2], b[2];
 #pragma unroll
@@ -1814,71 +1856,79 @@ __device__ __forceinline__ void gemm_item(double2* base, const GemmTask& tk, con
         b[j].y = flip_sign(b[j].y, conjB);
       }
       if constexpr (M3) {
-      double as[2], bs[2];
+        double as[2], bs[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
+        for (int i = 0; i < 2; ++i) as[i] = a[i].x + a[i].y;
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
+        for (int j = 0; j < 2; ++j) bs[j] = b[j].x + b[j].y;
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        if (i >= live_i) break;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (j >= live_j) break;
-          dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
-          dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].y);
-          dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
-        }
-      }
-      } else {
-      double nai[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) nai[i] = flip_sign(a[i].y, int(0x80000000));
-      if (live_i == 2 && live_j == 2) {
-        // all four subtiles live: the first product of every accumulator,
-        // then the second, so 8 independent DMMAs separate the dependent
-        // ones (the asm statements keep their order; same per-accumulator
-        // summation order as below)
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 2; ++i) {
+          if (i >= live_i) break;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
+            if (j >= live_j) break;
             dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
-            dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+            dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].y);
+            dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
           }
+        }
+      } else {
+        double nai[2];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 2; ++i) nai[i] = flip_sign(a[i].y, int(0x80000000));
+        if (live_i == 2 && live_j == 2) {
+          // all four subtiles live: the first product of every accumulator,
+          // then the second, so 8 independent DMMAs separate the dependent
+          // ones (the asm statements keep their order; same per-accumulator
+          // summation order as below)
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+              if constexpr (!b_re) dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+            }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              if constexpr (!a_re && !b_re) dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
+              if constexpr (!a_re) dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
+            }
+          return;
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (i >= live_i) break;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
-            dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
-            dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
+            if (j >= live_j) break;
+            dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
+            if constexpr (!a_re && !b_re) dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
+            if constexpr (!b_re) dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+            if constexpr (!a_re) dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
           }
-        return;
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        if (i >= live_i) break;
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (j >= live_j) break;
-          dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
-          dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
-          dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
-          dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
         }
-      }
       }
     };
-    if (live_i > 0 && live_j > 0) {
+    auto chunk = [&](auto re_c) {
       if (ksteps == KC) {  // full chunk: straight-line, loads can be hoisted
 #pragma unroll
-        for (int s = 0; s < KC / 4; ++s) kstep(s);
+        for (int s = 0; s < KC / 4; ++s) kstep(s, re_c);
       } else {
 #pragma unroll
         for (int s = 0; s < KC / 4; ++s) {
           if (4 * s >= ksteps) break;
-          kstep(s);
+          kstep(s, re_c);
         }
+      }
+    };
+    if (live_i > 0 && live_j > 0) {
+      switch (M3 ? 0 : tm.real) {
+        case 1: chunk(std::integral_constant<int, 1>{}); break;
+        case 2: chunk(std::integral_constant<int, 2>{}); break;
+        case 3: chunk(std::integral_constant<int, 3>{}); break;
+        default: chunk(std::integral_constant<int, 0>{});
       }
     }
     stage ^= 1;
@@ -2165,9 +2215,12 @@ static int sw_window(int m) {
   return m <= 76 ? 76 : 100;  // separators of the upper levels (few blocks: one CTA per SM)
 }
 
-template <int ROWS, int H, int S, int MINB>
-static void launch_sw(dim3 grid, const BatchArgs& b, const InvTask* dt, DevStatus* st, cudaStream_t s) {
-  k_inverse_sw<ROWS, H, S, MINB><<<grid, ROWS * H, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
+// MINB / MINR: resident CTAs per SM asked of the complex / real instantiation
+// (a real block needs half the registers).
+template <int ROWS, int H, int S, int MINB, int MINR>
+static void launch_sw(dim3 grid, const BatchArgs& b, const InvTask* dt, DevStatus* st, cudaStream_t s, bool real) {
+  if (real) k_inverse_sw<ROWS, H, S, MINR, true><<<grid, ROWS * H, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
+  else k_inverse_sw<ROWS, H, S, MINB, false><<<grid, ROWS * H, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
 }
 
 void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h_tasks, int count,
@@ -2185,10 +2238,11 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
 #endif
     int j = i;
     int mmax = 0;
-    // the register variants: one launch per window width; the shared-memory
-    // variants: one launch per padded size
+    // the register variants: one launch per window width and value type (real /
+    // complex blocks); the shared-memory variants: one launch per padded size
+    const bool real = win && h_tasks[i].real;
     while (j < count && inv_size_class(h_tasks[j].m) == c &&
-           (win ? sw_window(h_tasks[j].m) == win
+           (win ? (sw_window(h_tasks[j].m) == win && (h_tasks[j].real != 0) == real)
                 : (c < 3 || ((h_tasks[j].m + 7) & ~7) == ((h_tasks[i].m + 7) & ~7)))) {
       mmax = std::max(mmax, h_tasks[j].m);
       ++j;
@@ -2205,27 +2259,27 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
     }
     switch (win) {
       // <= 16 (-DNEGF_SW_TINY only): one warp per block, 3 x the 64-thread k_inverse_reg
-      case 8: launch_sw<32, 1, 8, 16>(grid, b, dt, st, s); break;
-      case 12: launch_sw<32, 1, 12, 16>(grid, b, dt, st, s); break;
-      case 16: launch_sw<32, 1, 16, 16>(grid, b, dt, st, s); break;
+      case 8: launch_sw<32, 1, 8, 16, 16>(grid, b, dt, st, s, real); break;
+      case 12: launch_sw<32, 1, 12, 16, 16>(grid, b, dt, st, s, real); break;
+      case 16: launch_sw<32, 1, 16, 16, 16>(grid, b, dt, st, s, real); break;
       // 17..32: one row per lane, one warp per block
-      case 20: launch_sw<32, 1, 20, 10>(grid, b, dt, st, s); break;
-      case 24: launch_sw<32, 1, 24, 10>(grid, b, dt, st, s); break;
-      case 28: launch_sw<32, 1, 28, 10>(grid, b, dt, st, s); break;
-      case 32: launch_sw<32, 1, 32, 10>(grid, b, dt, st, s); break;
+      case 20: launch_sw<32, 1, 20, 10, 16>(grid, b, dt, st, s, real); break;
+      case 24: launch_sw<32, 1, 24, 10, 16>(grid, b, dt, st, s, real); break;
+      case 28: launch_sw<32, 1, 28, 10, 16>(grid, b, dt, st, s, real); break;
+      case 32: launch_sw<32, 1, 32, 10, 16>(grid, b, dt, st, s, real); break;
       // 33..48: two lanes per row, three warps
-      case 36: launch_sw<48, 2, 18, 4>(grid, b, dt, st, s); break;
-      case 40: launch_sw<48, 2, 20, 4>(grid, b, dt, st, s); break;
-      case 44: launch_sw<48, 2, 22, 4>(grid, b, dt, st, s); break;
-      case 48: launch_sw<48, 2, 24, 4>(grid, b, dt, st, s); break;
+      case 36: launch_sw<48, 2, 18, 4, 8>(grid, b, dt, st, s, real); break;
+      case 40: launch_sw<48, 2, 20, 4, 8>(grid, b, dt, st, s, real); break;
+      case 44: launch_sw<48, 2, 22, 4, 8>(grid, b, dt, st, s, real); break;
+      case 48: launch_sw<48, 2, 24, 4, 8>(grid, b, dt, st, s, real); break;
       // 49..64: two lanes per row, four warps
-      case 52: launch_sw<64, 2, 26, 3>(grid, b, dt, st, s); break;
-      case 56: launch_sw<64, 2, 28, 3>(grid, b, dt, st, s); break;
-      case 60: launch_sw<64, 2, 30, 3>(grid, b, dt, st, s); break;
-      case 64: launch_sw<64, 2, 32, 3>(grid, b, dt, st, s); break;
+      case 52: launch_sw<64, 2, 26, 3, 6>(grid, b, dt, st, s, real); break;
+      case 56: launch_sw<64, 2, 28, 3, 6>(grid, b, dt, st, s, real); break;
+      case 60: launch_sw<64, 2, 30, 3, 6>(grid, b, dt, st, s, real); break;
+      case 64: launch_sw<64, 2, 32, 3, 6>(grid, b, dt, st, s, real); break;
       // 65..100: 2.3 / 1.1 x the look-ahead shared-memory kernel on 74 / 100 wide blocks
-      case 76: launch_sw<80, 2, 38, 1>(grid, b, dt, st, s); break;
-      case 100: launch_sw<104, 4, 25, 1>(grid, b, dt, st, s); break;
+      case 76: launch_sw<80, 2, 38, 1, 2>(grid, b, dt, st, s, real); break;
+      case 100: launch_sw<104, 4, 25, 1, 2>(grid, b, dt, st, s, real); break;
       default:
         switch (c) {
           case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
@@ -2675,6 +2729,12 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
       const int64_t as_r = a_rk ? tm.lda : 1, as_k = a_rk ? 1 : tm.lda;
       const int64_t bs_k = b_kr ? tm.ldb : 1, bs_c = b_kr ? 1 : tm.ldb;
       const bool va0 = ra0 < tk.m, va1 = ra1 < tk.m, vb0 = cb0 < tk.n, vb1 = cb1 < tk.n;
+      // RE (GemmTerm::real): products with an exactly-zero factor skipped (gemm_item)
+      auto kloop = [&](auto re_c) {
+        constexpr int RE = decltype(re_c)::value;
+        constexpr bool a_re = (RE & 1) != 0, b_re = (RE & 2) != 0;
+        (void)a_re;
+        (void)b_re;
 #pragma unroll kWarpUnroll
       for (int k0 = 0; k0 < tm.k; k0 += 4) {
         const int kk = k0 + t;
@@ -2719,14 +2779,14 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
-              dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+              if constexpr (!b_re) dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
             }
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-              dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
-              dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
+              if constexpr (!a_re && !b_re) dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
+              if constexpr (!a_re) dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
             }
         } else {
 #pragma unroll
@@ -2736,13 +2796,20 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
             for (int j = 0; j < 2; ++j) {
               if (j >= live_j) break;
               dmma(p1[i][j][0], p1[i][j][1], a[i].x, b[j].x);
-              dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
-              dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
-              dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
+              if constexpr (!a_re && !b_re) dmma(p1[i][j][0], p1[i][j][1], nai[i], b[j].y);
+              if constexpr (!b_re) dmma(p2[i][j][0], p2[i][j][1], a[i].x, b[j].y);
+              if constexpr (!a_re) dmma(p2[i][j][0], p2[i][j][1], a[i].y, b[j].x);
             }
           }
         }
         }
+      }
+      };
+      switch (M3 ? 0 : tm.real) {
+        case 1: kloop(std::integral_constant<int, 1>{}); break;
+        case 2: kloop(std::integral_constant<int, 2>{}); break;
+        case 3: kloop(std::integral_constant<int, 3>{}); break;
+        default: kloop(std::integral_constant<int, 0>{});
       }
     }
     gemm_epilogue(base, tk, tl.m0, tl.n0, false, [&](int i, int j, int q) {

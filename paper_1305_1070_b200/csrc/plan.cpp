@@ -64,6 +64,8 @@ struct Builder {
     g.ldb = ldb;
     g.a_off = a_off;
     g.b_off = b_off;
+    g.real = 0;
+    g.pad = 0;
     terms.push_back(g);
     return static_cast<int>(terms.size()) - 1;
   }
@@ -389,7 +391,9 @@ namespace {
 // quadratic form once, from 2 Psi), sparse (stencil-entry leaf Psi / Schur
 // contributions), hull (structural zero columns skipped), compact (the
 // diagonal-only rows of sparse leaves as one gathered Psi_H M Psi_H^T form per
-// leaf, MGatherTask; hull only, so exact zeros are all it skips).  Off by default,
+// leaf, MGatherTask; hull only, so exact zeros are all it skips), real (blocks
+// that are real for every energy -- mark_real_operands -- skip the products
+// with their zero imaginary parts: bit-identical results).  Off by default,
 // because they measurably lose accuracy against the dense truth at
 // ill-conditioned energies (profiles/parity_forms_r02.txt):
 // mirror_schur / mirror_g / mirror_p (upper triangle of a symmetric /
@@ -398,10 +402,99 @@ namespace {
 // replaces the set for A/B experiments.
 bool form_on(const char* name) {
   const char* e = std::getenv("NEGF_PLAN_FORMS");
-  const std::string s = std::string(",") + (e ? e : "symdiag_g,symdiag_p,sparse,hull,compact") + ",";
+  const std::string s = std::string(",") + (e ? e : "symdiag_g,symdiag_p,sparse,hull,compact,real") + ",";
   return s.find(std::string(",") + name + ",") != std::string::npos;
 }
 }  // namespace
+
+// Real blocks.  With a real Hamiltonian, A(E) = E - H - Sigma^r(E) is complex
+// only through Sigma^r, which touches the contact (and phonon) dofs.  A
+// cluster none of whose dofs, and none of whose descendants' dofs, carries a
+// Sigma^r entry is eliminated in real arithmetic: A_xx, A_{x,S}, their Schur
+// fill (all from such descendants), A_xx^-1 and Psi_x have exactly zero
+// imaginary parts at every energy, whatever values the caller passes.  GEMM
+// terms reading those regions are flagged (GemmTerm::real) and skip the DMMAs
+// whose factor is that zero; flagged inverses run the real kernel.  Skipped
+// products are exact zeros, so every result is bit-identical to the complex
+// evaluation.  The executed-work ledger counts a real x complex term at half
+// and a real x real term or a real inverse at a quarter of the complex cost.
+static void mark_real_operands(Plan& P) {
+  const ProblemDesc& d = P.desc;
+  for (const cplx& v : d.h_vals)
+    if (v.imag() != 0.0) return;
+  const Tree& t = P.tree;
+  const int nc = t.num_clusters();
+  std::vector<int> cl_of(static_cast<std::size_t>(d.n), -1);
+  for (int c = 0; c < nc; ++c)
+    for (int v : t.cluster(c).dofs) cl_of[static_cast<std::size_t>(v)] = c;
+  std::vector<char> real(static_cast<std::size_t>(nc), 1);
+  for (std::size_t k = 0; k < d.sr_rows.size(); ++k) {
+    real[static_cast<std::size_t>(cl_of[static_cast<std::size_t>(d.sr_rows[k])])] = 0;
+    real[static_cast<std::size_t>(cl_of[static_cast<std::size_t>(d.sr_cols[k])])] = 0;
+  }
+  // a complex cluster makes every ancestor complex (its Schur fill lands there)
+  for (int c = 0; c < nc; ++c)
+    if (!real[static_cast<std::size_t>(c)])
+      for (int a : t.cluster(c).anc) real[static_cast<std::size_t>(a)] = 0;
+  // arena regions that hold real data for the whole solve
+  std::vector<std::pair<int64_t, int64_t>> iv;
+  for (int c = 0; c < nc; ++c) {
+    if (!real[static_cast<std::size_t>(c)]) continue;
+    const ClusterInfo& X = P.ci[static_cast<std::size_t>(c)];
+    const int64_t m = X.m;
+    if (X.off_d >= 0) iv.push_back({X.off_d, X.off_d + m * m});
+    if (X.off_arow >= 0 && X.K > 0) iv.push_back({X.off_arow, X.off_arow + m * X.K});
+    if (X.off_psi >= 0 && X.K > 0) iv.push_back({X.off_psi, X.off_psi + m * X.K});
+    if (X.off_psi2 >= 0 && X.K > 0) iv.push_back({X.off_psi2, X.off_psi2 + m * X.K});
+    if (X.off_psic >= 0 && X.hc > 0) iv.push_back({X.off_psic, X.off_psic + m * X.hc});
+  }
+  if (iv.empty()) return;
+  std::sort(iv.begin(), iv.end());
+  auto is_real = [&](int64_t off) {
+    auto it = std::upper_bound(iv.begin(), iv.end(), std::make_pair(off, std::numeric_limits<int64_t>::max()));
+    if (it == iv.begin()) return false;
+    --it;
+    return off >= it->first && off < it->second;
+  };
+  for (GemmTerm& g : P.gemm_terms) g.real = (is_real(g.a_off) ? 1 : 0) | (is_real(g.b_off) ? 2 : 0);
+  for (InvTask& it : P.inv_tasks) it.real = real[static_cast<std::size_t>(it.cluster)] ? 1 : 0;
+  // executed work
+  P.exec_cmul = 0.0;
+  for (Op& op : P.ops) {
+    if (op.kind == K_GEMM && !op.inv_update) {
+      std::vector<double> area(static_cast<std::size_t>(op.task_count), 0.0);
+      for (int q = op.begin; q < op.begin + op.count; ++q) {
+        const GemmTile& tl = P.gemm_tiles[static_cast<std::size_t>(q)];
+        const GemmTask& tk = P.gemm_tasks[static_cast<std::size_t>(tl.task)];
+        const int lm = std::min(kArrTM[tl.arr], tk.m - tl.m0), ln = std::min(kArrTN[tl.arr], tk.n - tl.n0);
+        area[static_cast<std::size_t>(tl.task - op.task_begin)] += double(lm) * ln;
+      }
+      double cm = 0.0;
+      for (int a = 0; a < op.task_count; ++a) {
+        const GemmTask& tk = P.gemm_tasks[static_cast<std::size_t>(op.task_begin + a)];
+        for (int q = tk.term_begin; q < tk.term_begin + tk.term_count; ++q) {
+          const GemmTerm& g = P.gemm_terms[static_cast<std::size_t>(q)];
+          const double wgt = g.real == 3 ? 0.25 : g.real ? 0.5 : 1.0;
+          cm += area[static_cast<std::size_t>(a)] * g.k * wgt;
+        }
+      }
+      op.cmul = cm;
+    } else if (op.kind == K_INVERSE) {
+      double cm = 0.0;
+      for (int q = op.begin; q < op.begin + op.count; ++q) {
+        const InvTask& it = P.inv_tasks[static_cast<std::size_t>(q)];
+        cm += double(it.m) * it.m * it.m * (it.real ? 0.25 : 1.0);
+      }
+      op.cmul = cm;
+    }
+    P.exec_cmul += op.cmul;
+  }
+  P.exec_inv_cmul = 0.0;
+  for (int c = 0; c < nc; ++c) {
+    const double m = t.cluster(c).size();
+    P.exec_inv_cmul += m * m * m * ((real[static_cast<std::size_t>(c)] && m <= kSmemInvMax) ? 0.25 : 1.0);
+  }
+}
 
 Plan build_plan(ProblemDesc desc) {
   Plan P;
@@ -1705,6 +1798,7 @@ Plan build_plan(ProblemDesc desc) {
       break;
     }
   P.gr_done_op = P.lesser_op;
+  if (form_on("real")) mark_real_operands(P);
   return P;
 }
 

@@ -86,6 +86,10 @@ struct GemmTerm {
   int sign;        // +1 / -1
   int lda, ldb;
   int64_t a_off, b_off;
+  // bit 0: the A operand is real for every energy (zero imaginary parts,
+  // exactly), bit 1: B is -- set by mark_real_operands (plan.cpp)
+  int real;
+  int pad;
 };
 
 // CTA tile of a grouped GEMM launch.
@@ -119,7 +123,7 @@ struct InvTask {
   int m;
   int cluster;
   int fold_pos;   // position in fold order (root = nc-1): error precedence
-  int pad;
+  int real;       // the block is real for every energy (mark_real_operands)
   int64_t off;
 };
 

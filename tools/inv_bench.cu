@@ -18,7 +18,7 @@ int main(int argc, char** argv) {
   for (int b = 0; b < nb; ++b)
     for (int i = 0; i < m; ++i)
       for (int j = 0; j < m; ++j)
-        h[int64_t(b) * m * m + i * m + j] = make_double2(drand48() - 0.5 + (i == j ? 2.0 * m * dom : 0.0), drand48() - 0.5);
+        h[int64_t(b) * m * m + i * m + j] = make_double2(drand48() - 0.5 + (i == j ? 2.0 * m * dom : 0.0), getenv("INV_REAL") ? 0.0 * drand48() : drand48() - 0.5);
   double2* arena;
   cudaMalloc(&arena, sizeof(double2) * stride * nE);
   for (int e = 0; e < nE; ++e) cudaMemcpy(arena + e * stride, h.data(), sizeof(double2) * stride, cudaMemcpyHostToDevice);
@@ -27,7 +27,7 @@ int main(int argc, char** argv) {
     return 0;
   }
   std::vector<InvTask> t(nb);
-  for (int b = 0; b < nb; ++b) t[b] = InvTask{m, b, b, 0, int64_t(b) * m * m};
+  for (int b = 0; b < nb; ++b) t[b] = InvTask{m, b, b, getenv("INV_REAL") && !getenv("INV_REAL_COMPLEX_KERNEL") ? 1 : 0, int64_t(b) * m * m};
   InvTask* dt;
   cudaMalloc(&dt, sizeof(InvTask) * nb);
   cudaMemcpy(dt, t.data(), sizeof(InvTask) * nb, cudaMemcpyHostToDevice);
@@ -53,7 +53,8 @@ int main(int argc, char** argv) {
     else if (!strcmp(shape, "48x2")) k_inverse_rg<48, 2, 24><<<grid, 96>>>(arena, stride, dt, 0, st);
     // shifting-window kernel: sw:ROWSxHxS
 #define SWV(R, HH, SS, MB) else if (!strcmp(shape, "sw:" #R "x" #HH "x" #SS "x" #MB)) \
-      k_inverse_sw<R, HH, SS, MB><<<grid, R * HH>>>(arena, stride, dt, 0, st);
+      { if (getenv("SW_REAL")) k_inverse_sw<R, HH, SS, MB, true><<<grid, R * HH>>>(arena, stride, dt, 0, st); \
+        else k_inverse_sw<R, HH, SS, MB, false><<<grid, R * HH>>>(arena, stride, dt, 0, st); }
     SWV(32, 1, 8, 16) SWV(32, 1, 12, 16) SWV(32, 1, 16, 16) SWV(32, 1, 16, 12) SWV(32, 1, 28, 8) SWV(32, 1, 32, 8) SWV(32, 1, 32, 10) SWV(32, 2, 14, 8) SWV(32, 2, 16, 8) SWV(32, 2, 16, 10)
     SWV(32, 4, 8, 8) SWV(32, 4, 8, 12)
     SWV(48, 2, 20, 4) SWV(48, 2, 24, 4) SWV(48, 2, 24, 5) SWV(48, 4, 12, 4) SWV(48, 4, 12, 5) SWV(64, 1, 48, 2) SWV(64, 1, 48, 3)

@@ -1,6 +1,3 @@
-# Shifting-window inverse kernel variants against the dispatched kernels (tools/inv_bench).
+# real vs complex window inverse kernels on real blocks (tools/inv_bench)
 cd tools
-run() { m=$1; nb=$2; shift; shift; NEGF_INV_FORCE_LEGACY=1 ./inv_bench $m $nb 256 0; for s in "$@"; do echo -n "  $s: "; RG_SHAPE=$s ./inv_bench $m $nb 256 0; done; }
-run 6 500 sw:32x1x8x16 sw:32x1x12x16
-run 11 500 sw:32x1x12x16 sw:32x1x16x16 sw:32x1x16x12
-run 14 500 sw:32x1x16x16 sw:32x1x16x12
+for m in 27 32 40 48 56 64; do INV_REAL=1 INV_REAL_COMPLEX_KERNEL=1 ./inv_bench $m 200 256 0; INV_REAL=1 ./inv_bench $m 200 256 0; done
