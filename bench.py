@@ -538,12 +538,22 @@ def bench_ours(args, rank: int, world: int, local_rank: int) -> None:
         "plan": {"clusters": info.n_clusters, "levels": info.levels, "max_block": info.max_block,
                  "arena_mib_per_energy": info.arena_bytes_per_energy / 2**20,
                  "exec_gflop_per_energy": info.exec_flops / 1e9,
+                 "needed_gflop_per_energy_8mkn": info.needed_flops / 1e9,
+                 "real_clusters": info.n_real_clusters,
                  "ref_ledger_gflop_per_energy": info.ref_ledger_flops / 1e9,
                  "plan_seconds": plan_s, "max_real_residual": max_resid,
-                 "fp64_tflops_step": step_tflops, "fp64_peak_frac_step": step_tflops / FP64_PEAK_TFLOPS},
+                 "fp64_tflops_step": step_tflops, "fp64_peak_frac_step": step_tflops / FP64_PEAK_TFLOPS,
+                 "needed_8mkn_tflops_step": info.needed_flops * per_rank / (ms / 1e3) / 1e12,
+                 "note": "exec = real FP64 flops the pipes execute: products with a real operand (blocks of "
+                         "clusters the self-energies never reach have exactly zero imaginary parts) skip the "
+                         "DMMAs of the zero part and count 1/2 (real x real, real inverses: 1/4); "
+                         "needed_8mkn = the same needed-only work counted as complex throughout"},
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": gemm_tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": "k_gemm (grouped complex GEMM, DMMA.8x8x4)",
+                     "note": "achieved = executed real FP64 flops of k_gemm / its CUDA-event time; terms with a "
+                             "real operand execute 2 (real x real: 1) of the 4 DMMAs of a complex product, so "
+                             "most launches are bound by operand staging, not by the DMMA pipe",
                      "peak_source": "measured FP64 DMMA micro-benchmark (tools/fp64_peak.cu, profiles/fp64_peak_r01.txt); "
                                     "MEASURED_PEAKS.json has no FP64 figure",
                      "kernels": {k: {"ms_per_step": v["ms"] / args.steps,

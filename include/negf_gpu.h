@@ -99,9 +99,14 @@ typedef struct {
   int64_t arena_bytes_per_energy;
   int64_t ref_fold_mul, ref_fold_inv;    /* reference ledger, per energy */
   int64_t ref_gless_mul, ref_gless_inv;
-  double exec_cmul;                      /* executed complex MACs / energy */
+  double exec_cmul;                      /* executed work / energy in complex MACs (8 real flops):
+                                            a product with a real operand counts 1/2, real x real
+                                            and real inverses 1/4 (what the FP64 pipes execute) */
   double exec_inv_cmul;
   int n_ops, n_gemm_tasks, n_gemm_tiles, n_inv_tasks;
+  double needed_cmul;                    /* the same needed-only work counted as complex throughout
+                                            (8 m n k per product, 8 m^3 per inverse) */
+  int n_real_clusters, pad_;             /* clusters eliminated in real arithmetic */
 } negf_plan_info;
 
 int negf_plan_create(const negf_problem* p, negf_plan** out, negf_status* st);

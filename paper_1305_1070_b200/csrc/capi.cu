@@ -480,6 +480,9 @@ int negf_plan_info_get(const negf_plan* h, negf_plan_info* info) {
   info->ref_gless_inv = P.ref_gless.inverse_ops;
   info->exec_cmul = P.exec_cmul;
   info->exec_inv_cmul = P.exec_inv_cmul;
+  info->needed_cmul = P.needed_cmul > 0.0 ? P.needed_cmul : P.exec_cmul;
+  info->n_real_clusters = P.n_real_clusters;
+  info->pad_ = 0;
   info->n_ops = static_cast<int>(P.ops.size());
   info->n_gemm_tasks = static_cast<int>(P.gemm_tasks.size());
   info->n_gemm_tiles = static_cast<int>(P.gemm_tiles.size());

@@ -459,6 +459,8 @@ static void mark_real_operands(Plan& P) {
   for (GemmTerm& g : P.gemm_terms) g.real = (is_real(g.a_off) ? 1 : 0) | (is_real(g.b_off) ? 2 : 0);
   for (InvTask& it : P.inv_tasks) it.real = real[static_cast<std::size_t>(it.cluster)] ? 1 : 0;
   // executed work
+  P.needed_cmul = P.exec_cmul;
+  for (int c = 0; c < nc; ++c) P.n_real_clusters += real[static_cast<std::size_t>(c)] ? 1 : 0;
   P.exec_cmul = 0.0;
   for (Op& op : P.ops) {
     if (op.kind == K_GEMM && !op.inv_update) {

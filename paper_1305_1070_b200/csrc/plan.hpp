@@ -377,6 +377,8 @@ struct Plan {
   Ledger ref_fold, ref_gless;   // reference ledger per energy (hsc_fold / hsc_gless)
   double exec_cmul = 0.0;       // executed complex MACs per energy (incl. inversions m^3)
   double exec_inv_cmul = 0.0;
+  double needed_cmul = 0.0;     // exec_cmul before the real-block weights (0: no real blocks)
+  int n_real_clusters = 0;
   int max_block = 0;
 };
 

@@ -155,6 +155,9 @@ class _PlanInfo(C.Structure):
         ("n_gemm_tasks", C.c_int),
         ("n_gemm_tiles", C.c_int),
         ("n_inv_tasks", C.c_int),
+        ("needed_cmul", C.c_double),
+        ("n_real_clusters", C.c_int),
+        ("pad_", C.c_int),
     ]
 
 
@@ -405,6 +408,13 @@ class PlanInfo:
     n_gemm_tasks: int
     n_gemm_tiles: int
     n_inv_tasks: int
+    needed_cmul: float = 0.0
+    n_real_clusters: int = 0
+
+    @property
+    def needed_flops(self) -> float:
+        """The needed-only work per energy counted as complex throughout (8 m n k, 8 m^3)."""
+        return 8.0 * self.needed_cmul
 
     @property
     def ref_ledger_flops(self) -> float:
@@ -443,7 +453,7 @@ class HscPlan:
     def info(self) -> PlanInfo:
         i = _PlanInfo()
         _lib.negf_plan_info_get(self._h, C.byref(i))
-        return PlanInfo(*[getattr(i, f[0]) for f in _PlanInfo._fields_])
+        return PlanInfo(*[getattr(i, f[0]) for f in _PlanInfo._fields_ if f[0] != "pad_"])
 
     def tree(self) -> SeparatorTree:
         info = self.info()
