@@ -1661,13 +1661,16 @@ struct OperandLoader {
 };
 
 constexpr int kTermCache = 48;
-// Energy groups of the item order (measured on config 2, dynamic scheduling):
-// the CTA tiles run best with all energies in one group (energy fastest: the
-// copies of a tile run side by side, LPT over tiles; 70.7 vs 72.8 ms per batch
-// for groups of 4), the warp tiles of the small separators with one energy per
-// group (24.8 vs 25.4 ms).
+// Energy groups of the item order (gemm_energy_groups; measured on config 2,
+// dynamic scheduling).  CTA tiles: -1 = wave-sized groups, as many energies as
+// fill the launch's resident CTAs once, the last three waves as one tile-major
+// group (93.5 ms of k_gemm per batch and 197 GB of DRAM traffic, against 93.9 ms
+// and 283 GB with all energies in one group, 94.8 ms with groups of 4; before
+// the real-operand terms halved the DMMA work the single group was 0.7 %
+// faster).  Warp tiles of the small separators: one energy per group (24.8 vs
+// 25.4 ms).
 #ifndef NEGF_GEMM_EG_CTA
-#define NEGF_GEMM_EG_CTA (1 << 30)
+#define NEGF_GEMM_EG_CTA (-1)
 #endif
 #ifndef NEGF_GEMM_EG_WARP
 #define NEGF_GEMM_EG_WARP 1
@@ -2215,11 +2218,13 @@ static int sw_window(int m) {
   return m <= 76 ? 76 : 100;  // separators of the upper levels (few blocks: one CTA per SM)
 }
 
-// MINB / MINR: resident CTAs per SM asked of the complex / real instantiation
-// (a real block needs half the registers).
-template <int ROWS, int H, int S, int MINB, int MINR>
+// <ROWS, H, S, MINB>: the complex instantiation; <ROWS, HR, SR, MINR>: the real
+// one (a real block needs half the registers: 49..64-wide real blocks run with
+// one thread per row, 8.8 vs 10.6 ms for 326 x 256 blocks of 64).
+template <int ROWS, int H, int S, int MINB, int HR, int SR, int MINR>
 static void launch_sw(dim3 grid, const BatchArgs& b, const InvTask* dt, DevStatus* st, cudaStream_t s, bool real) {
-  if (real) k_inverse_sw<ROWS, H, S, MINR, true><<<grid, ROWS * H, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
+  static_assert(H * S == HR * SR, "same window for both value types");
+  if (real) k_inverse_sw<ROWS, HR, SR, MINR, true><<<grid, ROWS * HR, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
   else k_inverse_sw<ROWS, H, S, MINB, false><<<grid, ROWS * H, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
 }
 
@@ -2259,27 +2264,27 @@ void launch_inverse(const BatchArgs& b, const InvTask* d_tasks, const InvTask* h
     }
     switch (win) {
       // <= 16 (-DNEGF_SW_TINY only): one warp per block, 3 x the 64-thread k_inverse_reg
-      case 8: launch_sw<32, 1, 8, 16, 16>(grid, b, dt, st, s, real); break;
-      case 12: launch_sw<32, 1, 12, 16, 16>(grid, b, dt, st, s, real); break;
-      case 16: launch_sw<32, 1, 16, 16, 16>(grid, b, dt, st, s, real); break;
+      case 8: launch_sw<32, 1, 8, 16, 1, 8, 16>(grid, b, dt, st, s, real); break;
+      case 12: launch_sw<32, 1, 12, 16, 1, 12, 16>(grid, b, dt, st, s, real); break;
+      case 16: launch_sw<32, 1, 16, 16, 1, 16, 16>(grid, b, dt, st, s, real); break;
       // 17..32: one row per lane, one warp per block
-      case 20: launch_sw<32, 1, 20, 10, 16>(grid, b, dt, st, s, real); break;
-      case 24: launch_sw<32, 1, 24, 10, 16>(grid, b, dt, st, s, real); break;
-      case 28: launch_sw<32, 1, 28, 10, 16>(grid, b, dt, st, s, real); break;
-      case 32: launch_sw<32, 1, 32, 10, 16>(grid, b, dt, st, s, real); break;
+      case 20: launch_sw<32, 1, 20, 10, 1, 20, 16>(grid, b, dt, st, s, real); break;
+      case 24: launch_sw<32, 1, 24, 10, 1, 24, 16>(grid, b, dt, st, s, real); break;
+      case 28: launch_sw<32, 1, 28, 10, 1, 28, 16>(grid, b, dt, st, s, real); break;
+      case 32: launch_sw<32, 1, 32, 10, 1, 32, 16>(grid, b, dt, st, s, real); break;
       // 33..48: two lanes per row, three warps
-      case 36: launch_sw<48, 2, 18, 4, 8>(grid, b, dt, st, s, real); break;
-      case 40: launch_sw<48, 2, 20, 4, 8>(grid, b, dt, st, s, real); break;
-      case 44: launch_sw<48, 2, 22, 4, 8>(grid, b, dt, st, s, real); break;
-      case 48: launch_sw<48, 2, 24, 4, 8>(grid, b, dt, st, s, real); break;
+      case 36: launch_sw<48, 2, 18, 4, 2, 18, 8>(grid, b, dt, st, s, real); break;
+      case 40: launch_sw<48, 2, 20, 4, 2, 20, 8>(grid, b, dt, st, s, real); break;
+      case 44: launch_sw<48, 2, 22, 4, 2, 22, 8>(grid, b, dt, st, s, real); break;
+      case 48: launch_sw<48, 2, 24, 4, 2, 24, 8>(grid, b, dt, st, s, real); break;
       // 49..64: two lanes per row, four warps
-      case 52: launch_sw<64, 2, 26, 3, 6>(grid, b, dt, st, s, real); break;
-      case 56: launch_sw<64, 2, 28, 3, 6>(grid, b, dt, st, s, real); break;
-      case 60: launch_sw<64, 2, 30, 3, 6>(grid, b, dt, st, s, real); break;
-      case 64: launch_sw<64, 2, 32, 3, 6>(grid, b, dt, st, s, real); break;
+      case 52: launch_sw<64, 2, 26, 3, 1, 52, 5>(grid, b, dt, st, s, real); break;
+      case 56: launch_sw<64, 2, 28, 3, 1, 56, 5>(grid, b, dt, st, s, real); break;
+      case 60: launch_sw<64, 2, 30, 3, 1, 60, 5>(grid, b, dt, st, s, real); break;
+      case 64: launch_sw<64, 2, 32, 3, 1, 64, 5>(grid, b, dt, st, s, real); break;
       // 65..100: 2.3 / 1.1 x the look-ahead shared-memory kernel on 74 / 100 wide blocks
-      case 76: launch_sw<80, 2, 38, 1, 2>(grid, b, dt, st, s, real); break;
-      case 100: launch_sw<104, 4, 25, 1, 2>(grid, b, dt, st, s, real); break;
+      case 76: launch_sw<80, 2, 38, 1, 2, 38, 2>(grid, b, dt, st, s, real); break;
+      case 100: launch_sw<104, 4, 25, 1, 4, 25, 2>(grid, b, dt, st, s, real); break;
       default:
         switch (c) {
           case 0: k_inverse_reg<8, 2><<<grid, 64, 0, s>>>(b.arena, b.stride, dt, b.e_base, st); break;
@@ -2824,10 +2829,11 @@ __global__ void __launch_bounds__(256, NEGF_WARP_MINB) k_gemm_warp(double2* aren
 }
 
 // Energies per item group and the start of the last group (gemm_item_index).
-// NEGF_GEMM_EG = n > 0 forces groups of n (A/B); NEGF_GEMM_EG = -1 (CTA
-// tiles): wave-sized groups -- as many energies as fill the launch's resident
-// CTAs once, so the tiles of one task run together and share its operand
-// panels through L2 -- with the last three waves as one tile-major group.
+// Mode -1 (CTA tiles): wave-sized groups -- as many energies as fill the
+// launch's resident CTAs once, so the tiles of one task run together and share
+// its operand panels through L2 -- with the last three waves as one tile-major
+// group (no long tile starts last).  NEGF_GEMM_EG = n > 0 forces groups of n,
+// NEGF_GEMM_EG = 1073741824 one group of all energies (A/B).
 struct EnergyGroups {
   int eg, e_main;
 };

@@ -279,8 +279,15 @@ namespace {
 // and synchronising the chunk regardless of content, the rest per live 8x8
 // subtile (16 per tile).  Measured with tools/gemm_bench: an 8x8 live tile
 // costs 0.40 of a full one.
-constexpr double kTileFixed = 0.36;
+double tile_fixed() {  // NEGF_TILE_FIXED overrides (A/B)
+  static const double v = [] {
+    const char* e = std::getenv("NEGF_TILE_FIXED");
+    return e ? std::atof(e) : 0.36;
+  }();
+  return v;
+}
 double tile_cost(int arr, int m, int n, int m0, int n0) {
+  const double kTileFixed = tile_fixed();
   const int wr = arr == 1 ? 1 : arr == 2 ? 4 : 2, wc = 4 / wr;
   int live = 0;
   for (int a = 0; a < wr; ++a)
@@ -304,11 +311,13 @@ double grid_tiles(int arr, int m, int n, int r0, int r1, int c0, int c1, int tas
 }  // namespace
 
 void tile_task(int task, int m, int n, int ksum, std::vector<GemmTile>& out) {
-  // Small tasks (at most 16 rows, summed depth at most 64: the 6-13-dof
+  // Small tasks (at most 16 rows, summed depth at most 256: the 6-13-dof
   // separators of levels 2-4 on config 2): warp tiles (arr 3), one warp per
   // 16 x 16 block with register fragments straight from L2 / HBM -- measured
-  // 2.9 ms less per config-2 batch than the CTA tiles (fold levels 3-4, G / P
-  // rows of levels 2-3); taller or deeper tasks keep the staged CTA tiles.
+  // 6.3 ms less per config-2 batch than the CTA tiles; the depth bound was 64
+  // before the real-operand terms halved the DMMA work (256: another 0.9 ms;
+  // 32- or 48-row tasks on warp tiles: 2 ms more).  Taller tasks keep the
+  // staged CTA tiles.
   // NEGF_WARP_TILE_M / _K override the bounds (A/B experiments; M = 0 disables).
   static const int warp_m = [] {
     const char* e = std::getenv("NEGF_WARP_TILE_M");
@@ -316,7 +325,7 @@ void tile_task(int task, int m, int n, int ksum, std::vector<GemmTile>& out) {
   }();
   static const int warp_k = [] {
     const char* e = std::getenv("NEGF_WARP_TILE_K");
-    return e ? std::atoi(e) : 64;
+    return e ? std::atoi(e) : 256;
   }();
   if (m <= warp_m && ksum <= warp_k) {
     for (int y = 0; y < m; y += 16)

@@ -57,7 +57,7 @@ int main(int argc, char** argv) {
         else k_inverse_sw<R, HH, SS, MB, false><<<grid, R * HH>>>(arena, stride, dt, 0, st); }
     SWV(32, 1, 8, 16) SWV(32, 1, 12, 16) SWV(32, 1, 16, 16) SWV(32, 1, 16, 12) SWV(32, 1, 28, 8) SWV(32, 1, 32, 8) SWV(32, 1, 32, 10) SWV(32, 2, 14, 8) SWV(32, 2, 16, 8) SWV(32, 2, 16, 10)
     SWV(32, 4, 8, 8) SWV(32, 4, 8, 12)
-    SWV(48, 2, 20, 4) SWV(48, 2, 24, 4) SWV(48, 2, 24, 5) SWV(48, 4, 12, 4) SWV(48, 4, 12, 5) SWV(64, 1, 48, 2) SWV(64, 1, 48, 3)
+    SWV(48, 2, 20, 4) SWV(48, 2, 24, 4) SWV(48, 2, 24, 5) SWV(48, 4, 12, 4) SWV(48, 4, 12, 5) SWV(64, 1, 48, 2) SWV(64, 1, 48, 3) SWV(64, 1, 64, 3) SWV(64, 1, 64, 4) SWV(64, 1, 64, 5) SWV(64, 1, 64, 6) SWV(64, 1, 64, 7) SWV(64, 1, 56, 5) SWV(64, 1, 52, 5) SWV(64, 1, 52, 6) SWV(64, 1, 60, 5) SWV(64, 1, 60, 6) SWV(64, 1, 48, 6) SWV(64, 1, 40, 6) SWV(64, 1, 40, 8)
     SWV(64, 2, 28, 2) SWV(64, 2, 32, 2) SWV(64, 2, 32, 3) SWV(64, 4, 16, 2) SWV(64, 4, 16, 3) SWV(64, 4, 16, 4)
     SWV(96, 4, 24, 1) SWV(112, 4, 28, 1) SWV(104, 4, 25, 1) SWV(128, 4, 28, 1) SWV(80, 4, 20, 1) SWV(80, 4, 19, 1) SWV(80, 4, 20, 2) SWV(104, 4, 26, 1) SWV(104, 8, 13, 1) SWV(80, 2, 38, 1) SWV(112, 8, 14, 1) SWV(128, 8, 15, 1)
     else { printf("unknown RG_SHAPE %s\n", shape); return 1; }
