@@ -2635,8 +2635,11 @@ __device__ __forceinline__ void gemm_ctr_done(unsigned long long* ctr, unsigned 
   }
 }
 
+#ifndef NEGF_GEMM_MINB
+#define NEGF_GEMM_MINB 4  // resident CTAs per SM (A/B builds)
+#endif
 template <int WR, int WC, bool M3>
-__global__ void __launch_bounds__(128, 4) k_gemm(double2* arena, int64_t stride, int nE,
+__global__ void __launch_bounds__(128, NEGF_GEMM_MINB) k_gemm(double2* arena, int64_t stride, int nE,
                                                      const GemmTask* __restrict__ tasks,
                                                      const GemmTerm* __restrict__ terms,
                                                      const GemmTile* __restrict__ tiles, int tile_begin,
