@@ -1,7 +1,14 @@
 cd tools
-for s in sw:64x1x64x5 sw:64x1x64x6 sw:64x1x64x7; do echo -n "$s real: "; SW_REAL=1 INV_REAL=1 RG_SHAPE=$s ./inv_bench 64 326 256 0; done
-for s in sw:64x2x30x3 sw:64x1x60x5 sw:64x1x60x6; do echo -n "$s real: "; SW_REAL=1 INV_REAL=1 RG_SHAPE=$s ./inv_bench 60 326 256 0; done
-for s in sw:64x2x26x3 sw:64x1x52x5 sw:64x1x52x6; do echo -n "$s real: "; SW_REAL=1 INV_REAL=1 RG_SHAPE=$s ./inv_bench 52 326 256 0; done
-for s in sw:48x2x24x4 sw:64x1x48x6; do echo -n "$s real: "; SW_REAL=1 INV_REAL=1 RG_SHAPE=$s ./inv_bench 48 200 256 0; done
-for s in sw:48x2x20x4 sw:64x1x40x6 sw:64x1x40x8; do echo -n "$s real: "; SW_REAL=1 INV_REAL=1 RG_SHAPE=$s ./inv_bench 40 200 256 0; done
-for s in sw:48x2x20x4 sw:64x1x40x6 sw:64x1x40x8; do echo -n "$s real: "; SW_REAL=1 INV_REAL=1 RG_SHAPE=$s ./inv_bench 34 200 256 0; done
+for m in 64 60 56 52; do
+  INV_REAL=1 ./inv_bench $m 326 256 0
+  for s in sw2r:64x2x$((m/2))x3 ; do echo -n "  $s: "; INV_REAL=1 RG_SHAPE=$s ./inv_bench $m 326 256 0; done
+done
+echo -n "  sw2r:64x2x32x2: "; INV_REAL=1 RG_SHAPE=sw2r:64x2x32x2 ./inv_bench 64 326 256 0
+echo -n "  sw2r:64x4x16x2: "; INV_REAL=1 RG_SHAPE=sw2r:64x4x16x2 ./inv_bench 64 326 256 0
+echo -n "  odd nE sw2r:64x2x32x3: "; INV_REAL=1 RG_SHAPE=sw2r:64x2x32x3 ./inv_bench 64 326 255 0
+INV_REAL=1 ./inv_bench 48 200 256 0
+for s in sw2r:48x2x24x4 sw2r:48x2x24x5; do echo -n "  $s: "; INV_REAL=1 RG_SHAPE=$s ./inv_bench 48 200 256 0; done
+INV_REAL=1 ./inv_bench 40 200 256 0
+echo -n "  sw2r:48x2x20x5: "; INV_REAL=1 RG_SHAPE=sw2r:48x2x20x5 ./inv_bench 40 200 256 0
+INV_REAL=1 ./inv_bench 32 200 256 0
+for s in sw2r:32x1x32x8 sw2r:32x1x32x10 sw2r:32x2x16x12; do echo -n "  $s: "; INV_REAL=1 RG_SHAPE=$s ./inv_bench 32 200 256 0; done
