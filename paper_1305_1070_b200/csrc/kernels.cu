@@ -1347,182 +1347,6 @@ __global__ void __launch_bounds__(ROWS * H, MINB)
 }
 
 // ---------------------------------------------------------------------------
-// k_inverse_sw for real blocks, two energies of one task per CTA: the real
-// kernel is bound by the latency of the pivot chain (few FMAs per step), so
-// every warp runs the chains of two independent blocks side by side -- the
-// same instructions twice, interleaved.  Per block the arithmetic, the pivot
-// sequence and the singular rule are those of k_inverse_sw<.., true>; a
-// singular block is reported once and then ignored while its neighbour
-// finishes.
-// ---------------------------------------------------------------------------
-template <int ROWS, int H, int S, int MINB>
-__global__ void __launch_bounds__(ROWS * H, MINB)
-    k_inverse_sw2r(double2* arena, int64_t stride, const InvTask* __restrict__ tasks, int nE, int e_base,
-                   DevStatus* st) {
-  constexpr int NB = 2, NT = ROWS * H, NW = NT / 32, MW = H * S;
-  constexpr int PS = S | 1, PW = H * PS;
-  static_assert(NT % 32 == 0 && (H & (H - 1)) == 0 && H <= 32, "bad window inverse shape");
-  __shared__ double prow[NB][2][PW];
-  __shared__ InvCand cand[NB][2][NW];
-  __shared__ double red[NB][NW];
-  __shared__ int pos_of[NB][ROWS];
-  const InvTask tk = tasks[blockIdx.x];
-  const int m = tk.m;
-  const int e0 = blockIdx.y * NB;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, h = t & (H - 1), r = t / H;
-  const bool live = r < m;
-  double2* g[NB];
-  bool dead[NB];
-  double w[NB][S], thr2[NB], myip[NB];
-  int pos[NB];
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    dead[q] = e0 + q >= nE;  // odd batch: the last CTA has one block
-    g[q] = arena + int64_t(dead[q] ? e0 : e0 + q) * stride + tk.off;
-    double mx = 0.0;
-#pragma unroll
-    for (int j = 0; j < S; ++j) {
-      const int c = h * S + j;
-      w[q][j] = (live && c < m && !dead[q]) ? g[q][int64_t(r) * m + c].x : 0.0;
-      mx = fmax(mx, w[q][j] * w[q][j]);
-    }
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) red[q][warp] = mx;
-    pos[q] = r;
-    myip[q] = 1.0;
-  }
-  sw_barrier<NW>();
-#pragma unroll
-  for (int q = 0; q < NB; ++q) {
-    double mx = 0.0;
-#pragma unroll
-    for (int u = 0; u < NW; ++u) mx = fmax(mx, red[q][u]);
-    thr2[q] = 1e-26 * mx;  // (1e-13 max|a|)^2
-  }
-#pragma unroll 1
-  for (int k = 0; k < m; ++k) {
-    const int par = k & 1;
-    double f[NB], nx[NB], best[NB];
-    int bpos[NB], wl[NB];
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      f[q] = __shfl_sync(0xffffffffu, w[q][0], lane & ~(H - 1));
-      nx[q] = 0.0;
-      if constexpr (H > 1) nx[q] = __shfl_down_sync(0xffffffffu, w[q][0], 1);
-      best[q] = (live && h == 0 && pos[q] >= k) ? f[q] * f[q] : -1.0;
-      bpos[q] = (best[q] >= 0.0) ? pos[q] : 0x7fffffff;
-    }
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      const unsigned key = best[q] >= 0.0 ? __float_as_uint(__double2float_ru(best[q])) : 0u;
-      const unsigned kmax = __reduce_max_sync(0xffffffffu, key);
-      const unsigned tied = __ballot_sync(0xffffffffu, key == kmax && best[q] >= 0.0);
-      if (__popc(tied) <= 1) {
-        wl[q] = tied ? __ffs(tied) - 1 : 0;
-      } else {  // exact order among the lanes whose float images tie
-        double cb = (key == kmax) ? best[q] : -1.0;
-        int cp = (key == kmax) ? bpos[q] : 0x7fffffff, cl = lane;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, cb, o);
-          const int op = __shfl_xor_sync(0xffffffffu, cp, o);
-          const int ol = __shfl_xor_sync(0xffffffffu, cl, o);
-          if (ob > cb || (ob == cb && op < cp)) {
-            cb = ob;
-            cp = op;
-            cl = ol;
-          }
-        }
-        wl[q] = cl;
-      }
-    }
-    InvCand win[NB];
-    if constexpr (NW == 1) {
-#pragma unroll
-      for (int q = 0; q < NB; ++q) {
-        win[q].v = __shfl_sync(0xffffffffu, best[q], wl[q]);
-        win[q].pos = __shfl_sync(0xffffffffu, bpos[q], wl[q]);
-        win[q].row = __shfl_sync(0xffffffffu, r, wl[q]);
-        win[q].val.x = __shfl_sync(0xffffffffu, f[q], wl[q]);
-        win[q].val.y = 0.0;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < NB; ++q)
-        if (lane == wl[q]) cand[q][par][warp] = InvCand{best[q], bpos[q], r, make_double2(f[q], 0.0)};
-      __syncthreads();
-#pragma unroll
-      for (int q = 0; q < NB; ++q) {
-        win[q] = cand[q][par][0];
-#pragma unroll
-        for (int u = 1; u < NW; ++u) {
-          const InvCand o = cand[q][par][u];
-          if (o.v > win[q].v || (o.v == win[q].v && o.pos < win[q].pos)) win[q] = o;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      // |u_kk| <= 1e-13 max|a| (uniform across the CTA): report once, then the block is dead
-      if (!(win[q].v > thr2[q]) && win[q].v == win[q].v && !dead[q]) {
-        if (t == 0) report_singular(st, e_base + e0 + q, tk.fold_pos, k);
-        dead[q] = true;
-      }
-    }
-    if (dead[0] && dead[1]) return;
-    double fs[NB], last[NB];
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      if (t == 0) pos_of[q][k] = win[q].row;
-      double ip;
-      sw_recip(ip, win[q].val);
-      const bool pivot_row = r == win[q].row;
-      // the incoming column at the right end: the next chunk's first column,
-      // or (last chunk) the unit column of the pivot row
-      last[q] = pivot_row ? 1.0 : 0.0;
-      if constexpr (H > 1) {
-        if (h != H - 1) last[q] = nx[q];
-      }
-      if (pivot_row) {
-        double* d = &prow[q][par][h * PS];
-#pragma unroll
-        for (int j = 1; j < S; ++j) d[j - 1] = w[q][j];
-        d[S - 1] = last[q];
-        myip[q] = ip;
-      }
-      fs[q] = pivot_row ? 0.0 : f[q] * ip;
-      const int p = win[q].pos;
-      if (pos[q] == k) pos[q] = p;
-      else if (pos[q] == p) pos[q] = k;
-    }
-    sw_barrier<NW>();
-#pragma unroll
-    for (int j = 1; j < S; ++j) {
-#pragma unroll
-      for (int q = 0; q < NB; ++q) w[q][j - 1] = fma(-fs[q], prow[q][par][h * PS + j - 1], w[q][j]);
-    }
-#pragma unroll
-    for (int q = 0; q < NB; ++q) w[q][S - 1] = fma(-fs[q], prow[q][par][h * PS + S - 1], last[q]);
-  }
-  // row k of the inverse is the physical pivot row of step k (final position
-  // pos = k), scaled by its 1 / pivot; the column made at step c is the
-  // original column pos_of[c] (see k_inverse_sw)
-  __syncthreads();
-  if (live) {
-    const int shift = MW - m;
-#pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      if (dead[q]) continue;
-#pragma unroll
-      for (int j = 0; j < S; ++j) {
-        const int c = h * S + j - shift;
-        if (c >= 0) g[q][int64_t(pos[q]) * m + pos_of[q][c]] = make_double2(w[q][j] * myip[q], 0.0);
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Multi-CTA blocked Gauss-Jordan for large blocks (m > kSmemInvMax), see
 // plan.hpp: per kPanel-column inner panel, k_bigpanel (one CTA per block and
 // energy) factors the panel with row partial pivoting (in shared memory, or
@@ -2397,25 +2221,9 @@ static int sw_window(int m) {
 // <ROWS, H, S, MINB>: the complex instantiation; <ROWS, HR, SR, MINR>: the real
 // one (a real block needs half the registers: 49..64-wide real blocks run with
 // one thread per row, 8.8 vs 10.6 ms for 326 x 256 blocks of 64).
-// Real blocks of 49..64: two energies per CTA (k_inverse_sw2r) when
-// NEGF_SW2R=1 (A/B switch).
-static bool sw_two_per_cta() {
-  static const bool on = [] {
-    const char* e = std::getenv("NEGF_SW2R");
-    return e && std::atoi(e) != 0;
-  }();
-  return on;
-}
 template <int ROWS, int H, int S, int MINB, int HR, int SR, int MINR>
 static void launch_sw(dim3 grid, const BatchArgs& b, const InvTask* dt, DevStatus* st, cudaStream_t s, bool real) {
   static_assert(H * S == HR * SR, "same window for both value types");
-  if constexpr (ROWS == 64 && H == 2) {
-    if (real && sw_two_per_cta()) {
-      k_inverse_sw2r<ROWS, H, S, 3><<<dim3(grid.x, (b.nE + 1) / 2), ROWS * H, 0, s>>>(b.arena, b.stride, dt, b.nE,
-                                                                                     b.e_base, st);
-      return;
-    }
-  }
   if (real) k_inverse_sw<ROWS, HR, SR, MINR, true><<<grid, ROWS * HR, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
   else k_inverse_sw<ROWS, H, S, MINB, false><<<grid, ROWS * H, 0, s>>>(b.arena, b.stride, dt, b.e_base, st);
 }

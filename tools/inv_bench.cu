@@ -60,11 +60,6 @@ int main(int argc, char** argv) {
     SWV(48, 2, 20, 4) SWV(48, 2, 24, 4) SWV(48, 2, 24, 5) SWV(48, 4, 12, 4) SWV(48, 4, 12, 5) SWV(64, 1, 48, 2) SWV(64, 1, 48, 3) SWV(64, 1, 64, 3) SWV(64, 1, 64, 4) SWV(64, 1, 64, 5) SWV(64, 1, 64, 6) SWV(64, 1, 64, 7) SWV(64, 1, 56, 5) SWV(64, 1, 52, 5) SWV(64, 1, 52, 6) SWV(64, 1, 60, 5) SWV(64, 1, 60, 6) SWV(64, 1, 48, 6) SWV(64, 1, 40, 6) SWV(64, 1, 40, 8)
     SWV(64, 2, 28, 2) SWV(64, 2, 32, 2) SWV(64, 2, 32, 3) SWV(64, 4, 16, 2) SWV(64, 4, 16, 3) SWV(64, 4, 16, 4)
     SWV(96, 4, 24, 1) SWV(112, 4, 28, 1) SWV(104, 4, 25, 1) SWV(128, 4, 28, 1) SWV(80, 4, 20, 1) SWV(80, 4, 19, 1) SWV(80, 4, 20, 2) SWV(104, 4, 26, 1) SWV(104, 8, 13, 1) SWV(80, 2, 38, 1) SWV(112, 8, 14, 1) SWV(128, 8, 15, 1)
-    // two real blocks per CTA: sw2r:ROWSxHxSxMINB (needs INV_REAL=1)
-#define SW2(R, HH, SS, MB) else if (!strcmp(shape, "sw2r:" #R "x" #HH "x" #SS "x" #MB)) \
-      k_inverse_sw2r<R, HH, SS, MB><<<dim3(nb, (nE + 1) / 2), R * HH>>>(arena, stride, dt, nE, 0, st);
-    SW2(64, 2, 32, 2) SW2(64, 2, 32, 3) SW2(64, 2, 28, 3) SW2(64, 2, 26, 3) SW2(64, 2, 30, 3) SW2(64, 4, 16, 2) SW2(64, 4, 16, 3)
-    SW2(48, 2, 24, 4) SW2(48, 2, 24, 5) SW2(48, 2, 20, 5) SW2(32, 1, 32, 8) SW2(32, 1, 32, 10) SW2(32, 2, 16, 12)
     else { printf("unknown RG_SHAPE %s\n", shape); return 1; }
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
