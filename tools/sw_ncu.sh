@@ -8,4 +8,4 @@ cap() { name=$1; m=$2; shape=$3
   python ncu_summary.py /tmp/$name.ncu-rep > ../gpurun_out/ncu_sw/$name.summary.txt 2>&1
 }
 cap sw64 64 sw:64x2x32x3
-cap swr64 64 swr:4x16x8x8x2
+cap sw32 32 sw:32x1x32x10
